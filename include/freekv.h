@@ -1,0 +1,174 @@
+/*
+ * freekv.h -- C ABI of the B200-native FreeKV decode-step KV-retrieval path
+ * (arXiv 2505.13109).  C99-compatible; no CUDA or torch types in signatures.
+ *
+ * Notation (§2.1): nb batch rows, n_qo attention heads,
+ * n_kv KV heads, G = n_qo / n_kv, d head dim, p page size, budget B
+ * tokens with S sink and W window tokens kept, K = (B - S - W) / p selectable
+ * pages per unit (reading A-6).  A "unit" is one (batch row, KV head)
+ * pair, u = b * n_kv + m; all per-unit arrays are u-major.
+ *
+ * Memory: the caller owns all large memory.  `dev` is one device allocation
+ * (e.g. a torch.uint8 CUDA tensor) of freekv_query_sizes()->dev_bytes; `host`
+ * is one pinned, device-mapped host allocation (torch pin_memory tensor /
+ * cudaHostAlloc) of host_bytes -- the CPU KV pool of P:297 in the combined
+ * HND layout (n_page, n_kv, 2, p, d) of P:318.  Both must outlive the handle.
+ * Streams are cudaStream_t passed as void*; NULL selects the handle's compute
+ * stream.  All bf16 tensors are raw 16-bit patterns.
+ *
+ * Errors: every call returns FREEKV_OK (0) or a negative status; the message
+ * of the last failure on the calling thread is freekv_last_error().  Calls are
+ * asynchronous and stream-ordered; asynchronous CUDA faults surface as
+ * FREEKV_ECUDA on a later call or freekv_synchronize().  No call allocates
+ * device memory after freekv_init and none blocks the host except the
+ * freekv_get_* inspection calls and freekv_synchronize.
+ */
+#ifndef FREEKV_H
+#define FREEKV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FREEKV_ABI_VERSION 1
+
+typedef int32_t freekv_status;
+enum {
+    FREEKV_OK = 0,
+    FREEKV_EINVAL = -1,        /* invalid argument / violated config invariant */
+    FREEKV_ENOMEM = -2,        /* buffer smaller than freekv_query_sizes() */
+    FREEKV_ECUDA = -3,         /* CUDA runtime error (possibly from earlier async work) */
+    FREEKV_ENCCL = -4,         /* reserved: collective failure */
+    FREEKV_ESTATE = -5,        /* call out of order / handle in wrong state */
+    FREEKV_ERANGE = -6,        /* context would exceed max_ctx_tokens */
+    FREEKV_EUNSUPPORTED = -7   /* head_dim != 128, page_size not in {16,32,64}, G > 8 */
+};
+
+/* Correction modes, P:661-665 (Table tab:abl-tau): tau = 0 "No Correction",
+ * tau = 1 "No Speculation".  SPECULATIVE flags a unit iff mean_g C < tau
+ * (P:247-250), with tau <= 0 never and tau >= 1 always (reading A-13). */
+enum { FREEKV_MODE_SPECULATIVE = 0, FREEKV_MODE_ALWAYS_CORRECT = 1, FREEKV_MODE_NEVER_CORRECT = 2 };
+
+typedef struct freekv_config {
+    int32_t n_layers;        /* layers served by this handle */
+    int32_t batch;           /* nb: batch rows on this GPU */
+    int32_t n_qo, n_kv;      /* heads on this GPU; G = n_qo / n_kv <= 8 */
+    int32_t head_dim;        /* d, must be 128 */
+    int32_t page_size;       /* p in {16, 32, 64} (P:557 uses 32) */
+    int32_t budget_tokens;   /* B */
+    int32_t sink_tokens;     /* S, multiple of p (A-7) */
+    int32_t window_tokens;   /* W, multiple of p (A-7) */
+    int32_t max_ctx_tokens;  /* capacity of the host pool per sequence */
+    float tau;               /* correction threshold */
+    int32_t mode;            /* FREEKV_MODE_* */
+    int32_t first_layer_dense; /* must be 0 in ABI v1 (P:560 layer-0 exemption is served outside) */
+    /* multi-GPU shard description; informational in ABI v1 */
+    int32_t kv_head_begin, kv_head_end, batch_begin, batch_end;
+    int32_t n_ranks, rank;
+} freekv_config;
+
+typedef struct freekv_buffers {
+    void* dev;          /* device arena, >= dev_bytes, 256-byte aligned */
+    size_t dev_bytes;
+    void* host;         /* pinned, device-mapped host pool, >= host_bytes, 4 KiB aligned */
+    size_t host_bytes;
+} freekv_buffers;
+
+typedef struct freekv_handle freekv_handle;
+
+/* Sizes of the two caller-owned buffers for `cfg`.  Validates cfg. */
+freekv_status freekv_query_sizes(const freekv_config* cfg, size_t* dev_bytes, size_t* host_bytes);
+
+/* Create a handle over caller buffers.  compute_stream: stream of decode_step;
+ * recall_stream: dedicated stream for background recall.  Zeroes
+ * the device arena (stream-ordered on compute_stream). */
+freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs,
+                          void* compute_stream, void* recall_stream, freekv_handle** out);
+
+/* O-1 / row a9: append n_new tokens to every sequence of `layer`.
+ * k, v: device bf16 [nb][n_new][n_kv][d] (NHD, the natural projection layout,
+ * P:304-305).  Writes sink/local device pages; every page that leaves the
+ * window (page < n_off = max(S/p, floor(Lc/p) - W/p)) gets its channel-wise
+ * min/max summary and is stored to the host pool as one (2,p,d) page
+ * (the NHD->HND transpose at offload).  n_new > 1 (prefill) restarts
+ * speculation (reading R-9).  ERANGE if the context would exceed max_ctx. */
+freekv_status freekv_append_kv(freekv_handle* h, int32_t layer, const void* k, const void* v,
+                               int32_t n_new, void* stream);
+
+/* Rebuild the summaries of pages [page_begin, page_end) of every unit of
+ * `layer` from the host pool.  Pages must already be offloaded. */
+freekv_status freekv_summarize_pages(freekv_handle* h, int32_t layer, int32_t page_begin,
+                                     int32_t page_end, void* stream);
+
+/* Rows a1-a4: correction flags (vs the stored q_{i-1}) and the
+ * selection S_i with q_i for every unit: page scores (Quest bound,
+ * P:231), per-head softmax + MeanS group pooling, top-K with
+ * lowest-id ties, delta vs the resident set.  The result is pending:
+ * it changes neither the resident set nor q_prev.
+ * q: device bf16 [nb][n_qo][d].  pages_out (nullable): device int32
+ * [nb][n_kv][K], ascending, -1 padded.  corrected_out (nullable): device
+ * uint8 [nb][n_kv]. */
+freekv_status freekv_select_pages(freekv_handle* h, int32_t layer, const void* q,
+                                  int32_t* pages_out, uint8_t* corrected_out, void* stream);
+
+/* Rows a5/a6: recall the pending selection's missing pages (S_i minus
+ * resident, reading A-18) from the host pool into free cache slots.  Units
+ * whose correction flag is set are recalled synchronously on `stream` (before
+ * attention); the others are recalled in the background on the recall
+ * stream for use at the next step.  sync_mask must be NULL
+ * in ABI v1 (the flags of select_pages are used). */
+freekv_status freekv_recall_pages(freekv_handle* h, int32_t layer, const uint8_t* sync_mask,
+                                  void* stream);
+
+/* Row a7 + a8: sparse decode attention: for each q head of unit u
+ * o = softmax(q K_T^T / sqrt(d)) V_T over T = sink tokens U pages U local
+ * region (reading A-9), with pages = S_i for corrected units and the resident
+ * set otherwise.  out: device fp32 [nb][n_qo][d].  Then commits
+ * the speculative advance: resident := S_i, q_prev := q. */
+freekv_status freekv_sparse_decode_attn(freekv_handle* h, int32_t layer, const void* q, float* out,
+                                        void* stream);
+
+/* The composite decode step of one layer on the compute stream:
+ * append_kv(1 token) -> select_pages -> recall_pages -> sparse_decode_attn.
+ * q: [nb][n_qo][d], k_new/v_new: [nb][1][n_kv][d] bf16; out: fp32 [nb][n_qo][d]. */
+freekv_status freekv_decode_step(freekv_handle* h, int32_t layer, const void* q, const void* k_new,
+                                 const void* v_new, float* out);
+
+/* Inspection (blocking; host outputs).  All arrays u-major. */
+freekv_status freekv_get_selection(freekv_handle* h, int32_t layer, int32_t* pages /*[U][K]*/,
+                                   int32_t* frontier /*[U]*/, uint8_t* flags /*[U]*/, float* cbar /*[U]*/);
+freekv_status freekv_get_resident(freekv_handle* h, int32_t layer, int32_t* pages /*[U][K]*/,
+                                  int32_t* frontier /*[U]*/);
+freekv_status freekv_get_fetch(freekv_handle* h, int32_t layer, int32_t* n_fetch /*[U]*/,
+                               int32_t* fetch_pages /*[U][K]*/);
+/* Summaries of pages [page_begin, page_end) of unit u as [n][2][d] bf16 (min, max). */
+freekv_status freekv_get_summaries(freekv_handle* h, int32_t layer, int32_t unit, int32_t page_begin,
+                                   int32_t page_end, uint16_t* out);
+freekv_status freekv_get_context(freekv_handle* h, int32_t layer, int32_t* ctx_tokens);
+/* Numbers a caller needs to size its own tensors. */
+freekv_status freekv_get_dims(freekv_handle* h, int32_t* K, int32_t* n_page_max, int32_t* units);
+
+/* Per-kernel device timing for roofline reporting: while profiling is on,
+ * every kernel launch of the handle is bracketed by CUDA events on the stream
+ * it is launched on (at most max_launches launches are recorded).
+ * profile_end synchronises and returns, per kernel class, the summed device
+ * milliseconds and the launch count.  Classes: 0 append, 1 score, 2 select
+ * finalize, 3 synchronous recall, 4 background recall, 5 attention split,
+ * 6 attention combine + commit. */
+#define FREEKV_NUM_KERNEL_CLASSES 7
+freekv_status freekv_profile_begin(freekv_handle* h, int32_t max_launches);
+freekv_status freekv_profile_end(freekv_handle* h, float* ms /*[7]*/, int32_t* launches /*[7]*/);
+
+/* Wait for all work of the handle (both streams); surfaces async errors. */
+freekv_status freekv_synchronize(freekv_handle* h);
+void freekv_destroy(freekv_handle* h);
+const char* freekv_last_error(void);
+int32_t freekv_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FREEKV_H */

@@ -1,0 +1,527 @@
+// api.cu -- the C ABI of include/freekv.h: handle, config validation, arena
+// layout, stream/event choreography of the per-layer decode step.
+//
+// Per layer l, step i (SURVEY §8(a) choreography):
+//   compute stream:  wait(recall_done[l]) -> append -> score -> finalize
+//                    -> recall(sync, flagged units) -> record(select_done[l])
+//                    -> attention split -> combine + commit
+//   recall stream:   wait(select_done[l]) -> recall(background, unflagged units)
+//                    -> record(recall_done[l])
+// Background recall of layer l overlaps the rest of step i and the start of
+// step i+1 (PAPER.md P:221-225 speculative retrieval; P:320-324 streamed
+// recall).  No host synchronisation on the path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/freekv.h"
+#include "fkv_internal.cuh"
+
+using namespace fkv;
+
+static thread_local std::string g_last_error;
+
+static freekv_status fail(freekv_status st, const std::string& msg) {
+    g_last_error = msg;
+    return st;
+}
+
+#define FKV_CUDA(call)                                                                              \
+    do {                                                                                            \
+        cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess)                                                                      \
+            return fail(FREEKV_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));          \
+    } while (0)
+
+struct freekv_handle {
+    freekv_config cfg;
+    FkvDims D;
+    std::vector<FkvLayer> layers;
+    FkvScratch X;
+    cudaStream_t cs = nullptr, rs = nullptr;
+    std::vector<cudaEvent_t> ev_select, ev_recall;
+    std::vector<int> ctx_host;
+    std::vector<int> recall_pending;
+    int lpt = 1;  // leaves per thread of the finalize tree (fixed per handle, CFR-6)
+    // profiling (freekv_profile_begin/end)
+    bool prof = false;
+    std::vector<cudaEvent_t> prof_pool;
+    size_t prof_used = 0;
+    struct Rec { int cls; cudaEvent_t a, b; };
+    std::vector<Rec> prof_recs;
+};
+
+namespace {
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
+
+struct Sizes {
+    size_t layer_bytes, scratch_bytes, dev_bytes, host_layer_bytes, host_bytes;
+    // offsets inside one layer block
+    size_t o_summ, o_sink, o_slots, o_ring, o_qprev, o_res_pages, o_res_slot, o_res_front, o_res_valid,
+        o_pend_pages, o_pend_slot, o_pend_front, o_flags, o_cbar, o_fetch_page, o_fetch_slot, o_n_fetch, o_ctx,
+        o_n_off;
+    size_t o_scores, o_part_o, o_part_ml;
+};
+
+freekv_status validate(const freekv_config* c, FkvDims* D) {
+    if (!c) return fail(FREEKV_EINVAL, "config is NULL");
+    if (c->n_layers <= 0 || c->batch <= 0 || c->n_qo <= 0 || c->n_kv <= 0)
+        return fail(FREEKV_EINVAL, "n_layers, batch, n_qo, n_kv must be positive");
+    if (c->n_qo % c->n_kv != 0) return fail(FREEKV_EINVAL, "n_qo % n_kv != 0 (GQA group size G = n_qo/n_kv, P:98)");
+    if (c->head_dim != kHeadDim) return fail(FREEKV_EUNSUPPORTED, "head_dim must be 128");
+    if (!(c->page_size == 16 || c->page_size == 32 || c->page_size == 64))
+        return fail(FREEKV_EUNSUPPORTED, "page_size must be 16, 32 or 64");
+    const int G = c->n_qo / c->n_kv;
+    if (G > kMaxG) return fail(FREEKV_EUNSUPPORTED, "group size G > 8");
+    const int p = c->page_size;
+    if (c->sink_tokens < 0 || c->window_tokens < 0) return fail(FREEKV_EINVAL, "sink/window must be >= 0");
+    if (c->sink_tokens % p) return fail(FREEKV_EINVAL, "sink_tokens % page_size != 0 (reading A-7)");
+    if (c->window_tokens % p) return fail(FREEKV_EINVAL, "window_tokens % page_size != 0 (reading A-7)");
+    if (c->budget_tokens < c->sink_tokens + c->window_tokens)
+        return fail(FREEKV_EINVAL, "budget < sink + window (P:101)");
+    if ((c->budget_tokens - c->sink_tokens - c->window_tokens) % p)
+        return fail(FREEKV_EINVAL, "(budget - sink - window) % page_size != 0 (K = (B-S-W)/p, reading A-6)");
+    const int K = (c->budget_tokens - c->sink_tokens - c->window_tokens) / p;
+    if (K < 1 || K > 256) return fail(FREEKV_EUNSUPPORTED, "K = (B-S-W)/p must be in [1, 256]");
+    if (c->max_ctx_tokens <= 0) return fail(FREEKV_EINVAL, "max_ctx_tokens must be positive");
+    const int n_page_host = c->max_ctx_tokens / p + 1;
+    if (n_page_host > 8192) return fail(FREEKV_EUNSUPPORTED, "max_ctx_tokens / page_size > 8191 pages");
+    if (!(c->mode == 0 || c->mode == 1 || c->mode == 2)) return fail(FREEKV_EINVAL, "mode must be 0, 1 or 2");
+    if (!std::isfinite(c->tau)) return fail(FREEKV_EINVAL, "tau must be finite");
+    if (c->first_layer_dense) return fail(FREEKV_EUNSUPPORTED, "first_layer_dense is not served by ABI v1");
+    FkvDims d{};
+    d.nb = c->batch;
+    d.n_qo = c->n_qo;
+    d.n_kv = c->n_kv;
+    d.G = G;
+    d.d = kHeadDim;
+    d.p = p;
+    d.K = K;
+    d.n_sink = c->sink_tokens / p;
+    d.n_win = c->window_tokens / p;
+    d.S_tok = c->sink_tokens;
+    d.R_loc = d.n_win + 2;
+    d.n_page_host = n_page_host;
+    d.n_page_max = (n_page_host + 127) / 128 * 128;
+    d.max_ctx = c->max_ctx_tokens;
+    d.U = c->batch * c->n_kv;
+    d.mode = c->mode;
+    d.tau = c->tau;
+    d.score_r = (float)(1.4426950408889634074 / std::sqrt((double)kHeadDim));  // CFR-3
+    d.attn_c = (float)(1.4426950408889634074 / std::sqrt((double)kHeadDim));
+    d.pages_per_chunk = 2;
+    const int p_max = d.n_sink + K + d.R_loc;
+    d.n_chunks = (p_max + d.pages_per_chunk - 1) / d.pages_per_chunk;
+    *D = d;
+    return FREEKV_OK;
+}
+
+Sizes compute_sizes(const freekv_config* c, const FkvDims& D) {
+    Sizes s{};
+    const size_t U = D.U, K = D.K, pe_b = page_elems(D) * 2;
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        size_t at = o;
+        o = align_up(o + bytes);
+        return at;
+    };
+    s.o_summ = take(U * D.n_page_max * 2 * D.d * 2);
+    s.o_sink = take(U * D.n_sink * pe_b);
+    s.o_slots = take(U * 2 * K * pe_b);
+    s.o_ring = take(U * D.R_loc * pe_b);
+    s.o_qprev = take((size_t)D.nb * D.n_qo * D.d * 2);
+    s.o_res_pages = take(U * K * 4);
+    s.o_res_slot = take(U * K * 4);
+    s.o_res_front = take(U * 4);
+    s.o_res_valid = take(U * 4);
+    s.o_pend_pages = take(U * K * 4);
+    s.o_pend_slot = take(U * K * 4);
+    s.o_pend_front = take(U * 4);
+    s.o_flags = take(U);
+    s.o_cbar = take(U * 4);
+    s.o_fetch_page = take(U * K * 4);
+    s.o_fetch_slot = take(U * K * 4);
+    s.o_n_fetch = take(U * 4);
+    s.o_ctx = take(U * 4);
+    s.o_n_off = take(U * 4);
+    s.layer_bytes = o;
+    o = 0;
+    s.o_scores = take(U * D.G * D.n_page_max * 4);
+    s.o_part_o = take(U * D.n_chunks * D.G * D.d * 4);
+    s.o_part_ml = take(U * D.n_chunks * D.G * 2 * 4);
+    s.scratch_bytes = o;
+    s.dev_bytes = s.layer_bytes * c->n_layers + s.scratch_bytes;
+    s.host_layer_bytes = (size_t)D.nb * D.n_page_host * D.n_kv * pe_b;
+    s.host_bytes = s.host_layer_bytes * c->n_layers;
+    return s;
+}
+
+freekv_status check_layer(freekv_handle* h, int layer) {
+    if (!h) return fail(FREEKV_EINVAL, "handle is NULL");
+    if (layer < 0 || layer >= h->cfg.n_layers) return fail(FREEKV_EINVAL, "layer out of range");
+    return FREEKV_OK;
+}
+
+cudaStream_t pick(freekv_handle* h, void* s) { return s ? (cudaStream_t)s : h->cs; }
+
+int max_n_off(const FkvDims& D, int ctx) { return std::max(D.n_sink, ctx / D.p - D.n_win); }
+
+enum { K_APPEND = 0, K_SCORE, K_FINALIZE, K_RECALL_SYNC, K_RECALL_BG, K_ATTN_SPLIT, K_ATTN_COMBINE };
+
+template <class F>
+cudaError_t timed(freekv_handle* h, int cls, cudaStream_t s, F&& launch) {
+    if (!h->prof || h->prof_used + 2 > h->prof_pool.size()) return launch();
+    cudaEvent_t a = h->prof_pool[h->prof_used++], b = h->prof_pool[h->prof_used++];
+    cudaError_t e = cudaEventRecord(a, s);
+    if (e == cudaSuccess) e = launch();
+    if (e == cudaSuccess) e = cudaEventRecord(b, s);
+    h->prof_recs.push_back({cls, a, b});
+    return e;
+}
+
+freekv_status do_append(freekv_handle* h, int layer, const void* k, const void* v, int n_new, cudaStream_t s) {
+    if (!k || !v) return fail(FREEKV_EINVAL, "k/v is NULL");
+    if (n_new <= 0) return fail(FREEKV_EINVAL, "n_new must be positive");
+    if (h->ctx_host[layer] + n_new > h->D.max_ctx)
+        return fail(FREEKV_ERANGE, "context would exceed max_ctx_tokens");
+    if (h->recall_pending[layer]) FKV_CUDA(cudaStreamWaitEvent(s, h->ev_recall[layer], 0));
+    FKV_CUDA(timed(h, K_APPEND, s, [&] {
+        return launch_append(h->D, h->layers[layer], (const uint16_t*)k, (const uint16_t*)v, n_new, s);
+    }));
+    h->ctx_host[layer] += n_new;
+    return FREEKV_OK;
+}
+
+freekv_status do_select(freekv_handle* h, int layer, const void* q, int32_t* pages_out, uint8_t* corr_out,
+                        cudaStream_t s) {
+    if (!q) return fail(FREEKV_EINVAL, "q is NULL");
+    if (h->ctx_host[layer] <= 0) return fail(FREEKV_ESTATE, "select before any token was appended");
+    // the background recall of the previous step reads this layer's fetch list
+    if (h->recall_pending[layer]) FKV_CUDA(cudaStreamWaitEvent(s, h->ev_recall[layer], 0));
+    const int mno = max_n_off(h->D, h->ctx_host[layer]);
+    if (mno - h->D.n_sink > h->D.K)
+        FKV_CUDA(timed(h, K_SCORE, s, [&] {
+            return launch_score(h->D, h->layers[layer], h->X, (const uint16_t*)q, mno, s);
+        }));
+    FKV_CUDA(timed(h, K_FINALIZE, s, [&] {
+        return launch_finalize(h->D, h->layers[layer], h->X, (const uint16_t*)q, pages_out, corr_out, h->lpt, s);
+    }));
+    return FREEKV_OK;
+}
+
+freekv_status do_recall(freekv_handle* h, int layer, cudaStream_t s) {
+    FKV_CUDA(timed(h, K_RECALL_SYNC, s, [&] { return launch_recall(h->D, h->layers[layer], 1, s); }));
+    FKV_CUDA(cudaEventRecord(h->ev_select[layer], s));
+    FKV_CUDA(cudaStreamWaitEvent(h->rs, h->ev_select[layer], 0));
+    FKV_CUDA(timed(h, K_RECALL_BG, h->rs, [&] { return launch_recall(h->D, h->layers[layer], 0, h->rs); }));
+    FKV_CUDA(cudaEventRecord(h->ev_recall[layer], h->rs));
+    h->recall_pending[layer] = 1;
+    return FREEKV_OK;
+}
+
+freekv_status do_attn(freekv_handle* h, int layer, const void* q, float* out, cudaStream_t s) {
+    if (!q || !out) return fail(FREEKV_EINVAL, "q/out is NULL");
+    FKV_CUDA(timed(h, K_ATTN_SPLIT, s, [&] {
+        return launch_attn_split(h->D, h->layers[layer], h->X, (const uint16_t*)q, s);
+    }));
+    FKV_CUDA(timed(h, K_ATTN_COMBINE, s, [&] {
+        return launch_attn_combine(h->D, h->layers[layer], h->X, (const uint16_t*)q, out, s);
+    }));
+    return FREEKV_OK;
+}
+
+freekv_status sync_both(freekv_handle* h) {
+    FKV_CUDA(cudaStreamSynchronize(h->cs));
+    FKV_CUDA(cudaStreamSynchronize(h->rs));
+    return FREEKV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t freekv_abi_version(void) { return FREEKV_ABI_VERSION; }
+
+const char* freekv_last_error(void) { return g_last_error.c_str(); }
+
+freekv_status freekv_query_sizes(const freekv_config* cfg, size_t* dev_bytes, size_t* host_bytes) {
+    FkvDims D;
+    freekv_status st = validate(cfg, &D);
+    if (st != FREEKV_OK) return st;
+    Sizes s = compute_sizes(cfg, D);
+    if (dev_bytes) *dev_bytes = s.dev_bytes;
+    if (host_bytes) *host_bytes = s.host_bytes;
+    return FREEKV_OK;
+}
+
+freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, void* compute_stream,
+                          void* recall_stream, freekv_handle** out) {
+    if (!out) return fail(FREEKV_EINVAL, "out is NULL");
+    *out = nullptr;
+    FkvDims D;
+    freekv_status st = validate(cfg, &D);
+    if (st != FREEKV_OK) return st;
+    if (!bufs || !bufs->dev || !bufs->host) return fail(FREEKV_EINVAL, "buffers are NULL");
+    Sizes s = compute_sizes(cfg, D);
+    if (bufs->dev_bytes < s.dev_bytes) return fail(FREEKV_ENOMEM, "device arena smaller than freekv_query_sizes()");
+    if (bufs->host_bytes < s.host_bytes) return fail(FREEKV_ENOMEM, "host pool smaller than freekv_query_sizes()");
+    if ((uintptr_t)bufs->dev % kAlign) return fail(FREEKV_EINVAL, "device arena must be 256-byte aligned");
+    if ((uintptr_t)bufs->host % 16) return fail(FREEKV_EINVAL, "host pool must be 16-byte aligned");
+    void* host_dev = nullptr;
+    cudaError_t e = cudaHostGetDevicePointer(&host_dev, bufs->host, 0);
+    if (e != cudaSuccess)
+        return fail(FREEKV_EINVAL, std::string("host pool is not pinned/device-mapped: ") + cudaGetErrorString(e));
+
+    freekv_handle* h = new freekv_handle();
+    h->cfg = *cfg;
+    h->D = D;
+    h->cs = (cudaStream_t)compute_stream;
+    h->rs = (cudaStream_t)recall_stream;
+    if (!h->rs || h->rs == h->cs) {
+        delete h;
+        return fail(FREEKV_EINVAL, "recall_stream must be a distinct non-NULL stream");
+    }
+    uint8_t* dev = (uint8_t*)bufs->dev;
+    uint8_t* hd = (uint8_t*)host_dev;
+    h->layers.resize(cfg->n_layers);
+    for (int l = 0; l < cfg->n_layers; ++l) {
+        uint8_t* base = dev + s.layer_bytes * l;
+        FkvLayer& L = h->layers[l];
+        L.summ = (uint16_t*)(base + s.o_summ);
+        L.sink = (uint16_t*)(base + s.o_sink);
+        L.slots = (uint16_t*)(base + s.o_slots);
+        L.ring = (uint16_t*)(base + s.o_ring);
+        L.q_prev = (uint16_t*)(base + s.o_qprev);
+        L.res_pages = (int32_t*)(base + s.o_res_pages);
+        L.res_slot = (int32_t*)(base + s.o_res_slot);
+        L.res_front = (int32_t*)(base + s.o_res_front);
+        L.res_valid = (int32_t*)(base + s.o_res_valid);
+        L.pend_pages = (int32_t*)(base + s.o_pend_pages);
+        L.pend_slot = (int32_t*)(base + s.o_pend_slot);
+        L.pend_front = (int32_t*)(base + s.o_pend_front);
+        L.flags = (uint8_t*)(base + s.o_flags);
+        L.cbar = (float*)(base + s.o_cbar);
+        L.fetch_page = (int32_t*)(base + s.o_fetch_page);
+        L.fetch_slot = (int32_t*)(base + s.o_fetch_slot);
+        L.n_fetch = (int32_t*)(base + s.o_n_fetch);
+        L.ctx = (int32_t*)(base + s.o_ctx);
+        L.n_off = (int32_t*)(base + s.o_n_off);
+        L.host = (uint16_t*)(hd + s.host_layer_bytes * l);
+    }
+    uint8_t* sb = dev + s.layer_bytes * cfg->n_layers;
+    h->X.scores = (float*)(sb + s.o_scores);
+    h->X.part_o = (float*)(sb + s.o_part_o);
+    h->X.part_ml = (float*)(sb + s.o_part_ml);
+    {
+        int P2 = 1;
+        while (P2 < D.n_page_host) P2 <<= 1;
+        h->lpt = P2 <= 1024 ? 1 : P2 / 1024;
+    }
+    h->ctx_host.assign(cfg->n_layers, 0);
+    h->recall_pending.assign(cfg->n_layers, 0);
+    h->ev_select.resize(cfg->n_layers);
+    h->ev_recall.resize(cfg->n_layers);
+    for (int l = 0; l < cfg->n_layers; ++l) {
+        if (cudaEventCreateWithFlags(&h->ev_select[l], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->ev_recall[l], cudaEventDisableTiming) != cudaSuccess) {
+            freekv_destroy(h);
+            return fail(FREEKV_ECUDA, "cudaEventCreate failed");
+        }
+    }
+    e = cudaMemsetAsync(dev, 0, s.dev_bytes, h->cs);
+    std::vector<int32_t> n_off(D.U, D.n_sink);
+    for (int l = 0; l < cfg->n_layers && e == cudaSuccess; ++l)
+        e = cudaMemcpyAsync(h->layers[l].n_off, n_off.data(), D.U * 4, cudaMemcpyHostToDevice, h->cs);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->cs);
+    if (e != cudaSuccess) {
+        freekv_destroy(h);
+        return fail(FREEKV_ECUDA, std::string("arena init: ") + cudaGetErrorString(e));
+    }
+    *out = h;
+    return FREEKV_OK;
+}
+
+freekv_status freekv_append_kv(freekv_handle* h, int32_t layer, const void* k, const void* v, int32_t n_new,
+                               void* stream) {
+    freekv_status st = check_layer(h, layer);
+    if (st != FREEKV_OK) return st;
+    return do_append(h, layer, k, v, n_new, pick(h, stream));
+}
+
+freekv_status freekv_summarize_pages(freekv_handle* h, int32_t layer, int32_t page_begin, int32_t page_end,
+                                     void* stream) {
+    freekv_status st = check_layer(h, layer);
+    if (st != FREEKV_OK) return st;
+    const int n_off = max_n_off(h->D, h->ctx_host[layer]);
+    if (page_begin < 0 || page_end > n_off || page_begin > page_end)
+        return fail(FREEKV_ERANGE, "pages must lie in [0, n_off) (offloaded pages only)");
+    FKV_CUDA(launch_summarize(h->D, h->layers[layer], page_begin, page_end, pick(h, stream)));
+    return FREEKV_OK;
+}
+
+freekv_status freekv_select_pages(freekv_handle* h, int32_t layer, const void* q, int32_t* pages_out,
+                                  uint8_t* corrected_out, void* stream) {
+    freekv_status st = check_layer(h, layer);
+    if (st != FREEKV_OK) return st;
+    return do_select(h, layer, q, pages_out, corrected_out, pick(h, stream));
+}
+
+freekv_status freekv_recall_pages(freekv_handle* h, int32_t layer, const uint8_t* sync_mask, void* stream) {
+    freekv_status st = check_layer(h, layer);
+    if (st != FREEKV_OK) return st;
+    if (sync_mask) return fail(FREEKV_EUNSUPPORTED, "sync_mask must be NULL in ABI v1");
+    return do_recall(h, layer, pick(h, stream));
+}
+
+freekv_status freekv_sparse_decode_attn(freekv_handle* h, int32_t layer, const void* q, float* out, void* stream) {
+    freekv_status st = check_layer(h, layer);
+    if (st != FREEKV_OK) return st;
+    return do_attn(h, layer, q, out, pick(h, stream));
+}
+
+freekv_status freekv_decode_step(freekv_handle* h, int32_t layer, const void* q, const void* k_new,
+                                 const void* v_new, float* out) {
+    freekv_status st = check_layer(h, layer);
+    if (st != FREEKV_OK) return st;
+    cudaStream_t s = h->cs;
+    if ((st = do_append(h, layer, k_new, v_new, 1, s)) != FREEKV_OK) return st;
+    if ((st = do_select(h, layer, q, nullptr, nullptr, s)) != FREEKV_OK) return st;
+    if ((st = do_recall(h, layer, s)) != FREEKV_OK) return st;
+    return do_attn(h, layer, q, out, s);
+}
+
+
+freekv_status freekv_get_selection(freekv_handle* h, int32_t layer, int32_t* pages, int32_t* frontier,
+                                   uint8_t* flags, float* cbar) {
+    freekv_status st = check_layer(h, layer);
+    if (st != FREEKV_OK) return st;
+    if ((st = sync_both(h)) != FREEKV_OK) return st;
+    const FkvLayer& L = h->layers[layer];
+    const size_t U = h->D.U, K = h->D.K;
+    if (pages) FKV_CUDA(cudaMemcpy(pages, L.pend_pages, U * K * 4, cudaMemcpyDeviceToHost));
+    if (frontier) FKV_CUDA(cudaMemcpy(frontier, L.pend_front, U * 4, cudaMemcpyDeviceToHost));
+    if (flags) FKV_CUDA(cudaMemcpy(flags, L.flags, U, cudaMemcpyDeviceToHost));
+    if (cbar) FKV_CUDA(cudaMemcpy(cbar, L.cbar, U * 4, cudaMemcpyDeviceToHost));
+    return FREEKV_OK;
+}
+
+freekv_status freekv_get_resident(freekv_handle* h, int32_t layer, int32_t* pages, int32_t* frontier) {
+    freekv_status st = check_layer(h, layer);
+    if (st != FREEKV_OK) return st;
+    if ((st = sync_both(h)) != FREEKV_OK) return st;
+    const FkvLayer& L = h->layers[layer];
+    const size_t U = h->D.U, K = h->D.K;
+    if (pages) FKV_CUDA(cudaMemcpy(pages, L.res_pages, U * K * 4, cudaMemcpyDeviceToHost));
+    if (frontier) FKV_CUDA(cudaMemcpy(frontier, L.res_front, U * 4, cudaMemcpyDeviceToHost));
+    return FREEKV_OK;
+}
+
+freekv_status freekv_get_fetch(freekv_handle* h, int32_t layer, int32_t* n_fetch, int32_t* fetch_pages) {
+    freekv_status st = check_layer(h, layer);
+    if (st != FREEKV_OK) return st;
+    if ((st = sync_both(h)) != FREEKV_OK) return st;
+    const FkvLayer& L = h->layers[layer];
+    const size_t U = h->D.U, K = h->D.K;
+    if (n_fetch) FKV_CUDA(cudaMemcpy(n_fetch, L.n_fetch, U * 4, cudaMemcpyDeviceToHost));
+    if (fetch_pages) FKV_CUDA(cudaMemcpy(fetch_pages, L.fetch_page, U * K * 4, cudaMemcpyDeviceToHost));
+    return FREEKV_OK;
+}
+
+freekv_status freekv_get_summaries(freekv_handle* h, int32_t layer, int32_t unit, int32_t page_begin,
+                                   int32_t page_end, uint16_t* out) {
+    freekv_status st = check_layer(h, layer);
+    if (st != FREEKV_OK) return st;
+    const FkvDims& D = h->D;
+    if (unit < 0 || unit >= D.U || page_begin < 0 || page_end > D.n_page_max || page_begin > page_end || !out)
+        return fail(FREEKV_EINVAL, "bad unit/page range/out");
+    if ((st = sync_both(h)) != FREEKV_OK) return st;
+    const size_t unit_elems = (size_t)D.n_page_max * 2 * D.d;
+    std::vector<uint16_t> buf(unit_elems);
+    FKV_CUDA(cudaMemcpy(buf.data(), h->layers[layer].summ + unit * unit_elems, unit_elems * 2,
+                        cudaMemcpyDeviceToHost));
+    for (int j = page_begin; j < page_end; ++j)
+        for (int which = 0; which < 2; ++which)
+            for (int c = 0; c < D.d; ++c) {
+                const size_t blk = (size_t)(j >> 5) * (D.d / 8) + (c >> 3);
+                const size_t off = ((blk * 2 + which) * 32 + (j & 31)) * 8 + (c & 7);
+                out[((size_t)(j - page_begin) * 2 + which) * D.d + c] = buf[off];
+            }
+    return FREEKV_OK;
+}
+
+freekv_status freekv_get_context(freekv_handle* h, int32_t layer, int32_t* ctx_tokens) {
+    freekv_status st = check_layer(h, layer);
+    if (st != FREEKV_OK) return st;
+    if (ctx_tokens) *ctx_tokens = h->ctx_host[layer];
+    return FREEKV_OK;
+}
+
+freekv_status freekv_get_dims(freekv_handle* h, int32_t* K, int32_t* n_page_max, int32_t* units) {
+    if (!h) return fail(FREEKV_EINVAL, "handle is NULL");
+    if (K) *K = h->D.K;
+    if (n_page_max) *n_page_max = h->D.n_page_max;
+    if (units) *units = h->D.U;
+    return FREEKV_OK;
+}
+
+freekv_status freekv_profile_begin(freekv_handle* h, int32_t max_launches) {
+    if (!h) return fail(FREEKV_EINVAL, "handle is NULL");
+    if (max_launches <= 0) return fail(FREEKV_EINVAL, "max_launches must be positive");
+    while (h->prof_pool.size() < (size_t)max_launches * 2) {
+        cudaEvent_t e;
+        FKV_CUDA(cudaEventCreate(&e));
+        h->prof_pool.push_back(e);
+    }
+    h->prof_used = 0;
+    h->prof_recs.clear();
+    h->prof = true;
+    return FREEKV_OK;
+}
+
+freekv_status freekv_profile_end(freekv_handle* h, float* ms, int32_t* launches) {
+    if (!h) return fail(FREEKV_EINVAL, "handle is NULL");
+    h->prof = false;
+    freekv_status st = sync_both(h);
+    if (st != FREEKV_OK) return st;
+    float acc[FREEKV_NUM_KERNEL_CLASSES] = {0};
+    int32_t cnt[FREEKV_NUM_KERNEL_CLASSES] = {0};
+    for (auto& r : h->prof_recs) {
+        float t = 0.0f;
+        FKV_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+        acc[r.cls] += t;
+        cnt[r.cls] += 1;
+    }
+    for (int i = 0; i < FREEKV_NUM_KERNEL_CLASSES; ++i) {
+        if (ms) ms[i] = acc[i];
+        if (launches) launches[i] = cnt[i];
+    }
+    h->prof_recs.clear();
+    h->prof_used = 0;
+    return FREEKV_OK;
+}
+
+freekv_status freekv_synchronize(freekv_handle* h) {
+    if (!h) return fail(FREEKV_EINVAL, "handle is NULL");
+    return sync_both(h);
+}
+
+void freekv_destroy(freekv_handle* h) {
+    if (!h) return;
+    cudaStreamSynchronize(h->cs);
+    cudaStreamSynchronize(h->rs);
+    for (auto e : h->ev_select)
+        if (e) cudaEventDestroy(e);
+    for (auto e : h->ev_recall)
+        if (e) cudaEventDestroy(e);
+    for (auto e : h->prof_pool) cudaEventDestroy(e);
+    delete h;
+}
+
+}  // extern "C"

@@ -1,0 +1,93 @@
+// fkv_internal.cuh -- shared definitions of the CUDA path (NOT shared with oracle/).
+//
+// Layout of one layer's state in the device arena and the host pool
+// (DESIGN.md §4).  All kernels receive a FkvDims and a FkvLayer by value.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace fkv {
+
+constexpr int kHeadDim = 128;   // d (P:557 models: 128)
+constexpr int kMaxG = 8;        // GQA group size supported (Llama 4, Qwen 7, 70B 8)
+
+struct FkvDims {
+    int nb, n_qo, n_kv, G, d, p;
+    int K;            // selectable pages per unit
+    int n_sink;       // sink pages (S/p)
+    int n_win;        // window pages (W/p)
+    int S_tok;        // sink tokens
+    int R_loc;        // local ring pages = n_win + 2
+    int n_page_max;   // device page capacity per unit (multiple of 128; summaries, scores)
+    int n_page_host;  // host pool pages per sequence (max_ctx/p + 1)
+    int max_ctx;
+    int U;            // nb * n_kv
+    int mode;
+    float tau;
+    float score_r;    // CFR-3: fl32(log2(e)/sqrt(d))
+    float attn_c;     // log2(e)/sqrt(d) for attention softmax (not CFR)
+    int n_chunks;     // attention split chunks per unit
+    int pages_per_chunk;
+};
+
+struct FkvLayer {
+    uint16_t* summ;       // [U][n_page_max/32][d/8][2][32][8]
+    uint16_t* sink;       // [U][n_sink][2][p][d]
+    uint16_t* slots;      // [U][2K][2][p][d]
+    uint16_t* ring;       // [U][R_loc][2][p][d]
+    uint16_t* q_prev;     // [nb][n_qo][d]
+    int32_t* res_pages;   // [U][K]  resident selection R (ascending, -1 pad)
+    int32_t* res_slot;    // [U][K]
+    int32_t* res_front;   // [U]     frontier f_R of R
+    int32_t* res_valid;   // [U]     0 until the first commit (bootstrap, A-12)
+    int32_t* pend_pages;  // [U][K]  pending S_i
+    int32_t* pend_slot;   // [U][K]
+    int32_t* pend_front;  // [U]
+    uint8_t* flags;       // [U]     correction flags of this step
+    float* cbar;          // [U]
+    int32_t* fetch_page;  // [U][K]  S_i \ R, ascending
+    int32_t* fetch_slot;  // [U][K]
+    int32_t* n_fetch;     // [U]
+    int32_t* ctx;         // [U]     context length Lc (tokens)
+    int32_t* n_off;       // [U]     pages [0, n_off) are offloaded; candidates [n_sink, n_off)
+    uint16_t* host;       // device-mapped host pool of this layer: [nb][n_page_host][n_kv][2][p][d]
+};
+
+struct FkvScratch {
+    float* scores;        // [U][G][n_page_max]
+    float* part_o;        // [U][n_chunks][G][d]
+    float* part_ml;       // [U][n_chunks][G][2]
+};
+
+__host__ __device__ inline size_t page_elems(const FkvDims& D) { return (size_t)2 * D.p * D.d; }
+
+// summary element offset (in uint16) of page j, channel c, which (0 = min, 1 = max)
+__device__ __forceinline__ size_t summ_chunk_offset(const FkvDims& D, int u, int j, int c8, int which) {
+    size_t unit_base = (size_t)u * D.n_page_max * 2 * D.d;
+    size_t blk = (size_t)(j >> 5) * (D.d / 8) + c8;
+    return unit_base + ((blk * 2 + which) * 32 + (j & 31)) * 8;
+}
+
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+__device__ __forceinline__ float bf16f(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
+
+}  // namespace fkv
+
+// kernel launchers (defined in the .cu files), return cudaGetLastError()
+namespace fkv {
+cudaError_t launch_append(const FkvDims& D, const FkvLayer& L, const uint16_t* k, const uint16_t* v,
+                          int n_new, cudaStream_t s);
+cudaError_t launch_summarize(const FkvDims& D, const FkvLayer& L, int page_begin, int page_end,
+                             cudaStream_t s);
+cudaError_t launch_score(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
+                         int max_n_off, cudaStream_t s);
+cudaError_t launch_finalize(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
+                            int32_t* pages_out, uint8_t* corrected_out, int lpt, cudaStream_t s);
+cudaError_t launch_recall(const FkvDims& D, const FkvLayer& L, int sync_mode, cudaStream_t s);
+cudaError_t launch_attn_split(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
+                              cudaStream_t s);
+cudaError_t launch_attn_combine(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
+                                float* out, cudaStream_t s);
+}  // namespace fkv

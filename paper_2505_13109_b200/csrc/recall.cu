@@ -1,0 +1,59 @@
+// recall.cu -- rows a5/a6: recall of selected pages from the pinned host pool.
+//
+// the host pool is (n_page, n_kv, 2, p, d), so one (page, KV
+// head) is 2*p*d contiguous elements (16 KiB at p=32, d=128) and one transfer
+// moves a whole page.  P:255-256: corrected units are recalled before this
+// step's attention, the others in the background for reuse at step i+1.
+//
+// B200 design: the fetch list is produced on the GPU by the
+// select kernel, so the copy is a zero-copy gather: one CTA per fetched page
+// reads the device-mapped pinned host page over PCIe with 128-bit loads and
+// writes it into its free cache slot (slot double-buffering: the slot is not
+// read by any attention until the next commit).  Synchronous mode runs on the
+// compute stream for flagged units; background mode runs on the dedicated
+// recall stream for the others.
+#include "fkv_internal.cuh"
+
+namespace fkv {
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__global__ void __launch_bounds__(128) fkv_recall_kernel(FkvDims D, FkvLayer L, int sync_mode) {
+    const int u = blockIdx.x, f = blockIdx.y;
+    const int flag = L.flags[u];
+    if ((flag != 0) != (sync_mode != 0)) return;
+    if (f >= L.n_fetch[u]) return;
+    const int b = u / D.n_kv, m = u % D.n_kv;
+    const int j = L.fetch_page[(size_t)u * D.K + f];
+    const int slot = L.fetch_slot[(size_t)u * D.K + f];
+    const size_t pe = page_elems(D);
+    const uint4* src = reinterpret_cast<const uint4*>(L.host + (((size_t)b * D.n_page_host + j) * D.n_kv + m) * pe);
+    uint4* dst = reinterpret_cast<uint4*>(L.slots + ((size_t)u * 2 * D.K + slot) * pe);
+    const int n = (int)(pe / 8);
+    for (int base = 0; base < n; base += 8 * 128) {
+        uint4 r[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int idx = base + i * 128 + threadIdx.x;
+            if (idx < n) r[i] = ld_stream(src + idx);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int idx = base + i * 128 + threadIdx.x;
+            if (idx < n) dst[idx] = r[i];
+        }
+    }
+}
+
+cudaError_t launch_recall(const FkvDims& D, const FkvLayer& L, int sync_mode, cudaStream_t s) {
+    fkv_recall_kernel<<<dim3(D.U, D.K), 128, 0, s>>>(D, L, sync_mode);
+    return cudaGetLastError();
+}
+
+}  // namespace fkv

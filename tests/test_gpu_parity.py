@@ -1,0 +1,149 @@
+"""Parity of the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star): selected page indices, frontier,
+correction flags, pooled cosine and fetch lists bit-exact; page summaries
+bit-exact; attention outputs within max relative error 2e-3 per (b, h)
+(reading A-21: ||o - o_ref||_inf / max(||o_ref||_inf, 1e-6)).
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 2e-3
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+def rel_err(out, ref):
+    """max over (b, h) of ||o - o_ref||_inf / max(||o_ref||_inf, 1e-6)."""
+    num = np.abs(out - ref).max(axis=-1)
+    den = np.maximum(np.abs(ref).max(axis=-1), 1e-6)
+    return float((num / den).max())
+
+
+def run_parity(G=4, n_kv=2, batch=2, page=32, sink=64, window=64, budget=256, L0=700, steps=6,
+               n_layers=2, tau=0.8, mode=O.MODE_SPECULATIVE, event_rate=0.3, seed=11, tie_pages=False,
+               check_summaries=True, use_primitives=False):
+    _need_gpu()
+    import paper_2505_13109_b200 as P
+    d = 128
+    n_qo = G * n_kv
+    max_ctx = L0 + steps + 3
+    cfg = P.FreeKVConfig(n_layers=n_layers, batch=batch, n_qo=n_qo, n_kv=n_kv, head_dim=d, page_size=page,
+                         budget_tokens=budget, sink_tokens=sink, window_tokens=window, max_ctx_tokens=max_ctx,
+                         tau=tau, mode=mode)
+    fkv = P.FreeKV(cfg)
+    ocfg = O.OracleConfig(n_layers=n_layers, batch=batch, n_qo=n_qo, n_kv=n_kv, head_dim=d, page_size=page,
+                          budget_tokens=budget, sink_tokens=sink, window_tokens=window, max_ctx_tokens=max_ctx,
+                          tau=tau, mode=mode)
+    eng = O.OracleEngine(ocfg)
+    dev = fkv.device
+    for layer in range(n_layers):
+        k, v = synth.gen_prefill(batch, n_kv, d, page, L0, sink // page, cfg.K, seed, layer)
+        if tie_pages:  # exact duplicate pages -> exact score ties -> lowest page id must win
+            n_pages = L0 // page
+            for j in range(sink // page + 3, n_pages - 1, 3):
+                k[:, j * page:(j + 1) * page] = k[:, (j - 1) * page:j * page]
+        eng.append(layer, synth.bf16_bits(k), synth.bf16_bits(v))
+        with torch.cuda.stream(fkv.stream):
+            fkv.append_kv(layer, k.to(dev), v.to(dev))
+    qps = [synth.QueryProcess(batch, n_qo, n_kv, d, seed, layer, event_rate=event_rate)
+           for layer in range(n_layers)]
+    n_flag = n_unflag = 0
+    worst = 0.0
+    for i in range(steps):
+        for layer in range(n_layers):
+            q, _ = qps[layer].next()
+            kn, vn = synth.gen_decode_kv(batch, n_kv, d, page, L0 + i, seed, layer)
+            ref = eng.step(layer, synth.bf16_bits(q), synth.bf16_bits(kn), synth.bf16_bits(vn))
+            out = torch.empty(batch, n_qo, d, dtype=torch.float32, device=dev)
+            qd, kd, vd = q.to(dev), kn.to(dev), vn.to(dev)
+            fkv.stream.wait_stream(torch.cuda.current_stream())
+            if use_primitives:
+                fkv.append_kv(layer, kd, vd)
+                pages_out = torch.full((batch, n_kv, cfg.K), -7, dtype=torch.int32, device=dev)
+                corr_out = torch.zeros((batch, n_kv), dtype=torch.uint8, device=dev)
+                fkv.select_pages(layer, qd, pages_out, corr_out)
+                fkv.recall_pages(layer)
+                fkv.sparse_decode_attn(layer, qd, out)
+            else:
+                fkv.decode_step(layer, qd, kd, vd, out)
+            fkv.synchronize()
+            sel = fkv.get_selection(layer)
+            assert np.array_equal(sel["flags"], ref["flags"]), (i, layer, sel["flags"], ref["flags"])
+            assert np.array_equal(sel["cbar"].view(np.uint32), ref["cbar"].view(np.uint32)) or i == 0
+            assert np.array_equal(sel["frontier"], ref["frontier"])
+            assert np.array_equal(sel["pages"], ref["sel"]), (i, layer, sel["pages"], ref["sel"])
+            if use_primitives:
+                assert np.array_equal(pages_out.cpu().numpy().reshape(-1, cfg.K), ref["sel"])
+                assert np.array_equal(corr_out.cpu().numpy().reshape(-1), ref["flags"])
+            n_fetch, fetch_pages = fkv.get_fetch(layer)
+            for u in range(fkv.U):
+                exp = ref["fetch_sync"][u] if ref["flags"][u] else ref["fetch_bg"][u]
+                assert list(fetch_pages[u, :n_fetch[u]]) == exp, (i, layer, u)
+            e = rel_err(out.cpu().numpy().astype(np.float64), ref["out"])
+            worst = max(worst, e)
+            assert e <= REL_TOL, (i, layer, e)
+            n_flag += int(ref["flags"].sum())
+            n_unflag += int((1 - ref["flags"]).sum())
+    if check_summaries:
+        for layer in range(n_layers):
+            for u in range(fkv.U):
+                n_off = eng.n_off[layer][u]
+                got = fkv.get_summaries(layer, u, sink // page, n_off)
+                assert np.array_equal(got, eng.summ[layer][u, sink // page:n_off]), (layer, u)
+    fkv.close()
+    return n_flag, n_unflag, worst
+
+
+def test_parity_llama_shape_speculative():
+    nf, nu, worst = run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=6)
+    assert nf > 0 and nu > 0  # both paths (corrected / speculative) exercised
+
+
+def test_parity_primitives():
+    run_parity(G=4, n_kv=2, batch=1, page=32, L0=900, steps=4, use_primitives=True)
+
+
+@pytest.mark.parametrize("G", [1, 2, 7, 8])
+def test_parity_group_sizes(G):
+    run_parity(G=G, n_kv=2, batch=1, page=32, L0=1100, steps=4)
+
+
+@pytest.mark.parametrize("page,sink,window,budget", [(16, 32, 48, 160), (64, 64, 128, 512)])
+def test_parity_page_sizes(page, sink, window, budget):
+    run_parity(G=4, n_kv=2, batch=2, page=page, sink=sink, window=window, budget=budget, L0=1300, steps=4)
+
+
+@pytest.mark.parametrize("mode,tau", [(O.MODE_ALWAYS, 0.8), (O.MODE_NEVER, 0.8), (O.MODE_SPECULATIVE, 1.0),
+                                      (O.MODE_SPECULATIVE, 0.0)])
+def test_parity_modes(mode, tau):
+    run_parity(mode=mode, tau=tau, L0=800, steps=5)
+
+
+def test_parity_ties_lowest_id():
+    run_parity(tie_pages=True, L0=1200, steps=4, event_rate=0.0)
+
+
+def test_parity_dense_equivalence():
+    """Budget >= context: sparse path == dense attention (north star)."""
+    run_parity(budget=4096, L0=600, steps=4)
+
+
+def test_parity_short_context_ragged():
+    """Context inside sink + window, then crossing it; ragged tail (not a page multiple)."""
+    run_parity(L0=37, steps=4, sink=64, window=64, budget=256, page=32)
+    run_parity(L0=150, steps=40, sink=32, window=32, budget=128, page=32, n_layers=1)
+
+
+def test_parity_long_context_many_tiles():
+    """|J| > 1024 exercises the multi-leaf-per-thread tree and radix select."""
+    run_parity(G=4, n_kv=1, batch=1, page=16, sink=64, window=64, budget=640, L0=20000, steps=3, n_layers=1)
