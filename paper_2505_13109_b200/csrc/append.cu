@@ -54,6 +54,25 @@ __global__ void __launch_bounds__(256) fkv_append_kernel(FkvDims D, FkvLayer L, 
         const bool crossing = j >= old_off && j < new_off;
         if (!touched && !crossing) continue;
         const int t0 = j * p;
+        if (!crossing) {
+            // fast path (every decode step): copy the new token rows straight to their page
+            uint4* dst = nullptr;
+            if (j < D.n_sink)
+                dst = reinterpret_cast<uint4*>(L.sink + ((size_t)u * D.n_sink + j) * pe);
+            else if (j >= ring_lo)
+                dst = reinterpret_cast<uint4*>(L.ring + ((size_t)u * D.R_loc + (j % D.R_loc)) * pe);
+            if (dst) {
+                const int ta = max(t0, L0), tb = min(t0 + p, L1);
+                const int n_u4 = (tb - ta) * row_u4;
+                for (int i = threadIdx.x; i < 2 * n_u4; i += blockDim.x) {
+                    const int kv = i / n_u4, rem = i % n_u4, r = rem / row_u4, c = rem % row_u4;
+                    const int t = ta + r;
+                    const uint16_t* src = (kv == 0 ? k : v) + (((size_t)b * n_new + (t - L0)) * D.n_kv + m) * d;
+                    dst[((size_t)kv * p + (t - t0)) * row_u4 + c] = reinterpret_cast<const uint4*>(src)[c];
+                }
+            }
+            continue;  // no __syncthreads needed: distinct pages never alias within this branch
+        }
         const uint4* old_src =
             j < D.n_sink ? reinterpret_cast<const uint4*>(L.sink + ((size_t)u * D.n_sink + j) * pe)
                          : reinterpret_cast<const uint4*>(L.ring + ((size_t)u * D.R_loc + (j % D.R_loc)) * pe);

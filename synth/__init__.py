@@ -5,17 +5,19 @@ CUDA side (tests, bench).  It holds NONE of the method's arithmetic: it only
 draws random bf16 tensors with the structure of the paper's workloads.
 
   GEN-S (keys/values): per (layer, unit) a unit "topic" u_m (unit-norm
-        Gaussian); keys k_t = z_t + alpha * [page(t) is hot] * u_m with
-        z ~ N(0, I_d); values v ~ N(0, I_d).  At prefill 1.5*K random candidate
+        Gaussian); keys k_t = z_t + alpha * w_page(t) * u_m with z ~ N(0, I_d),
+        w = 0 for cold pages and w = 0.5 + Exp(1) (heavy-tailed importance) for
+        hot pages; values v ~ N(0, I_d).  At prefill 1.5*K random candidate
         pages are hot; every later page is hot with probability p_hot.  This
         mimics the vertical attention lines of P:184 (fig:algo-ob2) so
         selections stay stable across steps (delta recall).
   GEN-Q (queries): q_{h,i} = beta * u_{m(h)} + e_{h,i},
         e_{h,i} = rho * e_{h,i-1} + sqrt(1 - rho^2) * xi,  xi ~ N(0, I_d).
-        rho = 0.895 gives mean adjacent cosine ~0.9 (Table
-        tab:q-sim-all 0.82-0.92).  With probability `event_rate` per
+        beta = 6, rho = 0.872 give mean adjacent cosine ~0.89 (Table
+        tab:q-sim-all 0.82-0.92) and ~0.8 changed pages per unit per step at
+        K = 32 (measured).  With probability `event_rate` per
         (step, b, kv-head) the unit's heads redraw e with rho = 0
-        (cosine ~0.05 < tau): a controlled correction rate (Table
+        (cosine ~0.22 < tau): a controlled correction rate (Table
         tab:corr-rate 0.04-0.52).
 Everything is rounded once to bf16 (round-to-nearest-even by torch).
 """
@@ -26,6 +28,9 @@ import math
 import torch
 
 SEED0 = 250513109
+ALPHA = 8.0   # hot-page key shift along the unit topic (x heavy-tailed weight 0.5 + Exp(1))
+BETA = 6.0    # persistent query component along the topic
+RHO = 0.872   # AR(1) coefficient of the query innovation: mean adjacent cosine (36 + 128 rho)/164 = 0.90
 
 
 def _gen(seed: int, device) -> torch.Generator:
@@ -41,27 +46,32 @@ def topics(batch: int, n_kv: int, d: int, seed: int, layer: int, device="cpu") -
 
 
 def gen_prefill(batch, n_kv, d, page, L0, n_sink_pages, K, seed, layer, device="cpu",
-                alpha: float = 4.0):
-    """Prefill K/V, NHD [batch][L0][n_kv][d] bf16, with 1.5*K hot candidate pages per unit."""
+                alpha: float = ALPHA, hot_factor: float = 1.5):
+    """Prefill K/V, NHD [batch][L0][n_kv][d] bf16, with hot_factor*K hot candidate pages per unit.
+
+    Hot page j gets strength alpha * w_j with w_j = 0.5 + Exp(1): a heavy-tailed
+    page importance, so the top of the ranking is stable step to step and the
+    churn is concentrated at the selection boundary."""
     g = _gen(seed * 1000003 + layer * 7919 + 2, device)
     u = topics(batch, n_kv, d, seed, layer, device)
     k = torch.randn(batch, L0, n_kv, d, generator=g, device=device, dtype=torch.float32)
     v = torch.randn(batch, L0, n_kv, d, generator=g, device=device, dtype=torch.float32)
     n_pages = L0 // page
     n_cand = max(0, n_pages - n_sink_pages)
-    n_hot = min(n_cand, int(math.ceil(1.5 * K)))
+    n_hot = min(n_cand, int(math.ceil(hot_factor * K)))
     if n_hot > 0:
         hot = torch.zeros(batch, n_kv, n_pages, device=device, dtype=torch.float32)
         scores = torch.rand(batch, n_kv, n_cand, generator=g, device=device)
         idx = scores.topk(n_hot, dim=-1).indices + n_sink_pages
-        hot.scatter_(2, idx, 1.0)
+        w = 0.5 + torch.empty(batch, n_kv, n_hot, device=device).exponential_(1.0, generator=g)
+        hot.scatter_(2, idx, w)
         hot_tok = hot.repeat_interleave(page, dim=2)                     # [b][kv][n_pages*page]
         hot_tok = torch.nn.functional.pad(hot_tok, (0, L0 - hot_tok.shape[2]))
         k = k + alpha * hot_tok.permute(0, 2, 1).unsqueeze(-1) * u.unsqueeze(1)
     return k.to(torch.bfloat16), v.to(torch.bfloat16)
 
 
-def gen_decode_kv(batch, n_kv, d, page, t, seed, layer, device="cpu", alpha: float = 4.0,
+def gen_decode_kv(batch, n_kv, d, page, t, seed, layer, device="cpu", alpha: float = ALPHA,
                   p_hot: float = 0.05):
     """k/v of the token at position t, NHD [batch][1][n_kv][d] bf16."""
     g = _gen(seed * 1000003 + layer * 7919 + 3 + 104729 * t, device)
@@ -70,6 +80,7 @@ def gen_decode_kv(batch, n_kv, d, page, t, seed, layer, device="cpu", alpha: flo
     v = torch.randn(batch, 1, n_kv, d, generator=g, device=device, dtype=torch.float32)
     gp = _gen(seed * 1000003 + layer * 7919 + 5 + 104729 * (t // page), device)
     hot = (torch.rand(batch, n_kv, generator=gp, device=device) < p_hot).float()
+    hot = hot * (0.5 + torch.empty(batch, n_kv, device=device).exponential_(1.0, generator=gp))
     k = k + alpha * (hot.unsqueeze(-1) * u).unsqueeze(1)
     return k.to(torch.bfloat16), v.to(torch.bfloat16)
 
@@ -77,8 +88,8 @@ def gen_decode_kv(batch, n_kv, d, page, t, seed, layer, device="cpu", alpha: flo
 class QueryProcess:
     """GEN-Q for one layer: call next() once per decode step."""
 
-    def __init__(self, batch, n_qo, n_kv, d, seed, layer, device="cpu", beta: float = 2.5,
-                 rho: float = 0.895, event_rate: float = 0.05):
+    def __init__(self, batch, n_qo, n_kv, d, seed, layer, device="cpu", beta: float = BETA,
+                 rho: float = RHO, event_rate: float = 0.05):
         self.batch, self.n_qo, self.n_kv, self.d = batch, n_qo, n_kv, d
         self.G = n_qo // n_kv
         self.beta, self.rho, self.event_rate = beta, rho, event_rate
