@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=None)
+    ap.add_argument("--eager", action="store_true", help="per-layer C-ABI calls instead of the whole-step graph")
     return ap.parse_args()
 
 
@@ -153,7 +154,7 @@ def run_ours(args, c, rank, world, local_rank):
     kv_loc = n_kv // world
     kv0 = rank * kv_loc
     n_layers = c["n_layers"]
-    total_steps = args.warmup + args.steps + args.profile_steps + args.steps  # warm, timed, profiled, e2e
+    total_steps = args.warmup + 1 + args.steps + args.profile_steps + args.steps  # warm, timed, profiled, e2e
     max_ctx = c["ctx"] + total_steps + 1
     stream = torch.cuda.Stream(dev)
     t0 = time.time()
@@ -196,6 +197,21 @@ def run_ours(args, c, rank, world, local_rank):
                 with torch.cuda.stream(stream):
                     torch.distributed.all_gather_into_tensor(out_full[layer], out_loc[layer])
 
+    # whole-step graph: fixed input/output buffers, one replay per step
+    q_buf, k_buf, v_buf = torch.empty_like(Qs[0]), torch.empty_like(Ks[0]), torch.empty_like(Vs[0])
+    o_buf = torch.empty(n_layers, nb, kv_loc * G, d, dtype=torch.float32, device=dev)
+
+    def graph_step(i):
+        with torch.cuda.stream(stream):
+            q_buf.copy_(Qs[i], non_blocking=True)
+            k_buf.copy_(Ks[i], non_blocking=True)
+            v_buf.copy_(Vs[i], non_blocking=True)
+        fkv.step_graph_launch()
+        if world > 1:
+            with torch.cuda.stream(stream):
+                for layer in range(n_layers):
+                    torch.distributed.all_gather_into_tensor(out_full[layer], o_buf[layer])
+
     def barrier():
         if world > 1:
             torch.distributed.barrier()
@@ -205,6 +221,12 @@ def run_ours(args, c, rank, world, local_rank):
         one_step(step)
         step += 1
     fkv.synchronize()
+    if not args.eager:
+        fkv.step_graph_capture(q_buf, k_buf, v_buf, o_buf)
+        graph_step(step)  # first replay (instantiation warm-up) is a warm-up step too
+        step += 1
+        fkv.synchronize()
+    run = one_step if args.eager else graph_step
     # ---- timed region (device time, CUDA events on the compute stream)
     clocks = ClockSampler(local_rank)
     clocks.start()
@@ -213,7 +235,7 @@ def run_ours(args, c, rank, world, local_rank):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for _ in range(args.steps):
-        one_step(step)
+        run(step)
         step += 1
     ev1.record(stream)
     fkv.synchronize()
@@ -254,22 +276,25 @@ def run_ours(args, c, rank, world, local_rank):
     Kh = Ks[step:step + args.steps].cpu().pin_memory()
     Vh = Vs[step:step + args.steps].cpu().pin_memory()
     host_out = torch.empty(n_layers, nb, kv_loc * G, d, dtype=torch.float32, pin_memory=True)
-    qd, kd, vd = torch.empty_like(Qs[0, 0]), torch.empty_like(Ks[0, 0]), torch.empty_like(Vs[0, 0])
-    h2d = (Qh[0, 0].numel() + Kh[0, 0].numel() + Vh[0, 0].numel()) * 2 * n_layers
-    d2h = host_out[0].numel() * 4 * n_layers
+    h2d = (Qh[0].numel() + Kh[0].numel() + Vh[0].numel()) * 2
+    d2h = host_out.numel() * 4
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    with torch.cuda.stream(stream):
-        for i in range(args.steps):
+    for i in range(args.steps):
+        with torch.cuda.stream(stream):
+            q_buf.copy_(Qh[i], non_blocking=True)
+            k_buf.copy_(Kh[i], non_blocking=True)
+            v_buf.copy_(Vh[i], non_blocking=True)
+        if args.eager:
             for layer in range(n_layers):
-                qd.copy_(Qh[i, layer], non_blocking=True)
-                kd.copy_(Kh[i, layer], non_blocking=True)
-                vd.copy_(Vh[i, layer], non_blocking=True)
-                fkv.decode_step(layer, qd, kd, vd, out_loc[layer])
-                host_out[layer].copy_(out_loc[layer], non_blocking=True)
-            step += 1
+                fkv.decode_step(layer, q_buf[layer], k_buf[layer], v_buf[layer], o_buf[layer])
+        else:
+            fkv.step_graph_launch()
+        with torch.cuda.stream(stream):
+            host_out.copy_(o_buf, non_blocking=True)
+        step += 1
     e1.record(stream)
     fkv.synchronize()
     torch.cuda.synchronize()
@@ -402,6 +427,7 @@ def main():
         "e2e": {"value": round(tok_s_e2e, 2), "unit": "tokens/s", "h2d_bytes_per_step": r["h2d"],
                 "d2h_bytes_per_step": r["d2h"]},
         "gpu_launches": int(sum(v[1] for v in prof.values()) / max(args.profile_steps, 1) * args.steps),
+        "execution": "eager per-layer C-ABI calls" if args.eager else "whole-step CUDA graphs (compute + recall)",
         "clocks": r["clocks"],
         "setup_s": {"alloc_pin": round(r["t_alloc"], 1), "prefill": round(r["t_prefill"], 1)},
     }

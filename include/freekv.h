@@ -137,6 +137,21 @@ freekv_status freekv_sparse_decode_attn(freekv_handle* h, int32_t layer, const v
 freekv_status freekv_decode_step(freekv_handle* h, int32_t layer, const void* q, const void* k_new,
                                  const void* v_new, float* out);
 
+/* Whole-step CUDA graphs: capture one decode step of every layer (the same
+ * sequence as n_layers freekv_decode_step calls) with fixed device buffers
+ * q_all [n_layers][nb][n_qo][d], k_all / v_all [n_layers][nb][1][n_kv][d]
+ * (bf16) and out_all [n_layers][nb][n_qo][d] (fp32).  The compute-stream part
+ * and the background-recall part are two graphs joined by external event
+ * nodes (recall of layer l waits for its selection; step i+1's layer l waits
+ * for step i's recall of layer l), so background recall keeps overlapping the
+ * next layers and the next step exactly as in the eager path.  Kernel
+ * arguments read all step-varying state from device memory, so one capture
+ * replays for every later step.  step_graph_launch replays one step on the
+ * handle's streams (ERANGE when the context would exceed max_ctx_tokens). */
+freekv_status freekv_step_graph_capture(freekv_handle* h, const void* q_all, const void* k_all,
+                                        const void* v_all, float* out_all);
+freekv_status freekv_step_graph_launch(freekv_handle* h);
+
 /* Inspection (blocking; host outputs).  All arrays u-major. */
 freekv_status freekv_get_selection(freekv_handle* h, int32_t layer, int32_t* pages /*[U][K]*/,
                                    int32_t* frontier /*[U]*/, uint8_t* flags /*[U]*/, float* cbar /*[U]*/);

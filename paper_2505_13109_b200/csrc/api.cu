@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -44,27 +45,34 @@ struct freekv_handle {
     std::vector<FkvLayer> layers;
     FkvScratch X;
     cudaStream_t cs = nullptr, rs = nullptr;
-    std::vector<cudaEvent_t> ev_select, ev_recall;
+    cudaStream_t ss = nullptr;  // library-owned high-priority stream for the synchronous recall
+    std::vector<cudaEvent_t> ev_select, ev_recall, ev_sync, ev_sync_x;
     std::vector<int> ctx_host;
     std::vector<int> recall_pending;
     int lpt = 1;  // leaves per thread of the finalize tree (fixed per handle, CFR-6)
+    bool serial_recall = false;  // diagnostics: FREEKV_SERIAL_RECALL=1 runs background recall on the compute stream
     // profiling (freekv_profile_begin/end)
     bool prof = false;
     std::vector<cudaEvent_t> prof_pool;
     size_t prof_used = 0;
     struct Rec { int cls; cudaEvent_t a, b; };
     std::vector<Rec> prof_recs;
+    // whole-step graphs (freekv_step_graph_capture / launch)
+    bool capturing = false;
+    cudaGraphExec_t g_compute = nullptr, g_recall = nullptr;
 };
 
 namespace {
 
 constexpr size_t kAlign = 256;
+constexpr int kMaxAttnWarps = 148 * 16;  // partial-record capacity; the grid uses min(resident warps, this)
 size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
 
 struct Sizes {
     size_t layer_bytes, scratch_bytes, dev_bytes, host_layer_bytes, host_bytes;
     // offsets inside one layer block
-    size_t o_summ, o_sink, o_slots, o_ring, o_qprev, o_res_pages, o_res_slot, o_res_front, o_res_valid,
+    size_t o_summ, o_sink, o_slots, o_ring, o_qprev, o_res_pages, o_res_slot, o_res_front, o_res_valid, o_res_cnt,
+        o_pend_cnt,
         o_pend_pages, o_pend_slot, o_pend_front, o_flags, o_cbar, o_fetch_page, o_fetch_slot, o_n_fetch, o_ctx,
         o_n_off;
     size_t o_scores, o_part_o, o_part_ml;
@@ -116,9 +124,8 @@ freekv_status validate(const freekv_config* c, FkvDims* D) {
     d.tau = c->tau;
     d.score_r = (float)(1.4426950408889634074 / std::sqrt((double)kHeadDim));  // CFR-3
     d.attn_c = (float)(1.4426950408889634074 / std::sqrt((double)kHeadDim));
-    d.pages_per_chunk = 2;
-    const int p_max = d.n_sink + K + d.R_loc;
-    d.n_chunks = (p_max + d.pages_per_chunk - 1) / d.pages_per_chunk;
+    d.P_max = d.n_sink + K + d.R_loc;
+    d.attn_warps = std::min(kMaxAttnWarps, d.U * d.P_max);
     *D = d;
     return FREEKV_OK;
 }
@@ -141,6 +148,8 @@ Sizes compute_sizes(const freekv_config* c, const FkvDims& D) {
     s.o_res_slot = take(U * K * 4);
     s.o_res_front = take(U * 4);
     s.o_res_valid = take(U * 4);
+    s.o_res_cnt = take(U * 4);
+    s.o_pend_cnt = take(U * 4);
     s.o_pend_pages = take(U * K * 4);
     s.o_pend_slot = take(U * K * 4);
     s.o_pend_front = take(U * 4);
@@ -154,8 +163,8 @@ Sizes compute_sizes(const freekv_config* c, const FkvDims& D) {
     s.layer_bytes = o;
     o = 0;
     s.o_scores = take(U * D.G * D.n_page_max * 4);
-    s.o_part_o = take(U * D.n_chunks * D.G * D.d * 4);
-    s.o_part_ml = take(U * D.n_chunks * D.G * 2 * 4);
+    s.o_part_o = take((size_t)2 * kMaxAttnWarps * D.G * D.d * 4);
+    s.o_part_ml = take((size_t)2 * kMaxAttnWarps * D.G * 2 * 4);
     s.scratch_bytes = o;
     s.dev_bytes = s.layer_bytes * c->n_layers + s.scratch_bytes;
     s.host_layer_bytes = (size_t)D.nb * D.n_page_host * D.n_kv * pe_b;
@@ -191,7 +200,7 @@ freekv_status do_append(freekv_handle* h, int layer, const void* k, const void* 
     if (n_new <= 0) return fail(FREEKV_EINVAL, "n_new must be positive");
     if (h->ctx_host[layer] + n_new > h->D.max_ctx)
         return fail(FREEKV_ERANGE, "context would exceed max_ctx_tokens");
-    if (h->recall_pending[layer]) FKV_CUDA(cudaStreamWaitEvent(s, h->ev_recall[layer], 0));
+    if (h->recall_pending[layer] && !h->capturing) FKV_CUDA(cudaStreamWaitEvent(s, h->ev_recall[layer], 0));
     FKV_CUDA(timed(h, K_APPEND, s, [&] {
         return launch_append(h->D, h->layers[layer], (const uint16_t*)k, (const uint16_t*)v, n_new, s);
     }));
@@ -204,9 +213,12 @@ freekv_status do_select(freekv_handle* h, int layer, const void* q, int32_t* pag
     if (!q) return fail(FREEKV_EINVAL, "q is NULL");
     if (h->ctx_host[layer] <= 0) return fail(FREEKV_ESTATE, "select before any token was appended");
     // the background recall of the previous step reads this layer's fetch list
-    if (h->recall_pending[layer]) FKV_CUDA(cudaStreamWaitEvent(s, h->ev_recall[layer], 0));
-    const int mno = max_n_off(h->D, h->ctx_host[layer]);
-    if (mno - h->D.n_sink > h->D.K)
+    if (h->capturing)
+        FKV_CUDA(cudaStreamWaitEvent(s, h->ev_recall[layer], cudaEventWaitExternal));
+    else if (h->recall_pending[layer])
+        FKV_CUDA(cudaStreamWaitEvent(s, h->ev_recall[layer], 0));
+    const int mno = h->capturing ? max_n_off(h->D, h->D.max_ctx) : max_n_off(h->D, h->ctx_host[layer]);
+    if (h->capturing || mno - h->D.n_sink > h->D.K)
         FKV_CUDA(timed(h, K_SCORE, s, [&] {
             return launch_score(h->D, h->layers[layer], h->X, (const uint16_t*)q, mno, s);
         }));
@@ -218,6 +230,14 @@ freekv_status do_select(freekv_handle* h, int layer, const void* q, int32_t* pag
 
 freekv_status do_recall(freekv_handle* h, int layer, cudaStream_t s) {
     FKV_CUDA(timed(h, K_RECALL_SYNC, s, [&] { return launch_recall(h->D, h->layers[layer], 1, s); }));
+    if (h->capturing) {  // the background half is captured separately into the recall graph
+        FKV_CUDA(cudaEventRecordWithFlags(h->ev_select[layer], s, cudaEventRecordExternal));
+        return FREEKV_OK;
+    }
+    if (h->serial_recall) {
+        FKV_CUDA(timed(h, K_RECALL_BG, s, [&] { return launch_recall(h->D, h->layers[layer], 0, s); }));
+        return FREEKV_OK;
+    }
     FKV_CUDA(cudaEventRecord(h->ev_select[layer], s));
     FKV_CUDA(cudaStreamWaitEvent(h->rs, h->ev_select[layer], 0));
     FKV_CUDA(timed(h, K_RECALL_BG, h->rs, [&] { return launch_recall(h->D, h->layers[layer], 0, h->rs); }));
@@ -229,7 +249,7 @@ freekv_status do_recall(freekv_handle* h, int layer, cudaStream_t s) {
 freekv_status do_attn(freekv_handle* h, int layer, const void* q, float* out, cudaStream_t s) {
     if (!q || !out) return fail(FREEKV_EINVAL, "q/out is NULL");
     FKV_CUDA(timed(h, K_ATTN_SPLIT, s, [&] {
-        return launch_attn_split(h->D, h->layers[layer], h->X, (const uint16_t*)q, s);
+        return launch_attn_split(h->D, h->layers[layer], h->X, (const uint16_t*)q, 0, s);
     }));
     FKV_CUDA(timed(h, K_ATTN_COMBINE, s, [&] {
         return launch_attn_combine(h->D, h->layers[layer], h->X, (const uint16_t*)q, out, s);
@@ -237,8 +257,44 @@ freekv_status do_attn(freekv_handle* h, int layer, const void* q, float* out, cu
     return FREEKV_OK;
 }
 
+// Composite step tail (decode_step and the step graph): the
+// corrected units' synchronous recall runs on the high-priority stream ss while the
+// attention of every other unit (whose pages are resident) runs on the compute
+// stream; the corrected units are attended once their pages have landed.  The
+// background recall (rs) follows the synchronous one so it never competes with it
+// for the host link.
+freekv_status do_step_tail(freekv_handle* h, int layer, const void* q, float* out) {
+    cudaStream_t cs = h->cs;
+    const FkvDims& D = h->D;
+    FkvLayer& L = h->layers[layer];
+    FKV_CUDA(cudaEventRecord(h->ev_select[layer], cs));
+    FKV_CUDA(cudaStreamWaitEvent(h->ss, h->ev_select[layer], 0));
+    FKV_CUDA(timed(h, K_RECALL_SYNC, h->ss, [&] { return launch_recall(D, L, 1, h->ss); }));
+    FKV_CUDA(cudaEventRecord(h->ev_sync[layer], h->ss));
+    if (h->capturing) {
+        FKV_CUDA(cudaEventRecordWithFlags(h->ev_sync_x[layer], h->ss, cudaEventRecordExternal));
+    } else if (h->serial_recall) {
+        FKV_CUDA(timed(h, K_RECALL_BG, h->ss, [&] { return launch_recall(D, L, 0, h->ss); }));
+        FKV_CUDA(cudaEventRecord(h->ev_recall[layer], h->ss));
+        h->recall_pending[layer] = 1;
+    } else {
+        FKV_CUDA(cudaStreamWaitEvent(h->rs, h->ev_sync[layer], 0));
+        FKV_CUDA(timed(h, K_RECALL_BG, h->rs, [&] { return launch_recall(D, L, 0, h->rs); }));
+        FKV_CUDA(cudaEventRecord(h->ev_recall[layer], h->rs));
+        h->recall_pending[layer] = 1;
+    }
+    FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] { return launch_attn_split(D, L, h->X, (const uint16_t*)q, 1, cs); }));
+    FKV_CUDA(cudaStreamWaitEvent(cs, h->ev_sync[layer], 0));
+    FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] { return launch_attn_split(D, L, h->X, (const uint16_t*)q, 2, cs); }));
+    FKV_CUDA(timed(h, K_ATTN_COMBINE, cs, [&] {
+        return launch_attn_combine(D, L, h->X, (const uint16_t*)q, out, cs);
+    }));
+    return FREEKV_OK;
+}
+
 freekv_status sync_both(freekv_handle* h) {
     FKV_CUDA(cudaStreamSynchronize(h->cs));
+    FKV_CUDA(cudaStreamSynchronize(h->ss));
     FKV_CUDA(cudaStreamSynchronize(h->rs));
     return FREEKV_OK;
 }
@@ -303,6 +359,8 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         L.res_slot = (int32_t*)(base + s.o_res_slot);
         L.res_front = (int32_t*)(base + s.o_res_front);
         L.res_valid = (int32_t*)(base + s.o_res_valid);
+        L.res_cnt = (int32_t*)(base + s.o_res_cnt);
+        L.pend_cnt = (int32_t*)(base + s.o_pend_cnt);
         L.pend_pages = (int32_t*)(base + s.o_pend_pages);
         L.pend_slot = (int32_t*)(base + s.o_pend_slot);
         L.pend_front = (int32_t*)(base + s.o_pend_front);
@@ -324,13 +382,43 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         while (P2 < D.n_page_host) P2 <<= 1;
         h->lpt = P2 <= 1024 ? 1 : P2 / 1024;
     }
+    {
+        int warps = 0;
+        cudaError_t oe = attn_resident_warps(&warps);
+        if (oe != cudaSuccess) {
+            freekv_destroy(h);
+            return fail(FREEKV_ECUDA, std::string("occupancy query: ") + cudaGetErrorString(oe));
+        }
+        // T <= V (every warp owns >= 1 page), T * V < 2^31 (32-bit range math), and at most
+        // ~254 records per unit (combine kernel capacity)
+        const long long V = (long long)D.U * D.P_max;
+        long long T = std::min<long long>({(long long)warps, (long long)kMaxAttnWarps, V, 254LL * D.U});
+        while (T > 1 && T * V >= (1LL << 31)) T /= 2;
+        h->D.attn_warps = (int)std::max(1LL, T);
+    }
+    {
+        const char* sr = getenv("FREEKV_SERIAL_RECALL");
+        h->serial_recall = sr && sr[0] == '1';
+    }
     h->ctx_host.assign(cfg->n_layers, 0);
     h->recall_pending.assign(cfg->n_layers, 0);
     h->ev_select.resize(cfg->n_layers);
     h->ev_recall.resize(cfg->n_layers);
+    h->ev_sync.resize(cfg->n_layers);
+    h->ev_sync_x.resize(cfg->n_layers);
+    {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if (cudaStreamCreateWithPriority(&h->ss, cudaStreamNonBlocking, hi) != cudaSuccess) {
+            freekv_destroy(h);
+            return fail(FREEKV_ECUDA, "cudaStreamCreateWithPriority failed");
+        }
+    }
     for (int l = 0; l < cfg->n_layers; ++l) {
         if (cudaEventCreateWithFlags(&h->ev_select[l], cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&h->ev_recall[l], cudaEventDisableTiming) != cudaSuccess) {
+            cudaEventCreateWithFlags(&h->ev_recall[l], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->ev_sync[l], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->ev_sync_x[l], cudaEventDisableTiming) != cudaSuccess) {
             freekv_destroy(h);
             return fail(FREEKV_ECUDA, "cudaEventCreate failed");
         }
@@ -393,8 +481,7 @@ freekv_status freekv_decode_step(freekv_handle* h, int32_t layer, const void* q,
     cudaStream_t s = h->cs;
     if ((st = do_append(h, layer, k_new, v_new, 1, s)) != FREEKV_OK) return st;
     if ((st = do_select(h, layer, q, nullptr, nullptr, s)) != FREEKV_OK) return st;
-    if ((st = do_recall(h, layer, s)) != FREEKV_OK) return st;
-    return do_attn(h, layer, q, out, s);
+    return do_step_tail(h, layer, q, out);
 }
 
 
@@ -512,15 +599,94 @@ freekv_status freekv_synchronize(freekv_handle* h) {
     return sync_both(h);
 }
 
+static void drop_graphs(freekv_handle* h) {
+    if (h->g_compute) cudaGraphExecDestroy(h->g_compute);
+    if (h->g_recall) cudaGraphExecDestroy(h->g_recall);
+    h->g_compute = h->g_recall = nullptr;
+}
+
+freekv_status freekv_step_graph_capture(freekv_handle* h, const void* q_all, const void* k_all, const void* v_all,
+                                        float* out_all) {
+    if (!h) return fail(FREEKV_EINVAL, "handle is NULL");
+    if (!q_all || !k_all || !v_all || !out_all) return fail(FREEKV_EINVAL, "NULL buffer");
+    if (h->prof) return fail(FREEKV_ESTATE, "capture while profiling");
+    for (int l = 0; l < h->cfg.n_layers; ++l)
+        if (h->ctx_host[l] <= 0) return fail(FREEKV_ESTATE, "capture before the first append of every layer");
+    freekv_status st = sync_both(h);
+    if (st != FREEKV_OK) return st;
+    drop_graphs(h);
+    const FkvDims& D = h->D;
+    const size_t q_stride = (size_t)D.nb * D.n_qo * D.d * 2, kv_stride = (size_t)D.nb * D.n_kv * D.d * 2;
+    const size_t o_stride = (size_t)D.nb * D.n_qo * D.d;
+    cudaGraph_t gc = nullptr, gr = nullptr;
+    h->capturing = true;
+    cudaError_t e = cudaStreamBeginCapture(h->cs, cudaStreamCaptureModeThreadLocal);
+    for (int l = 0; l < h->cfg.n_layers && e == cudaSuccess && st == FREEKV_OK; ++l) {
+        const uint8_t* q = (const uint8_t*)q_all + q_stride * l;
+        const uint8_t* k = (const uint8_t*)k_all + kv_stride * l;
+        const uint8_t* v = (const uint8_t*)v_all + kv_stride * l;
+        e = launch_append(D, h->layers[l], (const uint16_t*)k, (const uint16_t*)v, 1, h->cs);
+        if (e == cudaSuccess) st = do_select(h, l, q, nullptr, nullptr, h->cs);
+        if (st == FREEKV_OK) st = do_step_tail(h, l, q, out_all + o_stride * l);
+    }
+    cudaError_t e2 = cudaStreamEndCapture(h->cs, &gc);
+    if (e == cudaSuccess) e = e2;
+    if (e == cudaSuccess && st == FREEKV_OK) {
+        e = cudaStreamBeginCapture(h->rs, cudaStreamCaptureModeThreadLocal);
+        for (int l = 0; l < h->cfg.n_layers && e == cudaSuccess; ++l) {
+            e = cudaStreamWaitEvent(h->rs, h->ev_sync_x[l], cudaEventWaitExternal);
+            if (e == cudaSuccess) e = launch_recall(D, h->layers[l], 0, h->rs);
+            if (e == cudaSuccess) e = cudaEventRecordWithFlags(h->ev_recall[l], h->rs, cudaEventRecordExternal);
+        }
+        e2 = cudaStreamEndCapture(h->rs, &gr);
+        if (e == cudaSuccess) e = e2;
+    }
+    h->capturing = false;
+    if (e == cudaSuccess && st == FREEKV_OK) e = cudaGraphInstantiate(&h->g_compute, gc, 0);
+    if (e == cudaSuccess && st == FREEKV_OK) e = cudaGraphInstantiate(&h->g_recall, gr, 0);
+    if (gc) cudaGraphDestroy(gc);
+    if (gr) cudaGraphDestroy(gr);
+    if (st != FREEKV_OK) {
+        drop_graphs(h);
+        return st;
+    }
+    if (e != cudaSuccess) {
+        drop_graphs(h);
+        return fail(FREEKV_ECUDA, std::string("step graph capture: ") + cudaGetErrorString(e));
+    }
+    return FREEKV_OK;
+}
+
+freekv_status freekv_step_graph_launch(freekv_handle* h) {
+    if (!h) return fail(FREEKV_EINVAL, "handle is NULL");
+    if (!h->g_compute || !h->g_recall) return fail(FREEKV_ESTATE, "no captured step graph");
+    for (int l = 0; l < h->cfg.n_layers; ++l)
+        if (h->ctx_host[l] + 1 > h->D.max_ctx) return fail(FREEKV_ERANGE, "context would exceed max_ctx_tokens");
+    FKV_CUDA(cudaGraphLaunch(h->g_compute, h->cs));
+    FKV_CUDA(cudaGraphLaunch(h->g_recall, h->rs));
+    for (int l = 0; l < h->cfg.n_layers; ++l) {
+        h->ctx_host[l] += 1;
+        h->recall_pending[l] = 1;
+    }
+    return FREEKV_OK;
+}
+
 void freekv_destroy(freekv_handle* h) {
     if (!h) return;
     cudaStreamSynchronize(h->cs);
+    if (h->ss) cudaStreamSynchronize(h->ss);
     cudaStreamSynchronize(h->rs);
+    drop_graphs(h);
     for (auto e : h->ev_select)
         if (e) cudaEventDestroy(e);
     for (auto e : h->ev_recall)
         if (e) cudaEventDestroy(e);
+    for (auto e : h->ev_sync)
+        if (e) cudaEventDestroy(e);
+    for (auto e : h->ev_sync_x)
+        if (e) cudaEventDestroy(e);
     for (auto e : h->prof_pool) cudaEventDestroy(e);
+    if (h->ss) cudaStreamDestroy(h->ss);
     delete h;
 }
 

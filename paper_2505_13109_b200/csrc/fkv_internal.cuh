@@ -27,8 +27,8 @@ struct FkvDims {
     float tau;
     float score_r;    // CFR-3: fl32(log2(e)/sqrt(d))
     float attn_c;     // log2(e)/sqrt(d) for attention softmax (not CFR)
-    int n_chunks;     // attention split chunks per unit
-    int pages_per_chunk;
+    int P_max;        // upper bound of attention pages per unit: n_sink + K + R_loc
+    int attn_warps;   // T: warps of the balanced split-KV attention grid (<= resident warps)
 };
 
 struct FkvLayer {
@@ -41,6 +41,8 @@ struct FkvLayer {
     int32_t* res_slot;    // [U][K]
     int32_t* res_front;   // [U]     frontier f_R of R
     int32_t* res_valid;   // [U]     0 until the first commit (bootstrap, A-12)
+    int32_t* res_cnt;     // [U]     number of valid entries of res_pages
+    int32_t* pend_cnt;    // [U]     number of valid entries of pend_pages
     int32_t* pend_pages;  // [U][K]  pending S_i
     int32_t* pend_slot;   // [U][K]
     int32_t* pend_front;  // [U]
@@ -56,8 +58,8 @@ struct FkvLayer {
 
 struct FkvScratch {
     float* scores;        // [U][G][n_page_max]
-    float* part_o;        // [U][n_chunks][G][d]
-    float* part_ml;       // [U][n_chunks][G][2]
+    float* part_o;        // [2 * attn_warps][G][d]   per-warp, per-unit-segment partial outputs
+    float* part_ml;       // [2 * attn_warps][G][2]   (running max, running sum)
 };
 
 __host__ __device__ inline size_t page_elems(const FkvDims& D) { return (size_t)2 * D.p * D.d; }
@@ -73,6 +75,39 @@ __device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w 
 __device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
 __device__ __forceinline__ float bf16f(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
 
+// ---- TMA bulk copy (cp.async.bulk, SASS UBLKCP) + mbarrier helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst_smem)),
+        "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
 }  // namespace fkv
 
 // kernel launchers (defined in the .cu files), return cudaGetLastError()
@@ -86,8 +121,9 @@ cudaError_t launch_score(const FkvDims& D, const FkvLayer& L, const FkvScratch& 
 cudaError_t launch_finalize(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                             int32_t* pages_out, uint8_t* corrected_out, int lpt, cudaStream_t s);
 cudaError_t launch_recall(const FkvDims& D, const FkvLayer& L, int sync_mode, cudaStream_t s);
+cudaError_t attn_resident_warps(int* warps);  // SMs x resident warps/SM of the split kernel
 cudaError_t launch_attn_split(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                              cudaStream_t s);
+                              int phase, cudaStream_t s);
 cudaError_t launch_attn_combine(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                                 float* out, cudaStream_t s);
 }  // namespace fkv

@@ -25,33 +25,38 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
 }
 
 __global__ void __launch_bounds__(128) fkv_recall_kernel(FkvDims D, FkvLayer L, int sync_mode) {
-    const int u = blockIdx.x, f = blockIdx.y;
+    const int u = blockIdx.x;
     const int flag = L.flags[u];
     if ((flag != 0) != (sync_mode != 0)) return;
-    if (f >= L.n_fetch[u]) return;
+    const int nf = L.n_fetch[u];
     const int b = u / D.n_kv, m = u % D.n_kv;
-    const int j = L.fetch_page[(size_t)u * D.K + f];
-    const int slot = L.fetch_slot[(size_t)u * D.K + f];
     const size_t pe = page_elems(D);
-    const uint4* src = reinterpret_cast<const uint4*>(L.host + (((size_t)b * D.n_page_host + j) * D.n_kv + m) * pe);
-    uint4* dst = reinterpret_cast<uint4*>(L.slots + ((size_t)u * 2 * D.K + slot) * pe);
-    const int n = (int)(pe / 8);
-    for (int base = 0; base < n; base += 8 * 128) {
-        uint4 r[8];
+    const int n = (int)(pe / 8);  // uint4 per page
+    for (int f = blockIdx.y; f < nf; f += gridDim.y) {
+        const int j = L.fetch_page[(size_t)u * D.K + f];
+        const int slot = L.fetch_slot[(size_t)u * D.K + f];
+        const uint4* src =
+            reinterpret_cast<const uint4*>(L.host + (((size_t)b * D.n_page_host + j) * D.n_kv + m) * pe);
+        uint4* dst = reinterpret_cast<uint4*>(L.slots + ((size_t)u * 2 * D.K + slot) * pe);
+        for (int base = 0; base < n; base += 8 * 128) {
+            uint4 r[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int idx = base + i * 128 + threadIdx.x;
-            if (idx < n) r[i] = ld_stream(src + idx);
-        }
+            for (int i = 0; i < 8; ++i) {
+                const int idx = base + i * 128 + threadIdx.x;
+                if (idx < n) r[i] = ld_stream(src + idx);
+            }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int idx = base + i * 128 + threadIdx.x;
-            if (idx < n) dst[idx] = r[i];
+            for (int i = 0; i < 8; ++i) {
+                const int idx = base + i * 128 + threadIdx.x;
+                if (idx < n) dst[idx] = r[i];
+            }
         }
     }
 }
 
 cudaError_t launch_recall(const FkvDims& D, const FkvLayer& L, int sync_mode, cudaStream_t s) {
+    // one CTA per (unit, fetch slot): a corrected unit's pages all stream over PCIe at once
+    // (latency-critical before attention); CTAs beyond n_fetch exit immediately
     fkv_recall_kernel<<<dim3(D.U, D.K), 128, 0, s>>>(D, L, sync_mode);
     return cudaGetLastError();
 }

@@ -12,6 +12,8 @@
 // Every floating-point step that decides an index follows the canonical fp32
 // recipe with explicit round-to-nearest intrinsics, so the page
 // indices are bit-identical to the CPU oracle.
+#include <algorithm>
+
 #include "fkv_internal.cuh"
 
 namespace fkv {
@@ -34,67 +36,122 @@ __device__ __forceinline__ float cexp2_cfr(float x) {
 }
 
 // ----------------------------------------------------------- a2: scoring
-// Thread per page.  CFR-2 in the two-FMA form: for c ascending,
+// Thread per page, warp per 32-page summary block.  Each warp pulls its whole
+// 16 KiB block (32 pages x {min,max} x 128 channels, bf16) into shared memory
+// with ONE cp.async.bulk (TMA engine, mbarrier completion), so every warp has
+// its full working set in flight at once; q is staged meanwhile.  Lanes then
+// read their page's 16-byte channel chunks conflict-free.
+// CFR-2 in the two-FMA form: for c ascending,
 //   u = fma(max(q_c,0), mx_c, u); u = fma(min(q_c,0), mn_c, u)
 // -- exactly one of the two changes u, by fl(u + q_c * m_c) with an exact
 // product, so u equals the recipe's sequential sum up to the sign of zero.
+constexpr int kScoreWarps = 4;
+constexpr int kSummBlockBytes = 32 * 2 * kHeadDim * 2;  // 16 KiB: 32 pages x {min,max} x 128 ch
+
+// Heads of a group are split over the 4 warps of a CTA (warp w scores heads
+// w, w+4 for every page of the block), so all 4 warps share one 16 KiB summary
+// block in shared memory.  Each CTA takes a contiguous range of the flattened
+// (unit-major) list of active 32-page blocks and streams it through a 2-stage
+// ring of cp.async.bulk (TMA) copies with mbarrier completion: block i+1 lands
+// while block i is scored.  ~6 CTAs (24 warps) per SM hide the FMA latency.
+
 template <int G>
-__global__ void __launch_bounds__(128) fkv_score_kernel(FkvDims D, FkvLayer L, float* __restrict__ scores,
-                                                        const uint16_t* __restrict__ q) {
-    constexpr int GP = (G + 3) / 4 * 4;
-    __shared__ __align__(16) float qp[kHeadDim][GP];
-    __shared__ __align__(16) float qn[kHeadDim][GP];
-    const int u = blockIdx.x, b = u / D.n_kv, m = u % D.n_kv;
-    const int n_off = L.n_off[u];
-    const int j0 = blockIdx.y * blockDim.x;
-    if (j0 >= n_off) return;
-    for (int i = threadIdx.x; i < GP * kHeadDim; i += blockDim.x) {
-        const int h = i / kHeadDim, c = i % kHeadDim;
-        float x = 0.0f;
-        if (h < G) x = bf16f(q[((size_t)b * D.n_qo + m * G + h) * kHeadDim + c]);
-        qp[c][h] = fmaxf(x, 0.0f);
-        qn[c][h] = fminf(x, 0.0f);
+__global__ void __launch_bounds__(kScoreWarps * 32) fkv_score_kernel(FkvDims D, FkvLayer L,
+                                                                     float* __restrict__ scores,
+                                                                     const uint16_t* __restrict__ q, int blk_lo,
+                                                                     int nb_act) {
+    constexpr int NH = (G + kScoreWarps - 1) / kScoreWarps;  // heads of this warp (<= 2)
+    extern __shared__ __align__(128) uint8_t s_raw[];
+    uint4* buf = reinterpret_cast<uint4*>(s_raw);                                   // [2][16 KiB]
+    float4* qpn = reinterpret_cast<float4*>(s_raw + 2 * kSummBlockBytes);          // [G][64]: (q+,q-) x 2 ch
+    __shared__ __align__(8) uint64_t bar[2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long N = (long long)D.U * nb_act;
+    const long long i0 = (long long)blockIdx.x * N / gridDim.x, i1 = (long long)(blockIdx.x + 1) * N / gridDim.x;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
     }
     __syncthreads();
-    const int j = j0 + threadIdx.x;
-    float acc[G];
+    auto active = [&](long long i) {
+        const int u = (int)(i / nb_act), blk = blk_lo + (int)(i % nb_act);
+        const int n_off = L.n_off[u];
+        return blk * 32 < n_off && blk * 32 + 31 >= D.n_sink;
+    };
+    auto issue = [&](long long i, int sb) {  // thread 0 only
+        const int u = (int)(i / nb_act), blk = blk_lo + (int)(i % nb_act);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bar[sb], kSummBlockBytes);
+        bulk_g2s(buf + sb * (kSummBlockBytes / 16), L.summ + summ_chunk_offset(D, u, blk * 32, 0, 0),
+                 kSummBlockBytes, &bar[sb]);
+    };
+    if (threadIdx.x == 0) {
+        if (i0 < i1 && active(i0)) issue(i0, 0);
+        if (i0 + 1 < i1 && active(i0 + 1)) issue(i0 + 1, 1);
+    }
+    uint32_t phase_bits = 0u;
+    int q_unit = -1;
+    for (long long i = i0; i < i1; ++i) {
+        const int sb = (int)((i - i0) & 1);
+        const int u = (int)(i / nb_act), blk = blk_lo + (int)(i % nb_act);
+        const bool act = active(i);
+        if (act && u != q_unit) {  // stage (q+, q-) of this unit, two channels per float4
+            const int b = u / D.n_kv, m = u % D.n_kv;
+            for (int e = threadIdx.x; e < G * kHeadDim / 2; e += blockDim.x) {
+                const int h = e / (kHeadDim / 2), c2 = e % (kHeadDim / 2);
+                const uint32_t w2 = *reinterpret_cast<const uint32_t*>(
+                    q + ((size_t)b * D.n_qo + m * G + h) * kHeadDim + 2 * c2);
+                const float x0 = bf16_lo(w2), x1 = bf16_hi(w2);
+                qpn[h * (kHeadDim / 2) + c2] = make_float4(fmaxf(x0, 0.0f), fminf(x0, 0.0f), fmaxf(x1, 0.0f),
+                                                           fminf(x1, 0.0f));
+            }
+            __syncthreads();
+            q_unit = u;
+        }
+        if (act) {
+            mbar_wait(&bar[sb], (phase_bits >> sb) & 1u);
+            phase_bits ^= 1u << sb;
+            const uint4* blkp = buf + sb * (kSummBlockBytes / 16);
+            float acc[NH];
 #pragma unroll
-    for (int h = 0; h < G; ++h) acc[h] = 0.0f;
-    const uint4* base = reinterpret_cast<const uint4*>(L.summ);
+            for (int k = 0; k < NH; ++k) acc[k] = 0.0f;
 #pragma unroll 2
-    for (int c8 = 0; c8 < kHeadDim / 8; ++c8) {
-        const uint4 mn4 = __ldg(base + summ_chunk_offset(D, u, j, c8, 0) / 8);
-        const uint4 mx4 = __ldg(base + summ_chunk_offset(D, u, j, c8, 1) / 8);
-        const uint32_t mnw[4] = {mn4.x, mn4.y, mn4.z, mn4.w};
-        const uint32_t mxw[4] = {mx4.x, mx4.y, mx4.z, mx4.w};
+            for (int c8 = 0; c8 < kHeadDim / 8; ++c8) {
+                const uint4 mn4 = blkp[(c8 * 2 + 0) * 32 + lane];
+                const uint4 mx4 = blkp[(c8 * 2 + 1) * 32 + lane];
+                const uint32_t mnw[4] = {mn4.x, mn4.y, mn4.z, mn4.w};
+                const uint32_t mxw[4] = {mx4.x, mx4.y, mx4.z, mx4.w};
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
+                for (int wd = 0; wd < 4; ++wd) {
+                    const float mn0 = bf16_lo(mnw[wd]), mn1 = bf16_hi(mnw[wd]);
+                    const float mx0 = bf16_lo(mxw[wd]), mx1 = bf16_hi(mxw[wd]);
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                const int c = c8 * 8 + 2 * w + half;
-                const float mn = half ? bf16_hi(mnw[w]) : bf16_lo(mnw[w]);
-                const float mx = half ? bf16_hi(mxw[w]) : bf16_lo(mxw[w]);
-#pragma unroll
-                for (int h4 = 0; h4 < GP; h4 += 4) {
-                    const float4 p4 = *reinterpret_cast<const float4*>(&qp[c][h4]);
-                    const float4 n4 = *reinterpret_cast<const float4*>(&qn[c][h4]);
-                    const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
-                    const float nv[4] = {n4.x, n4.y, n4.z, n4.w};
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        if (h4 + e < G) {
-                            acc[h4 + e] = __fmaf_rn(pv[e], mx, acc[h4 + e]);
-                            acc[h4 + e] = __fmaf_rn(nv[e], mn, acc[h4 + e]);
+                    for (int k = 0; k < NH; ++k) {
+                        const int h = warp + k * kScoreWarps;
+                        if (h < G) {
+                            const float4 qq = qpn[h * (kHeadDim / 2) + c8 * 4 + wd];
+                            // channel 2*wd (ascending), then channel 2*wd+1 -- CFR-2 order
+                            acc[k] = __fmaf_rn(qq.x, mx0, acc[k]);
+                            acc[k] = __fmaf_rn(qq.y, mn0, acc[k]);
+                            acc[k] = __fmaf_rn(qq.z, mx1, acc[k]);
+                            acc[k] = __fmaf_rn(qq.w, mn1, acc[k]);
                         }
                     }
                 }
             }
-        }
-    }
-    if (j >= D.n_sink && j < n_off) {
+            const int j = blk * 32 + lane;
+            const int n_off = L.n_off[u];
+            if (j >= D.n_sink && j < n_off) {
 #pragma unroll
-        for (int h = 0; h < G; ++h)
-            scores[((size_t)u * G + h) * D.n_page_max + j] = __fmul_rn(acc[h], D.score_r);  // CFR-3
+                for (int k = 0; k < NH; ++k) {
+                    const int h = warp + k * kScoreWarps;
+                    if (h < G) scores[((size_t)u * G + h) * D.n_page_max + j] = __fmul_rn(acc[k], D.score_r);  // CFR-3
+                }
+            }
+        }
+        __syncthreads();  // every warp is done with buffer sb (and with q) before it is refilled
+        if (threadIdx.x == 0 && i + 2 < i1 && active(i + 2)) issue(i + 2, sb);
     }
 }
 
@@ -149,12 +206,25 @@ __global__ void __launch_bounds__(1024) fkv_select_finalize_kernel(FkvDims D, Fk
     __shared__ int s_isfetch[kMaxK];
     __shared__ int s_free[2 * kMaxK];
     __shared__ unsigned char s_used[2 * kMaxK];
+    __shared__ uint32_t s_qa[kMaxG * kHeadDim / 2], s_qb[kMaxG * kHeadDim / 2];
+    extern __shared__ float s_sc[];  // [G][n_page_max] scores of this unit (candidates only)
 
-    // ---- a1: correction (CFR-10), threads 0..G-1, sequential over channels
+    // ---- a1: correction (CFR-10).  q_i and q_{i-1} of the group are staged in shared
+    // memory with coalesced loads; threads 0..G-1 then run the sequential channel sums.
+    {
+        const uint32_t* qa32 = reinterpret_cast<const uint32_t*>(q + ((size_t)b * D.n_qo + m * G) * kHeadDim);
+        const uint32_t* qb32 = reinterpret_cast<const uint32_t*>(L.q_prev + ((size_t)b * D.n_qo + m * G) * kHeadDim);
+        for (int i = tid; i < G * kHeadDim / 2; i += blockDim.x) {
+            s_qa[i] = qa32[i];
+            s_qb[i] = qb32[i];
+        }
+    }
+    __syncthreads();
     if (tid < G) {
-        const uint16_t* qa = q + ((size_t)b * D.n_qo + m * G + tid) * kHeadDim;
-        const uint16_t* qb = L.q_prev + ((size_t)b * D.n_qo + m * G + tid) * kHeadDim;
+        const uint16_t* qa = reinterpret_cast<const uint16_t*>(s_qa) + tid * kHeadDim;
+        const uint16_t* qb = reinterpret_cast<const uint16_t*>(s_qb) + tid * kHeadDim;
         float dot = 0.0f, n1 = 0.0f, n2 = 0.0f;
+#pragma unroll 16
         for (int c = 0; c < kHeadDim; ++c) {
             const float x = bf16f(qa[c]), y = bf16f(qb[c]);
             dot = __fmaf_rn(x, y, dot);  // exact product, one rounding = fl(dot + x*y)
@@ -179,23 +249,38 @@ __global__ void __launch_bounds__(1024) fkv_select_finalize_kernel(FkvDims D, Fk
         __syncthreads();
     } else {
         const size_t srow = (size_t)D.n_page_max;
-        const float* su = scores + (size_t)u * G * srow;
+        {
+            const float* sg = scores + (size_t)u * G * srow;
+            for (int j = n_sink + tid; j < n_off; j += blockDim.x) {
+                float v[kMaxG];  // all heads' loads in flight together
+#pragma unroll
+                for (int g = 0; g < kMaxG; ++g)
+                    if (g < G) v[g] = sg[g * srow + j];
+#pragma unroll
+                for (int g = 0; g < kMaxG; ++g)
+                    if (g < G) s_sc[g * srow + j] = v[g];
+            }
+        }
+        __syncthreads();
+        const float* su = s_sc;
         const int jb = tid * LPT;
         // ---- CFR-4: max per head
         float mx[kMaxG];
 #pragma unroll
         for (int g = 0; g < kMaxG; ++g) mx[g] = -INFINITY;
-        for (int g = 0; g < G; ++g)
 #pragma unroll
-            for (int l = 0; l < LPT; ++l) {
-                const int j = jb + l;
-                if (j >= n_sink && j < n_off) mx[g] = fmaxf(mx[g], su[g * srow + j]);
+        for (int g = 0; g < kMaxG; ++g) {
+            if (g < G) {
+#pragma unroll
+                for (int l = 0; l < LPT; ++l) {
+                    const int j = jb + l;
+                    if (j >= n_sink && j < n_off) mx[g] = fmaxf(mx[g], su[g * srow + j]);
+                }
+                float v = mx[g];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+                if (lane == 0) s_red[warp][g] = v;
             }
-        for (int g = 0; g < G; ++g) {
-            float v = mx[g];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-            if (lane == 0) s_red[warp][g] = v;
         }
         __syncthreads();
         if (warp == 0) {
@@ -384,16 +469,32 @@ __global__ void __launch_bounds__(1024) fkv_select_finalize_kernel(FkvDims D, Fk
             }
             nf += __popc(bal);
         }
-        if (lane == 0) L.n_fetch[u] = nf;
+        if (lane == 0) {
+            L.n_fetch[u] = nf;
+            L.pend_cnt[u] = cnt;
+        }
     }
 }
 
 template <int G>
 static void launch_score_g(const FkvDims& D, const FkvLayer& L, float* scores, const uint16_t* q, int max_n_off,
                            cudaStream_t s) {
-    const int gy = (max_n_off + 127) / 128;
-    if (gy <= 0) return;
-    fkv_score_kernel<G><<<dim3(D.U, gy), 128, 0, s>>>(D, L, scores, q);
+    const int blk_lo = D.n_sink / 32;
+    const int nb_act = (max_n_off + 31) / 32 - blk_lo;
+    if (nb_act <= 0) return;
+    const int smem = 2 * kSummBlockBytes + G * kHeadDim * 2 * 4;
+    static int max_ctas = 0;
+    if (!max_ctas) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(fkv_score_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fkv_score_kernel<G>, kScoreWarps * 32, smem);
+        max_ctas = sms * (per_sm > 0 ? per_sm : 1);
+    }
+    const long long n = (long long)D.U * nb_act;
+    const int grid = (int)std::min<long long>(max_ctas, n);
+    fkv_score_kernel<G><<<grid, kScoreWarps * 32, smem, s>>>(D, L, scores, q, blk_lo, nb_act);
 }
 
 cudaError_t launch_score(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
@@ -412,18 +513,32 @@ cudaError_t launch_score(const FkvDims& D, const FkvLayer& L, const FkvScratch& 
     return cudaGetLastError();
 }
 
+template <int LPT>
+static cudaError_t launch_fin(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
+                              int32_t* pages_out, uint8_t* corrected_out, size_t smem, cudaStream_t s) {
+    static size_t configured = 0;
+    if (smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(fkv_select_finalize_kernel<LPT>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    fkv_select_finalize_kernel<LPT><<<D.U, 1024, smem, s>>>(D, L, X.scores, q, pages_out, corrected_out);
+    return cudaGetLastError();
+}
+
 // lpt = leaves per thread of the 1024-thread tree; 1024 * lpt >= next_pow2(n_off) for every n_off the
 // handle can reach (a larger zero-padded tree gives the same Z, CFR-6).
 cudaError_t launch_finalize(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                             int32_t* pages_out, uint8_t* corrected_out, int lpt, cudaStream_t s) {
+    const size_t smem = (size_t)D.G * D.n_page_max * sizeof(float);
     switch (lpt) {
-        case 1: fkv_select_finalize_kernel<1><<<D.U, 1024, 0, s>>>(D, L, X.scores, q, pages_out, corrected_out); break;
-        case 2: fkv_select_finalize_kernel<2><<<D.U, 1024, 0, s>>>(D, L, X.scores, q, pages_out, corrected_out); break;
-        case 4: fkv_select_finalize_kernel<4><<<D.U, 1024, 0, s>>>(D, L, X.scores, q, pages_out, corrected_out); break;
-        case 8: fkv_select_finalize_kernel<8><<<D.U, 1024, 0, s>>>(D, L, X.scores, q, pages_out, corrected_out); break;
+        case 1: return launch_fin<1>(D, L, X, q, pages_out, corrected_out, smem, s);
+        case 2: return launch_fin<2>(D, L, X, q, pages_out, corrected_out, smem, s);
+        case 4: return launch_fin<4>(D, L, X, q, pages_out, corrected_out, smem, s);
+        case 8: return launch_fin<8>(D, L, X, q, pages_out, corrected_out, smem, s);
         default: return cudaErrorInvalidValue;
     }
-    return cudaGetLastError();
 }
 
 }  // namespace fkv

@@ -147,3 +147,52 @@ def test_parity_short_context_ragged():
 def test_parity_long_context_many_tiles():
     """|J| > 1024 exercises the multi-leaf-per-thread tree and radix select."""
     run_parity(G=4, n_kv=1, batch=1, page=16, sink=64, window=64, budget=640, L0=20000, steps=3, n_layers=1)
+
+
+def test_step_graph_matches_eager():
+    """Whole-step CUDA graphs (two graphs joined by external event nodes) give the
+    same selections and bit-identical outputs as the eager per-layer calls."""
+    _need_gpu()
+    import paper_2505_13109_b200 as P
+    nb, n_kv, G, d, p, L0, steps, n_layers = 2, 2, 4, 128, 32, 1200, 6, 3
+    n_qo = G * n_kv
+    mk = lambda: P.FreeKV(P.FreeKVConfig(n_layers=n_layers, batch=nb, n_qo=n_qo, n_kv=n_kv, budget_tokens=256,
+                                         sink_tokens=64, window_tokens=64, max_ctx_tokens=L0 + steps + 2))
+    a, b = mk(), mk()
+    dev = a.device
+    seed = 77
+    for layer in range(n_layers):
+        k, v = synth.gen_prefill(nb, n_kv, d, p, L0, 2, a.K, seed, layer, device=dev)
+        torch.cuda.synchronize()
+        a.append_kv(layer, k, v)
+        b.append_kv(layer, k, v)
+        a.synchronize()
+        b.synchronize()
+    qps = [synth.QueryProcess(nb, n_qo, n_kv, d, seed, l, device=dev, event_rate=0.3) for l in range(n_layers)]
+    Q = torch.empty(steps, n_layers, nb, n_qo, d, dtype=torch.bfloat16, device=dev)
+    Kn = torch.empty(steps, n_layers, nb, 1, n_kv, d, dtype=torch.bfloat16, device=dev)
+    Vn = torch.empty_like(Kn)
+    for i in range(steps):
+        for l in range(n_layers):
+            q, _ = qps[l].next()
+            kn, vn = synth.gen_decode_kv(nb, n_kv, d, p, L0 + i, seed, l, device=dev)
+            Q[i, l], Kn[i, l], Vn[i, l] = q, kn, vn
+    torch.cuda.synchronize()
+    qb, kb, vb = torch.empty_like(Q[0]), torch.empty_like(Kn[0]), torch.empty_like(Vn[0])
+    ob = torch.empty(n_layers, nb, n_qo, d, dtype=torch.float32, device=dev)
+    b.synchronize()
+    b.step_graph_capture(qb, kb, vb, ob)
+    oa = torch.empty(nb, n_qo, d, dtype=torch.float32, device=dev)
+    for i in range(steps):
+        with torch.cuda.stream(b.stream):
+            qb.copy_(Q[i]); kb.copy_(Kn[i]); vb.copy_(Vn[i])
+        b.step_graph_launch()
+        b.synchronize()
+        for l in range(n_layers):
+            a.decode_step(l, Q[i, l], Kn[i, l], Vn[i, l], oa)
+            a.synchronize()
+            sa, sb = a.get_selection(l), b.get_selection(l)
+            assert np.array_equal(sa["pages"], sb["pages"]) and np.array_equal(sa["flags"], sb["flags"]), (i, l)
+            assert torch.equal(oa, ob[l]), (i, l)
+    a.close()
+    b.close()

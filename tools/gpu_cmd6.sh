@@ -1,0 +1,11 @@
+python -c "import __graft_entry__ as g; g.build()"
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest6.log 2>&1; echo "rc=$?" >> gpurun_out/pytest6.log
+K="python tools/kbench.py --layers 2 --steps 20 --warmup 5"
+timeout 300 $K > gpurun_out/kb6_par.json 2>&1
+K2="python tools/kbench.py --layers 2 --steps 2 --warmup 5 --no-profile"
+timeout 300 $K2 > gpurun_out/kb6_plain.log 2>&1 && \
+timeout 600 ncu -k regex:fkv_ --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s 72 -c 28 --csv --log-file gpurun_out/kb6_launches.csv $K2 > gpurun_out/ncu6.log 2>&1 && \
+timeout 600 ncu -k regex:fkv_select_finalize --set full --import-source on --clock-control none -s 10 -c 1 -o gpurun_out/fin_r1 $K2 > gpurun_out/ncu6b.log 2>&1 && \
+timeout 600 ncu -k regex:fkv_attn_split --set full --import-source on --clock-control none -s 10 -c 1 -o gpurun_out/attn_r1b $K2 > gpurun_out/ncu6c.log 2>&1 && \
+timeout 600 ncu -k regex:fkv_score --set full --import-source on --clock-control none -s 10 -c 1 -o gpurun_out/score_r1b $K2 > gpurun_out/ncu6d.log 2>&1
+echo "rc=$?" >> gpurun_out/ncu6.log

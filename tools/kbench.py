@@ -1,0 +1,63 @@
+"""Kernel micro-bench at c2 (Llama-3.1-8B shape, 32K ctx, batch 8) with few layers:
+per-kernel device time from the library's event profiler.  Used for fast
+build -> measure iterations and as the ncu target."""
+import argparse, json, os, sys, time
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch
+import paper_2505_13109_b200 as P
+import synth
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--layers", type=int, default=2)
+ap.add_argument("--steps", type=int, default=20)
+ap.add_argument("--warmup", type=int, default=5)
+ap.add_argument("--ctx", type=int, default=32768)
+ap.add_argument("--batch", type=int, default=8)
+ap.add_argument("--n_qo", type=int, default=32)
+ap.add_argument("--n_kv", type=int, default=8)
+ap.add_argument("--event_rate", type=float, default=0.05)
+ap.add_argument("--no-profile", action="store_true")
+a = ap.parse_args()
+dev = torch.device("cuda", 0)
+nb, nq, nk, d, p = a.batch, a.n_qo, a.n_kv, 128, 32
+G = nq // nk
+cfg = P.FreeKVConfig(n_layers=a.layers, batch=nb, n_qo=nq, n_kv=nk, max_ctx_tokens=a.ctx + a.warmup + a.steps + 2)
+fkv = P.FreeKV(cfg)
+s = fkv.stream
+seed = synth.SEED0 + 2
+with torch.cuda.stream(s):
+    for l in range(a.layers):
+        k, v = synth.gen_prefill(nb, nk, d, p, a.ctx, 16, cfg.K, seed, l, device=dev)
+        fkv.append_kv(l, k, v)
+        del k, v
+    qps = [synth.QueryProcess(nb, nq, nk, d, seed, l, device=dev, event_rate=a.event_rate) for l in range(a.layers)]
+    T = a.warmup + a.steps
+    Q = torch.empty(T, a.layers, nb, nq, d, dtype=torch.bfloat16, device=dev)
+    Kn = torch.empty(T, a.layers, nb, 1, nk, d, dtype=torch.bfloat16, device=dev)
+    Vn = torch.empty_like(Kn)
+    for i in range(T):
+        for l in range(a.layers):
+            q, _ = qps[l].next()
+            kn, vn = synth.gen_decode_kv(nb, nk, d, p, a.ctx + i, seed, l, device=dev)
+            Q[i, l], Kn[i, l], Vn[i, l] = q, kn, vn
+out = torch.empty(nb, nq, d, dtype=torch.float32, device=dev)
+s.synchronize()
+for i in range(a.warmup):
+    for l in range(a.layers):
+        fkv.decode_step(l, Q[i, l], Kn[i, l], Vn[i, l], out)
+fkv.synchronize()
+if not a.no_profile:
+    fkv.profile_begin(a.steps * a.layers * 8 + 16)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(s)
+for i in range(a.warmup, T):
+    for l in range(a.layers):
+        fkv.decode_step(l, Q[i, l], Kn[i, l], Vn[i, l], out)
+e1.record(s)
+fkv.synchronize()
+res = {"us_per_layer": e0.elapsed_time(e1) * 1e3 / (a.steps * a.layers)}
+if not a.no_profile:
+    prof = fkv.profile_end()
+    res["kernels_us"] = {k: round(v[0] / max(v[1], 1) * 1e3, 2) for k, v in prof.items()}
+print(json.dumps(res))
