@@ -149,16 +149,18 @@ def run_ours(args, c, rank, world, local_rank):
     seed = args.seed if args.seed is not None else synth.SEED0 + 1 + list(CONFIGS).index(args.config)
     n_kv, n_qo, nb, d = c["n_kv"], c["n_qo"], c["batch"], 128
     G = n_qo // n_kv
-    # KV-head sharding: contiguous blocks of n_kv / world heads per rank
-    assert n_kv % world == 0, "ranks must divide n_kv"
-    kv_loc = n_kv // world
-    kv0 = rank * kv_loc
+    # KV-head (then batch) sharding, SURVEY §8(e)
+    from paper_2505_13109_b200.shard import shard_for
+    sh = shard_for(n_kv, nb, world, rank)
+    kv_loc, kv0 = sh.n_kv, sh.kv_begin
+    b0, b1 = sh.batch_begin, sh.batch_end
+    nb_loc = sh.batch
     n_layers = c["n_layers"]
     total_steps = args.warmup + 1 + args.steps + args.profile_steps + args.steps  # warm, timed, profiled, e2e
     max_ctx = c["ctx"] + total_steps + 1
     stream = torch.cuda.Stream(dev)
     t0 = time.time()
-    cfg, fkv = build_handle(P, c, kv_loc, kv_loc * G, max_ctx, stream)
+    cfg, fkv = build_handle(P, dict(c, batch=nb_loc), kv_loc, kv_loc * G, max_ctx, stream)
     t_alloc = time.time() - t0
     K = cfg.K
     p = 32
@@ -167,26 +169,27 @@ def run_ours(args, c, rank, world, local_rank):
     with torch.cuda.stream(stream):
         for layer in range(n_layers):
             k, v = synth.gen_prefill(nb, n_kv, d, p, c["ctx"], c["sink"] // p, K, seed, layer, device=dev)
-            fkv.append_kv(layer, k[:, :, kv0:kv0 + kv_loc].contiguous(), v[:, :, kv0:kv0 + kv_loc].contiguous())
+            fkv.append_kv(layer, k[b0:b1, :, kv0:kv0 + kv_loc].contiguous(),
+                          v[b0:b1, :, kv0:kv0 + kv_loc].contiguous())
             del k, v
     stream.synchronize()
     t_prefill = time.time() - t0
     # ---- pre-generate every step's inputs (GEN-Q / GEN-S) outside the timed regions
     qps = [synth.QueryProcess(nb, n_qo, n_kv, d, seed, layer, device=dev, event_rate=c["event_rate"])
            for layer in range(n_layers)]
-    Qs = torch.empty(total_steps, n_layers, nb, kv_loc * G, d, dtype=torch.bfloat16, device=dev)
-    Ks = torch.empty(total_steps, n_layers, nb, 1, kv_loc, d, dtype=torch.bfloat16, device=dev)
+    Qs = torch.empty(total_steps, n_layers, nb_loc, kv_loc * G, d, dtype=torch.bfloat16, device=dev)
+    Ks = torch.empty(total_steps, n_layers, nb_loc, 1, kv_loc, d, dtype=torch.bfloat16, device=dev)
     Vs = torch.empty_like(Ks)
     with torch.cuda.stream(stream):
         for i in range(total_steps):
             for layer in range(n_layers):
                 q, _ = qps[layer].next()
                 kn, vn = synth.gen_decode_kv(nb, n_kv, d, p, c["ctx"] + i, seed, layer, device=dev)
-                Qs[i, layer] = q[:, kv0 * G:(kv0 + kv_loc) * G]
-                Ks[i, layer] = kn[:, :, kv0:kv0 + kv_loc]
-                Vs[i, layer] = vn[:, :, kv0:kv0 + kv_loc]
-    out_loc = [torch.empty(nb, kv_loc * G, d, dtype=torch.float32, device=dev) for _ in range(n_layers)]
-    out_full = [torch.empty(world, nb, kv_loc * G, d, dtype=torch.float32, device=dev) for _ in range(n_layers)] \
+                Qs[i, layer] = q[b0:b1, kv0 * G:(kv0 + kv_loc) * G]
+                Ks[i, layer] = kn[b0:b1, :, kv0:kv0 + kv_loc]
+                Vs[i, layer] = vn[b0:b1, :, kv0:kv0 + kv_loc]
+    out_loc = [torch.empty(nb_loc, kv_loc * G, d, dtype=torch.float32, device=dev) for _ in range(n_layers)]
+    out_full = [torch.empty(world, nb_loc, kv_loc * G, d, dtype=torch.float32, device=dev) for _ in range(n_layers)] \
         if world > 1 else None
     stream.synchronize()
 
@@ -199,7 +202,7 @@ def run_ours(args, c, rank, world, local_rank):
 
     # whole-step graph: fixed input/output buffers, one replay per step
     q_buf, k_buf, v_buf = torch.empty_like(Qs[0]), torch.empty_like(Ks[0]), torch.empty_like(Vs[0])
-    o_buf = torch.empty(n_layers, nb, kv_loc * G, d, dtype=torch.float32, device=dev)
+    o_buf = torch.empty(n_layers, nb_loc, kv_loc * G, d, dtype=torch.float32, device=dev)
 
     def graph_step(i):
         with torch.cuda.stream(stream):
@@ -247,15 +250,21 @@ def run_ours(args, c, rank, world, local_rank):
         t = torch.tensor([ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    # ---- profiled pass: per-kernel device time for the roofline + recall statistics
-    fkv.profile_begin(args.profile_steps * n_layers * 8 + 64)
-    fetched = 0
-    flagged = 0
-    units = 0
-    t_unit_tokens = 0
-    j_pages = 0
+    # ---- profiled pass: per-kernel device time (CUDA events captured as graph nodes on the
+    # stream each kernel is launched on) + recall / correction statistics
+    import paper_2505_13109_b200.freekv as FK
+    prof = {kc: [0.0, 0] for kc in FK.KERNEL_CLASSES}
+    if not args.eager:
+        fkv.step_graph_capture(q_buf, k_buf, v_buf, o_buf, profile=True)
+    else:
+        fkv.profile_begin(args.profile_steps * n_layers * 8 + 64)
+    fetched = flagged = units = t_unit_tokens = j_pages = 0
     for _ in range(args.profile_steps):
-        one_step(step)
+        run(step)
+        if not args.eager:
+            for kc, (t, n) in fkv.step_graph_profile().items():
+                prof[kc][0] += t
+                prof[kc][1] += n
         for layer in range(n_layers):
             n_fetch, _ = fkv.get_fetch(layer)
             sel = fkv.get_selection(layer)
@@ -265,17 +274,21 @@ def run_ours(args, c, rank, world, local_rank):
             Lc = fkv.context(layer)
             n_off = max(c["sink"] // p, Lc // p - c["window"] // p)
             n_sel = (sel["pages"] >= 0).sum(axis=1)
-            # |T| per unit = sink + selected pages + local [f*p, Lc) with f the frontier in use (A-9)
+            # |T| per unit = sink + selected pages + local [f*p, Lc) (A-9); f = this step's frontier
             f_used = sel["frontier"].astype(np.int64)
             t_unit_tokens += int((min(c["sink"], Lc) + n_sel * p + (Lc - f_used * p)).sum())
             j_pages += fkv.U * (n_off - c["sink"] // p)
         step += 1
-    prof = fkv.profile_end()
+    if args.eager:
+        prof = {k: list(v) for k, v in fkv.profile_end().items()}
+    else:
+        fkv.step_graph_capture(q_buf, k_buf, v_buf, o_buf, profile=False)
+    prof = {k: tuple(v) for k, v in prof.items()}
     # ---- end-to-end pass: inputs from pinned host memory, outputs back to host, every step
     Qh = Qs[step:step + args.steps].cpu().pin_memory()
     Kh = Ks[step:step + args.steps].cpu().pin_memory()
     Vh = Vs[step:step + args.steps].cpu().pin_memory()
-    host_out = torch.empty(n_layers, nb, kv_loc * G, d, dtype=torch.float32, pin_memory=True)
+    host_out = torch.empty(n_layers, nb_loc, kv_loc * G, d, dtype=torch.float32, pin_memory=True)
     h2d = (Qh[0].numel() + Kh[0].numel() + Vh[0].numel()) * 2
     d2h = host_out.numel() * 4
     barrier()
@@ -306,7 +319,7 @@ def run_ours(args, c, rank, world, local_rank):
     link = host_link_peak(torch) if rank == 0 else None
     res = dict(ms=ms, ms_e2e=ms_e2e, prof=prof, fetched=fetched, flagged=flagged, units=units,
                t_unit_tokens=t_unit_tokens, j_pages=j_pages, clocks=clk, link=link, t_alloc=t_alloc,
-               t_prefill=t_prefill, h2d=h2d, d2h=d2h, K=K, G=G, kv_loc=kv_loc, seed=seed)
+               t_prefill=t_prefill, h2d=h2d, d2h=d2h, K=K, G=G, kv_loc=kv_loc, nb_loc=nb_loc, seed=seed)
     fkv.close()
     return res
 
@@ -360,7 +373,7 @@ def main():
     cfg_out = {"workload": c["workload"], "n_layers": c["n_layers"], "batch": c["batch"], "n_qo": c["n_qo"],
                "n_kv": c["n_kv"], "ctx": c["ctx"], "page": 32, "budget": c["budget"], "sink": c["sink"],
                "window": c["window"], "tau": c["tau"], "correction_event_rate": c["event_rate"],
-               "parallelism": f"kv-head shard x{args.gpus}", "l2": "inputs larger than L2 (~100 MB per layer, "
+               "parallelism": f"kv-head/batch shard x{args.gpus} + per-layer NCCL all-gather of head outputs", "l2": "inputs larger than L2 (~100 MB per layer, "
                f"{c['n_layers']} layers per step)", "seed": seed}
     if args.impl == "reference":
         if rank != 0:
@@ -387,10 +400,11 @@ def main():
     prof = r["prof"]
     d = 128
     G = r["G"]
-    units_per_launch = c["batch"] * r["kv_loc"]
+    units_per_launch = r["nb_loc"] * r["kv_loc"]
     # algorithmic bytes: attention reads |T|*2*d*2 B KV + G*d*2 B q per unit
     attn_ms, attn_n = prof["attn_split"]
-    attn_bytes = r["t_unit_tokens"] * 2 * d * 2 + attn_n * units_per_launch * G * d * 2
+    attn_steps = attn_n // 2  # two phases per layer-step (unflagged, corrected); bytes per layer-step
+    attn_bytes = r["t_unit_tokens"] * 2 * d * 2 + max(attn_steps, 1) * units_per_launch * G * d * 2
     attn_gbs = attn_bytes / (attn_ms / 1e3) / 1e9 if attn_ms > 0 else 0.0
     sc_ms, sc_n = prof["score"]
     sc_bytes = r["j_pages"] * 2 * d * 2 + sc_n * units_per_launch * G * d * 2
@@ -402,9 +416,10 @@ def main():
                    "us_avg": round(v[0] / v[1] * 1e3, 3) if v[1] else None} for k, v in prof.items()}
     dominant = "attn_split" if attn_ms >= sc_ms else "score"
     if dominant == "attn_split":
-        roof = {"kernel": "fkv_attn_split_kernel", "bound": "hbm", "achieved": round(attn_gbs, 1), "peak": hbm_peak,
+        roof = {"kernel": "fkv_attn_split_kernel (both phases of a layer-step)", "bound": "hbm",
+                "achieved": round(attn_gbs, 1), "peak": hbm_peak,
                 "unit": "GB/s", "frac": round(attn_gbs / hbm_peak, 4), "traffic": None,
-                "algorithmic_bytes_per_launch": int(attn_bytes / max(attn_n, 1))}
+                "algorithmic_bytes_per_layer_step": int(attn_bytes / max(attn_steps, 1))}
     else:
         roof = {"kernel": "fkv_score_kernel", "bound": "hbm", "achieved": round(sc_gbs, 1), "peak": hbm_peak,
                 "unit": "GB/s", "frac": round(sc_gbs / hbm_peak, 4), "traffic": None,

@@ -149,8 +149,13 @@ freekv_status freekv_decode_step(freekv_handle* h, int32_t layer, const void* q,
  * replays for every later step.  step_graph_launch replays one step on the
  * handle's streams (ERANGE when the context would exceed max_ctx_tokens). */
 freekv_status freekv_step_graph_capture(freekv_handle* h, const void* q_all, const void* k_all,
-                                        const void* v_all, float* out_all);
+                                        const void* v_all, float* out_all, int32_t profile);
 freekv_status freekv_step_graph_launch(freekv_handle* h);
+/* With profile != 0 at capture, every kernel node is bracketed by event-record
+ * nodes; after a replay has completed, this returns per kernel class the summed
+ * device milliseconds and launch counts of that replay (classes as in
+ * freekv_profile_end).  Blocking. */
+freekv_status freekv_step_graph_profile(freekv_handle* h, float* ms /*[7]*/, int32_t* launches /*[7]*/);
 
 /* Inspection (blocking; host outputs).  All arrays u-major. */
 freekv_status freekv_get_selection(freekv_handle* h, int32_t layer, int32_t* pages /*[U][K]*/,

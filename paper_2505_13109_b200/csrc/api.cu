@@ -10,6 +10,8 @@
 // Background recall of layer l overlaps the rest of step i and the start of
 // step i+1 (PAPER.md P:221-225 speculative retrieval; P:320-324 streamed
 // recall).  No host synchronisation on the path.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -40,6 +42,8 @@ static freekv_status fail(freekv_status st, const std::string& msg) {
     } while (0)
 
 struct freekv_handle {
+    alignas(64) CUtensorMap tmap_kv;  // the device arena as a 2D tensor of 256-byte rows (TMA)
+    const uint16_t* arena = nullptr;
     freekv_config cfg;
     FkvDims D;
     std::vector<FkvLayer> layers;
@@ -60,6 +64,7 @@ struct freekv_handle {
     // whole-step graphs (freekv_step_graph_capture / launch)
     bool capturing = false;
     cudaGraphExec_t g_compute = nullptr, g_recall = nullptr;
+    std::vector<Rec> graph_recs;  // event pairs captured into the step graph (profile mode)
 };
 
 namespace {
@@ -188,9 +193,11 @@ template <class F>
 cudaError_t timed(freekv_handle* h, int cls, cudaStream_t s, F&& launch) {
     if (!h->prof || h->prof_used + 2 > h->prof_pool.size()) return launch();
     cudaEvent_t a = h->prof_pool[h->prof_used++], b = h->prof_pool[h->prof_used++];
-    cudaError_t e = cudaEventRecord(a, s);
+    // under stream capture only "external" records become real event-record graph nodes
+    const unsigned fl = h->capturing ? cudaEventRecordExternal : 0u;
+    cudaError_t e = cudaEventRecordWithFlags(a, s, fl);
     if (e == cudaSuccess) e = launch();
-    if (e == cudaSuccess) e = cudaEventRecord(b, s);
+    if (e == cudaSuccess) e = cudaEventRecordWithFlags(b, s, fl);
     h->prof_recs.push_back({cls, a, b});
     return e;
 }
@@ -208,23 +215,29 @@ freekv_status do_append(freekv_handle* h, int layer, const void* k, const void* 
     return FREEKV_OK;
 }
 
+// k_new/v_new non-NULL: the decode step's single-token append is fused into the
+// finalize kernel (requires W >= p so the summaries of this step's candidates were
+// written at page completion in earlier steps; append_unit.cuh).
 freekv_status do_select(freekv_handle* h, int layer, const void* q, int32_t* pages_out, uint8_t* corr_out,
-                        cudaStream_t s) {
+                        cudaStream_t s, const void* k_new = nullptr, const void* v_new = nullptr) {
     if (!q) return fail(FREEKV_EINVAL, "q is NULL");
-    if (h->ctx_host[layer] <= 0) return fail(FREEKV_ESTATE, "select before any token was appended");
+    const int pending = k_new ? 1 : 0;
+    if (h->ctx_host[layer] + pending <= 0) return fail(FREEKV_ESTATE, "select before any token was appended");
     // the background recall of the previous step reads this layer's fetch list
     if (h->capturing)
         FKV_CUDA(cudaStreamWaitEvent(s, h->ev_recall[layer], cudaEventWaitExternal));
     else if (h->recall_pending[layer])
         FKV_CUDA(cudaStreamWaitEvent(s, h->ev_recall[layer], 0));
-    const int mno = h->capturing ? max_n_off(h->D, h->D.max_ctx) : max_n_off(h->D, h->ctx_host[layer]);
+    const int mno = h->capturing ? max_n_off(h->D, h->D.max_ctx) : max_n_off(h->D, h->ctx_host[layer] + pending);
     if (h->capturing || mno - h->D.n_sink > h->D.K)
         FKV_CUDA(timed(h, K_SCORE, s, [&] {
-            return launch_score(h->D, h->layers[layer], h->X, (const uint16_t*)q, mno, s);
+            return launch_score(h->D, h->layers[layer], h->X, (const uint16_t*)q, mno, pending, s);
         }));
     FKV_CUDA(timed(h, K_FINALIZE, s, [&] {
-        return launch_finalize(h->D, h->layers[layer], h->X, (const uint16_t*)q, pages_out, corr_out, h->lpt, s);
+        return launch_finalize(h->D, h->layers[layer], h->X, (const uint16_t*)q, (const uint16_t*)k_new,
+                               (const uint16_t*)v_new, pages_out, corr_out, h->lpt, s);
     }));
+    if (k_new && !h->capturing) h->ctx_host[layer] += 1;
     return FREEKV_OK;
 }
 
@@ -249,7 +262,7 @@ freekv_status do_recall(freekv_handle* h, int layer, cudaStream_t s) {
 freekv_status do_attn(freekv_handle* h, int layer, const void* q, float* out, cudaStream_t s) {
     if (!q || !out) return fail(FREEKV_EINVAL, "q/out is NULL");
     FKV_CUDA(timed(h, K_ATTN_SPLIT, s, [&] {
-        return launch_attn_split(h->D, h->layers[layer], h->X, (const uint16_t*)q, 0, s);
+        return launch_attn_split(h->D, h->layers[layer], h->X, (const uint16_t*)q, 0, h->tmap_kv, h->arena, s);
     }));
     FKV_CUDA(timed(h, K_ATTN_COMBINE, s, [&] {
         return launch_attn_combine(h->D, h->layers[layer], h->X, (const uint16_t*)q, out, s);
@@ -270,9 +283,10 @@ freekv_status do_step_tail(freekv_handle* h, int layer, const void* q, float* ou
     FKV_CUDA(cudaEventRecord(h->ev_select[layer], cs));
     FKV_CUDA(cudaStreamWaitEvent(h->ss, h->ev_select[layer], 0));
     FKV_CUDA(timed(h, K_RECALL_SYNC, h->ss, [&] { return launch_recall(D, L, 1, h->ss); }));
+    if (h->capturing)  // external record first: the internal record below joins every ss node back into cs
+        FKV_CUDA(cudaEventRecordWithFlags(h->ev_sync_x[layer], h->ss, cudaEventRecordExternal));
     FKV_CUDA(cudaEventRecord(h->ev_sync[layer], h->ss));
     if (h->capturing) {
-        FKV_CUDA(cudaEventRecordWithFlags(h->ev_sync_x[layer], h->ss, cudaEventRecordExternal));
     } else if (h->serial_recall) {
         FKV_CUDA(timed(h, K_RECALL_BG, h->ss, [&] { return launch_recall(D, L, 0, h->ss); }));
         FKV_CUDA(cudaEventRecord(h->ev_recall[layer], h->ss));
@@ -283,9 +297,9 @@ freekv_status do_step_tail(freekv_handle* h, int layer, const void* q, float* ou
         FKV_CUDA(cudaEventRecord(h->ev_recall[layer], h->rs));
         h->recall_pending[layer] = 1;
     }
-    FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] { return launch_attn_split(D, L, h->X, (const uint16_t*)q, 1, cs); }));
+    FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] { return launch_attn_split(D, L, h->X, (const uint16_t*)q, 1, h->tmap_kv, h->arena, cs); }));
     FKV_CUDA(cudaStreamWaitEvent(cs, h->ev_sync[layer], 0));
-    FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] { return launch_attn_split(D, L, h->X, (const uint16_t*)q, 2, cs); }));
+    FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] { return launch_attn_split(D, L, h->X, (const uint16_t*)q, 2, h->tmap_kv, h->arena, cs); }));
     FKV_CUDA(timed(h, K_ATTN_COMBINE, cs, [&] {
         return launch_attn_combine(D, L, h->X, (const uint16_t*)q, out, cs);
     }));
@@ -346,6 +360,28 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
     }
     uint8_t* dev = (uint8_t*)bufs->dev;
     uint8_t* hd = (uint8_t*)host_dev;
+    {
+        // TMA descriptor: the arena as [rows][128] bf16, box {64 ch, 16 rows}, 128-byte swizzle
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess || !fn) {
+            delete h;
+            return fail(FREEKV_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+        }
+        const cuuint64_t dims[2] = {(cuuint64_t)kHeadDim, (cuuint64_t)(s.dev_bytes / (kHeadDim * 2))};
+        const cuuint64_t strides[1] = {(cuuint64_t)kHeadDim * 2};
+        const cuuint32_t box[2] = {64, 16};
+        const cuuint32_t estr[2] = {1, 1};
+        CUresult cr = ((PFN_cuTensorMapEncodeTiled)fn)(
+            &h->tmap_kv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dev, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (cr != CUDA_SUCCESS) {
+            delete h;
+            return fail(FREEKV_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
+        }
+        h->arena = (const uint16_t*)dev;
+    }
     h->layers.resize(cfg->n_layers);
     for (int l = 0; l < cfg->n_layers; ++l) {
         uint8_t* base = dev + s.layer_bytes * l;
@@ -479,8 +515,14 @@ freekv_status freekv_decode_step(freekv_handle* h, int32_t layer, const void* q,
     freekv_status st = check_layer(h, layer);
     if (st != FREEKV_OK) return st;
     cudaStream_t s = h->cs;
-    if ((st = do_append(h, layer, k_new, v_new, 1, s)) != FREEKV_OK) return st;
-    if ((st = do_select(h, layer, q, nullptr, nullptr, s)) != FREEKV_OK) return st;
+    if (!k_new || !v_new) return fail(FREEKV_EINVAL, "k_new/v_new is NULL");
+    if (h->ctx_host[layer] + 1 > h->D.max_ctx) return fail(FREEKV_ERANGE, "context would exceed max_ctx_tokens");
+    if (h->D.n_win >= 1) {
+        if ((st = do_select(h, layer, q, nullptr, nullptr, s, k_new, v_new)) != FREEKV_OK) return st;
+    } else {  // W = 0: the page completed by this token is a candidate now -> append first
+        if ((st = do_append(h, layer, k_new, v_new, 1, s)) != FREEKV_OK) return st;
+        if ((st = do_select(h, layer, q, nullptr, nullptr, s)) != FREEKV_OK) return st;
+    }
     return do_step_tail(h, layer, q, out);
 }
 
@@ -606,10 +648,15 @@ static void drop_graphs(freekv_handle* h) {
 }
 
 freekv_status freekv_step_graph_capture(freekv_handle* h, const void* q_all, const void* k_all, const void* v_all,
-                                        float* out_all) {
+                                        float* out_all, int32_t profile) {
     if (!h) return fail(FREEKV_EINVAL, "handle is NULL");
     if (!q_all || !k_all || !v_all || !out_all) return fail(FREEKV_EINVAL, "NULL buffer");
     if (h->prof) return fail(FREEKV_ESTATE, "capture while profiling");
+    h->graph_recs.clear();
+    if (profile) {  // event pool: <= 8 kernels per layer, 2 events each
+        freekv_status ps = freekv_profile_begin(h, h->cfg.n_layers * 8 + 8);
+        if (ps != FREEKV_OK) return ps;
+    }
     for (int l = 0; l < h->cfg.n_layers; ++l)
         if (h->ctx_host[l] <= 0) return fail(FREEKV_ESTATE, "capture before the first append of every layer");
     freekv_status st = sync_both(h);
@@ -625,8 +672,12 @@ freekv_status freekv_step_graph_capture(freekv_handle* h, const void* q_all, con
         const uint8_t* q = (const uint8_t*)q_all + q_stride * l;
         const uint8_t* k = (const uint8_t*)k_all + kv_stride * l;
         const uint8_t* v = (const uint8_t*)v_all + kv_stride * l;
-        e = launch_append(D, h->layers[l], (const uint16_t*)k, (const uint16_t*)v, 1, h->cs);
-        if (e == cudaSuccess) st = do_select(h, l, q, nullptr, nullptr, h->cs);
+        if (D.n_win >= 1) {
+            st = do_select(h, l, q, nullptr, nullptr, h->cs, k, v);
+        } else {
+            e = launch_append(D, h->layers[l], (const uint16_t*)k, (const uint16_t*)v, 1, h->cs);
+            if (e == cudaSuccess) st = do_select(h, l, q, nullptr, nullptr, h->cs);
+        }
         if (st == FREEKV_OK) st = do_step_tail(h, l, q, out_all + o_stride * l);
     }
     cudaError_t e2 = cudaStreamEndCapture(h->cs, &gc);
@@ -635,13 +686,18 @@ freekv_status freekv_step_graph_capture(freekv_handle* h, const void* q_all, con
         e = cudaStreamBeginCapture(h->rs, cudaStreamCaptureModeThreadLocal);
         for (int l = 0; l < h->cfg.n_layers && e == cudaSuccess; ++l) {
             e = cudaStreamWaitEvent(h->rs, h->ev_sync_x[l], cudaEventWaitExternal);
-            if (e == cudaSuccess) e = launch_recall(D, h->layers[l], 0, h->rs);
+            if (e == cudaSuccess) e = timed(h, K_RECALL_BG, h->rs, [&] { return launch_recall(D, h->layers[l], 0, h->rs); });
             if (e == cudaSuccess) e = cudaEventRecordWithFlags(h->ev_recall[l], h->rs, cudaEventRecordExternal);
         }
         e2 = cudaStreamEndCapture(h->rs, &gr);
         if (e == cudaSuccess) e = e2;
     }
     h->capturing = false;
+    if (profile) {
+        h->prof = false;
+        h->graph_recs = h->prof_recs;
+        h->prof_recs.clear();
+    }
     if (e == cudaSuccess && st == FREEKV_OK) e = cudaGraphInstantiate(&h->g_compute, gc, 0);
     if (e == cudaSuccess && st == FREEKV_OK) e = cudaGraphInstantiate(&h->g_recall, gr, 0);
     if (gc) cudaGraphDestroy(gc);
@@ -653,6 +709,26 @@ freekv_status freekv_step_graph_capture(freekv_handle* h, const void* q_all, con
     if (e != cudaSuccess) {
         drop_graphs(h);
         return fail(FREEKV_ECUDA, std::string("step graph capture: ") + cudaGetErrorString(e));
+    }
+    return FREEKV_OK;
+}
+
+freekv_status freekv_step_graph_profile(freekv_handle* h, float* ms, int32_t* launches) {
+    if (!h) return fail(FREEKV_EINVAL, "handle is NULL");
+    if (h->graph_recs.empty()) return fail(FREEKV_ESTATE, "step graph was not captured with profile != 0");
+    freekv_status st = sync_both(h);
+    if (st != FREEKV_OK) return st;
+    float acc[FREEKV_NUM_KERNEL_CLASSES] = {0};
+    int32_t cnt[FREEKV_NUM_KERNEL_CLASSES] = {0};
+    for (auto& r : h->graph_recs) {
+        float t = 0.0f;
+        FKV_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+        acc[r.cls] += t;
+        cnt[r.cls] += 1;
+    }
+    for (int i = 0; i < FREEKV_NUM_KERNEL_CLASSES; ++i) {
+        if (ms) ms[i] = acc[i];
+        if (launches) launches[i] = cnt[i];
     }
     return FREEKV_OK;
 }

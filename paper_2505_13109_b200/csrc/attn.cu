@@ -96,49 +96,65 @@ __device__ __forceinline__ const uint16_t* page_ptr(const FkvDims& D, const FkvL
     return L.ring + ((size_t)u * D.R_loc + (j % D.R_loc)) * pe;
 }
 
-struct Slab {
-    uint4 k[2][4];  // K rows slab*16 + nt*8 + g, channels 32c + 8t .. +7
-    uint4 v[4][2];  // V rows 2t, 2t+1, 2t+8, 2t+9; channels 16g + 8h .. +7
-    int valid;      // valid tokens of this slab (<= 0: empty)
-};
+// ---- TMA staging.  The whole device arena is one 2D tensor of 256-byte rows
+// (128 bf16 channels); a 16-token slab of a page is K rows [row, row+16) and V
+// rows [row+p, row+p+16), fetched as four {64 ch x 16 rows} boxes with the
+// 128-byte swizzle (16-byte chunk c of row r lives at chunk c ^ (r % 8)).  The
+// fragment mapping below is chosen so every quarter-warp LDS.128 hits 8
+// distinct chunks (conflict-free) under that swizzle.
+constexpr int kStages = 3;          // slab stages per warp (2 slabs in flight while one is consumed)
+constexpr int kBoxBytes = 16 * 128; // 16 rows x 64 channels bf16
+constexpr int kSlabBytes = 4 * kBoxBytes;
 
-__device__ __forceinline__ void load_slab(const FkvDims& D, const FkvLayer& L, int u, const UnitMeta& M, int x,
-                                          int g, int t, Slab& S) {
+__device__ __forceinline__ void tma_load_2d(void* smem, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(smem)),
+        "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ uint4 lds128(const uint8_t* p) { return *reinterpret_cast<const uint4*>(p); }
+
+// valid tokens of slab x of unit u (<= 0: empty), and its first K row in the arena tensor
+__device__ __forceinline__ int slab_info(const FkvDims& D, const FkvLayer& L, int u, const UnitMeta& M, int x,
+                                         const uint16_t* arena, int& row) {
     const int spp = D.p >> 4;
     const int pi = x / spp, slab = x - pi * spp;
     int pv;
     const uint16_t* base = page_ptr(D, L, u, M, pi, pv);
-    S.valid = pv - slab * 16;
-    if (S.valid <= 0) return;
-    const uint16_t* Kp = base + (size_t)slab * 16 * kHeadDim;
-    const uint16_t* Vp = base + (size_t)D.p * kHeadDim + (size_t)slab * 16 * kHeadDim;
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) S.k[nt][c] = ldg_stream(Kp + (size_t)(nt * 8 + g) * kHeadDim + 32 * c + 8 * t);
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const int tok = 2 * t + (r & 1) + (r >> 1) * 8;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) S.v[r][h] = ldg_stream(Vp + (size_t)tok * kHeadDim + 16 * g + 8 * h);
-    }
+    row = (int)((base - arena) / kHeadDim) + slab * 16;
+    return pv - slab * 16;
 }
 
-__device__ __forceinline__ void compute_slab(const Slab& S, const uint4 (&qa)[4], float sc, int t, float& m_run,
-                                             float& l_run, float (&oacc)[8][4]) {
-    if (S.valid <= 0) return;
-    // ---- S = Q K^T for two n-tiles of 8 tokens
+__device__ __forceinline__ void issue_slab(const CUtensorMap* map, uint8_t* st, uint64_t* bar, int row, int p) {
+    mbar_expect_tx(bar, kSlabBytes);
+    tma_load_2d(st + 0 * kBoxBytes, map, 0, row, bar);
+    tma_load_2d(st + 1 * kBoxBytes, map, 64, row, bar);
+    tma_load_2d(st + 2 * kBoxBytes, map, 0, row + p, bar);
+    tma_load_2d(st + 3 * kBoxBytes, map, 64, row + p, bar);
+}
+
+__device__ __forceinline__ void compute_slab(const uint8_t* st, int valid, const uint4 (&qa)[2][2], float sc, int g,
+                                             int t, float& m_run, float& l_run, float (&oacc)[8][4]) {
+    // ---- S = Q K^T for two n-tiles of 8 tokens.  Lane (g, t) holds, per 64-channel box b,
+    // channels 64b + 16t .. +16 of token row nt*8 + g (chunks 2t, 2t+1, swizzled by row % 8 = g)
     float s[2][4];
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) s[nt][k] = 0.0f;
+        const int r = nt * 8 + g;
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-            for (int sh = 0; sh < 2; ++sh)
-                mma16816(s[nt], u4get(qa[c], 2 * sh), 0u, u4get(qa[c], 2 * sh + 1), 0u, u4get(S.k[nt][c], 2 * sh),
-                         u4get(S.k[nt][c], 2 * sh + 1));
+        for (int b = 0; b < 2; ++b) {
+            const uint8_t* rowp = st + b * kBoxBytes + r * 128;
+            const uint4 k0 = lds128(rowp + (((2 * t) ^ g) << 4));
+            const uint4 k1 = lds128(rowp + (((2 * t + 1) ^ g) << 4));
+            mma16816(s[nt], qa[b][0].x, 0u, qa[b][0].y, 0u, k0.x, k0.y);
+            mma16816(s[nt], qa[b][0].z, 0u, qa[b][0].w, 0u, k0.z, k0.w);
+            mma16816(s[nt], qa[b][1].x, 0u, qa[b][1].y, 0u, k1.x, k1.y);
+            mma16816(s[nt], qa[b][1].z, 0u, qa[b][1].w, 0u, k1.z, k1.w);
+        }
     }
     // ---- online softmax (row = head g; the 4 lanes of a quad share a row)
     float x[2][2];
@@ -148,7 +164,7 @@ __device__ __forceinline__ void compute_slab(const Slab& S, const uint4 (&qa)[4]
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
             const int tok = nt * 8 + 2 * t + e;
-            x[nt][e] = tok < S.valid ? s[nt][e] * sc : -INFINITY;
+            x[nt][e] = tok < valid ? s[nt][e] * sc : -INFINITY;
             smax = fmaxf(smax, x[nt][e]);
         }
     smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, 1));
@@ -182,13 +198,26 @@ __device__ __forceinline__ void compute_slab(const Slab& S, const uint4 (&qa)[4]
     const __nv_bfloat162 h1 = *reinterpret_cast<const __nv_bfloat162*>(&bh1);
     const uint32_t bl0 = pack_bf16(pv[0][0] - __low2float(h0), pv[0][1] - __high2float(h0));
     const uint32_t bl1 = pack_bf16(pv[1][0] - __low2float(h1), pv[1][1] - __high2float(h1));
+    // ---- V fragments: lane (g, t) reads tokens 2t, 2t+1, 2t+8, 2t+9 and, in box g / 4, the
+    // chunks g % 4 (m-tiles 0-3) and g % 4 + 4 (m-tiles 4-7), swizzled by row % 8
+    uint4 vr[4][2];
+    {
+        const uint8_t* vb = st + 2 * kBoxBytes + (g >> 2) * kBoxBytes;
+        const int c0 = g & 3;
+#pragma unroll
+        for (int ri = 0; ri < 4; ++ri) {
+            const int r = 2 * t + (ri & 1) + (ri >> 1) * 8;
+            vr[ri][0] = lds128(vb + r * 128 + ((c0 ^ (r & 7)) << 4));
+            vr[ri][1] = lds128(vb + r * 128 + (((c0 + 4) ^ (r & 7)) << 4));
+        }
+    }
     // ---- O^T += V^T P^T over 8 m-tiles of 16 channels
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {
-        const uint32_t x0 = u4get(S.v[0][mt >> 2], mt & 3);  // token 2t
-        const uint32_t x1 = u4get(S.v[1][mt >> 2], mt & 3);  // token 2t+1
-        const uint32_t x8 = u4get(S.v[2][mt >> 2], mt & 3);  // token 2t+8
-        const uint32_t x9 = u4get(S.v[3][mt >> 2], mt & 3);  // token 2t+9
+        const uint32_t x0 = u4get(vr[0][mt >> 2], mt & 3);  // token 2t
+        const uint32_t x1 = u4get(vr[1][mt >> 2], mt & 3);  // token 2t+1
+        const uint32_t x8 = u4get(vr[2][mt >> 2], mt & 3);  // token 2t+8
+        const uint32_t x9 = u4get(vr[3][mt >> 2], mt & 3);  // token 2t+9
         const uint32_t A0 = __byte_perm(x0, x1, 0x5410);
         const uint32_t A1 = __byte_perm(x0, x1, 0x7632);
         const uint32_t A2 = __byte_perm(x8, x9, 0x5410);
@@ -204,15 +233,26 @@ __device__ __forceinline__ long long range_start(long long w, long long V, long 
 // half runs while the synchronous recall of the corrected units is in flight);
 // 2 = corrected units only (after that recall).  Each unit is attended in exactly
 // one phase, so every partial record is written once per step.
-__global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 2) fkv_attn_split_kernel(FkvDims D, FkvLayer L,
-                                                                                   FkvScratch X,
-                                                                                   const uint16_t* __restrict__ q,
-                                                                                   int phase) {
+__global__ void __launch_bounds__(kAttnWarpsPerCta * 32) fkv_attn_split_kernel(FkvDims D, FkvLayer L, FkvScratch X,
+                                                                               const uint16_t* __restrict__ q,
+                                                                               int phase,
+                                                                               const __grid_constant__ CUtensorMap tmap,
+                                                                               const uint16_t* arena) {
+    extern __shared__ __align__(1024) uint8_t s_stage[];  // [warps][kStages][8 KiB]
+    __shared__ __align__(8) uint64_t bar[kAttnWarpsPerCta][kStages];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
     const int w = blockIdx.x * kAttnWarpsPerCta + warp;
     const int T = D.attn_warps;
     if (w >= T) return;
+    uint8_t* ring = s_stage + warp * (kStages * kSlabBytes);
+    if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < kStages; ++i) mbar_init(&bar[warp][i], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    uint32_t phase_bits = 0u;  // parity of each stage's next completion
     const long long V = (long long)D.U * D.P_max;
     const long long s0 = range_start(w, V, T), s1 = range_start(w + 1, V, T);
     const int G = D.G, spp = D.p >> 4;
@@ -221,23 +261,33 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 2) fkv_attn_split_kerne
     for (long long seg = s0; seg < s1; ++k_rec) {
         const int u = (int)(seg / D.P_max);
         const long long seg_end = min(s1, (long long)(u + 1) * D.P_max);
-        if (phase != 0 && ((L.flags[u] != 0) != (phase == 2))) {
-            seg = seg_end;  // this unit is attended in the other phase
-            continue;
-        }
-        const UnitMeta M = load_meta(D, L, u);
         const int pa = (int)(seg - (long long)u * D.P_max);
-        const int pb = min((int)(seg_end - (long long)u * D.P_max), M.n_pages);
         seg = seg_end;
+        if (phase != 0 && ((L.flags[u] != 0) != (phase == 2))) continue;  // attended in the other phase
+        const UnitMeta M = load_meta(D, L, u);
+        const int pb = min((int)(seg_end - (long long)u * D.P_max), M.n_pages);
         const int b = u / D.n_kv, m = u % D.n_kv;
-        // Q fragments: lane (g, t) holds Q[head g][32c + 8t .. 8t+7], c = 0..3 (heads >= G are zero)
-        uint4 qa[4];
+        const int x0 = pa * spp, nx = pb > pa ? (pb - pa) * spp : 0;
+        // prologue: first kStages slabs of this segment in flight
+        if (lane == 0) {
+#pragma unroll
+            for (int i = 0; i < kStages; ++i) {
+                int row;
+                if (i < nx && slab_info(D, L, u, M, x0 + i, arena, row) > 0)
+                    issue_slab(&tmap, ring + i * kSlabBytes, &bar[warp][i], row, D.p);
+            }
+        }
+        // Q fragments: lane (g, t) holds Q[head g][64b + 16t + 8e .. +8] (heads >= G are zero)
+        uint4 qa[2][2];
         {
             const bool hv = g < G;
             const uint16_t* qrow = q + ((size_t)b * D.n_qo + m * G + (hv ? g : 0)) * kHeadDim;
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
-                qa[c] = hv ? *reinterpret_cast<const uint4*>(qrow + 32 * c + 8 * t) : make_uint4(0u, 0u, 0u, 0u);
+            for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    qa[bb][e] = hv ? *reinterpret_cast<const uint4*>(qrow + 64 * bb + 16 * t + 8 * e)
+                                   : make_uint4(0u, 0u, 0u, 0u);
         }
         float oacc[8][4];
 #pragma unroll
@@ -245,15 +295,22 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 2) fkv_attn_split_kerne
 #pragma unroll
             for (int k = 0; k < 4; ++k) oacc[i][k] = 0.0f;
         float m_run = -INFINITY, l_run = 0.0f;
-        const int x0 = pa * spp, nx = pb > pa ? (pb - pa) * spp : 0;
-        Slab A, B;
-        if (nx > 0) load_slab(D, L, u, M, x0, g, t, A);
-        for (int x = 0; x < nx; x += 2) {
-            if (x + 1 < nx) load_slab(D, L, u, M, x0 + x + 1, g, t, B);
-            compute_slab(A, qa, sc, t, m_run, l_run, oacc);
-            if (x + 1 < nx) {
-                if (x + 2 < nx) load_slab(D, L, u, M, x0 + x + 2, g, t, A);
-                compute_slab(B, qa, sc, t, m_run, l_run, oacc);
+        for (int i = 0; i < nx; ++i) {
+            const int stg = i % kStages;
+            int row;
+            const int valid = slab_info(D, L, u, M, x0 + i, arena, row);
+            if (valid > 0) {
+                mbar_wait(&bar[warp][stg], (phase_bits >> stg) & 1u);
+                phase_bits ^= 1u << stg;
+                compute_slab(ring + stg * kSlabBytes, valid, qa, sc, g, t, m_run, l_run, oacc);
+            }
+            __syncwarp();  // every lane is done with this stage before it is refilled
+            if (lane == 0 && i + kStages < nx) {
+                int row2;
+                if (slab_info(D, L, u, M, x0 + i + kStages, arena, row2) > 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    issue_slab(&tmap, ring + stg * kSlabBytes, &bar[warp][stg], row2, D.p);
+                }
             }
         }
         // ---- partial record (w, k_rec) of unit u: unnormalised, relative to m_run
@@ -265,102 +322,93 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 2) fkv_attn_split_kerne
             X.part_ml[(rec * G + g) * 2 + 0] = m_run;
             X.part_ml[(rec * G + g) * 2 + 1] = l_tot;
         }
+        // logical channel (mt, g) lives at physical 64(g/4) + 8(g%4) + 32(mt/4) + 2(mt%4); (mt, g+8) at +1
+        const int base0 = 64 * (g >> 2) + 8 * (g & 3);
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
             const int h = 2 * t + hh;
             if (h < G) {
-                float4* dst = reinterpret_cast<float4*>(X.part_o + (rec * G + h) * kHeadDim + 16 * g);
+                float* dst = X.part_o + (rec * G + h) * kHeadDim + base0;
 #pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4)
-                    dst[q4] = make_float4(oacc[2 * q4][hh], oacc[2 * q4][2 + hh], oacc[2 * q4 + 1][hh],
-                                          oacc[2 * q4 + 1][2 + hh]);
+                for (int half = 0; half < 2; ++half) {
+                    float4* d4 = reinterpret_cast<float4*>(dst + 32 * half);
+                    const int mb = 4 * half;
+                    d4[0] = make_float4(oacc[mb][hh], oacc[mb][2 + hh], oacc[mb + 1][hh], oacc[mb + 1][2 + hh]);
+                    d4[1] = make_float4(oacc[mb + 2][hh], oacc[mb + 2][2 + hh], oacc[mb + 3][hh], oacc[mb + 3][2 + hh]);
+                }
             }
         }
     }
 }
 
 // Merge a unit's partial records and commit the speculative advance (row a8).
-// Phase 1 stages every record's (m, l) in shared memory, phase 2 turns them
-// into weights 2^(m_r - M) / L per head, phase 3 has thread (h, c) reduce the
-// weighted partial outputs.
-constexpr int kMaxRecs = 256;
+// The records of unit u are the contiguous warps w_first..w_last whose page
+// ranges intersect [u*P_max, (u+1)*P_max) (every warp owns >= 1 page, T <= V;
+// 32-bit range math, T * V < 2^31 is guaranteed on the host).  Thread (h, c)
+// issues the loads of a batch of records at once and merges them with an
+// online max, so the kernel costs ~2 global round trips.
+constexpr int kCombBatch = 12;
 
 __global__ void __launch_bounds__(1024) fkv_attn_combine_kernel(FkvDims D, FkvLayer L, FkvScratch X,
                                                                 const uint16_t* __restrict__ q,
                                                                 float* __restrict__ out) {
-    __shared__ int s_rec[kMaxRecs];
-    __shared__ int s_nrec, s_first;
-    __shared__ float s_ml[kMaxRecs * kMaxG * 2];
-    __shared__ float s_w[kMaxRecs * kMaxG];
     const int u = blockIdx.x, b = u / D.n_kv, m = u % D.n_kv, G = D.G;
-    const long long V = (long long)D.U * D.P_max, T = D.attn_warps;
-    const long long x0 = (long long)u * D.P_max, x1 = x0 + D.P_max;
-    // Records of unit u: the warps whose range [start(w), start(w+1)) intersects
-    // [x0, x1).  Every warp owns >= 1 page (T <= V), so they are the contiguous run
-    // w_first..w_last; candidates are tested in parallel with 32-bit arithmetic
-    // (T * V < 2^31 and records <= kMaxRecs are guaranteed on the host).
-    if (threadIdx.x == 0) {
-        s_nrec = 0;
-        s_first = 0x7fffffff;
+    const unsigned T = (unsigned)D.attn_warps, V = (unsigned)(D.U * D.P_max);
+    const unsigned x0 = (unsigned)u * D.P_max, x1 = x0 + D.P_max;
+    const int w_first = (int)(((x0 + 1) * T + V - 1) / V) - 1;
+    const int w_last = (int)((x1 * T + V - 1) / V) - 1;
+    const int nr = w_last - w_first + 1;
+    // commit loads first (independent of the merge)
+    int rp = 0, rs = 0;
+    if (threadIdx.x < D.K) {
+        rp = L.pend_pages[(size_t)u * D.K + threadIdx.x];
+        rs = L.pend_slot[(size_t)u * D.K + threadIdx.x];
     }
-    __syncthreads();
-    {
-        const unsigned Ti = (unsigned)T, Vi = (unsigned)V;
-        const int w_lo = max(0, (int)(((long long)x0 * Ti) / Vi) - 1);
-        for (int w = w_lo + (int)threadIdx.x; w < (int)Ti && w < w_lo + kMaxRecs + 2; w += blockDim.x) {
-            const int a = (int)((unsigned)w * Vi / Ti), e = (int)((unsigned)(w + 1) * Vi / Ti);
-            if (e > (int)x0 && a < (int)x1) {
-                atomicMin(&s_first, w);
-                atomicAdd(&s_nrec, 1);
-            }
-        }
-        __syncthreads();
-        for (int w = w_lo + (int)threadIdx.x; w < (int)Ti && w < w_lo + kMaxRecs + 2; w += blockDim.x) {
-            const int a = (int)((unsigned)w * Vi / Ti), e = (int)((unsigned)(w + 1) * Vi / Ti);
-            if (e > (int)x0 && a < (int)x1) s_rec[w - s_first] = w * 2 + ((a / D.P_max == u) ? 0 : 1);
-        }
-    }
-    __syncthreads();
-    const int nr = s_nrec;
-    for (int i = threadIdx.x; i < nr * G * 2; i += blockDim.x) {
-        const int r = i / (G * 2), rem = i % (G * 2);
-        s_ml[i] = X.part_ml[(size_t)s_rec[r] * G * 2 + rem];
-    }
-    __syncthreads();
-    if (threadIdx.x < G) {
-        const int h = threadIdx.x;
-        float M = -INFINITY;
-        for (int r = 0; r < nr; ++r) M = fmaxf(M, s_ml[(r * G + h) * 2]);
-        float Ls = 0.0f;
-        for (int r = 0; r < nr; ++r) {
-            const float mr = s_ml[(r * G + h) * 2];
-            const float wgt = mr == -INFINITY ? 0.0f : exp2f(mr - M);
-            s_w[r * G + h] = wgt;
-            Ls += wgt * s_ml[(r * G + h) * 2 + 1];
-        }
-        const float inv = 1.0f / Ls;
-        for (int r = 0; r < nr; ++r) s_w[r * G + h] *= inv;
-    }
-    __syncthreads();
     const int h = threadIdx.x / kHeadDim, c = threadIdx.x % kHeadDim;
     if (h < G) {
-        // unconditional, unrolled loads keep all records' reads in flight (every listed
-        // record was written this step; empty segments carry weight 0 and o = 0)
-        float O = 0.0f;
-        int r = 0;
-        for (; r + 8 <= nr; r += 8) {
-            float v[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) v[i] = X.part_o[((size_t)s_rec[r + i] * G + h) * kHeadDim + c];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) O += s_w[(r + i) * G + h] * v[i];
-        }
-        for (; r < nr; ++r) O += s_w[r * G + h] * X.part_o[((size_t)s_rec[r] * G + h) * kHeadDim + c];
         const size_t row = (size_t)b * D.n_qo + m * G + h;
-        out[row * kHeadDim + c] = O;
-        L.q_prev[row * kHeadDim + c] = q[row * kHeadDim + c];  // q_prev := q_i
+        const uint16_t qv = q[row * kHeadDim + c];
+        float M = -INFINITY, Ls = 0.0f, O = 0.0f;
+        for (int r0 = 0; r0 < nr; r0 += kCombBatch) {
+            float vo[kCombBatch], vm[kCombBatch], vl[kCombBatch];
+#pragma unroll
+            for (int i = 0; i < kCombBatch; ++i) {
+                vm[i] = -INFINITY;
+                vl[i] = 0.0f;
+                vo[i] = 0.0f;
+                if (r0 + i < nr) {
+                    const unsigned w = (unsigned)(w_first + r0 + i);
+                    const unsigned a = w * V / T;
+                    const size_t rec = (size_t)w * 2 + ((a / D.P_max == (unsigned)u) ? 0 : 1);
+                    vm[i] = X.part_ml[(rec * G + h) * 2 + 0];
+                    vl[i] = X.part_ml[(rec * G + h) * 2 + 1];
+                    vo[i] = X.part_o[(rec * G + h) * kHeadDim + c];
+                }
+            }
+            float Mb = M;
+#pragma unroll
+            for (int i = 0; i < kCombBatch; ++i) Mb = fmaxf(Mb, vm[i]);
+            if (Mb != -INFINITY) {
+                const float sc = exp2f(M - Mb);  // M = -inf -> 0
+                Ls *= sc;
+                O *= sc;
+#pragma unroll
+                for (int i = 0; i < kCombBatch; ++i) {
+                    const float wgt = vm[i] == -INFINITY ? 0.0f : exp2f(vm[i] - Mb);
+                    Ls += wgt * vl[i];
+                    O += wgt * vo[i];
+                }
+                M = Mb;
+            }
+        }
+        out[row * kHeadDim + c] = O / Ls;
+        L.q_prev[row * kHeadDim + c] = qv;  // q_prev := q_i
     }
-    for (int i = threadIdx.x; i < D.K; i += blockDim.x) {
+    if (threadIdx.x < D.K) {
+        L.res_pages[(size_t)u * D.K + threadIdx.x] = rp;
+        L.res_slot[(size_t)u * D.K + threadIdx.x] = rs;
+    }
+    for (int i = threadIdx.x + blockDim.x; i < D.K; i += blockDim.x) {  // K > block size
         L.res_pages[(size_t)u * D.K + i] = L.pend_pages[(size_t)u * D.K + i];
         L.res_slot[(size_t)u * D.K + i] = L.pend_slot[(size_t)u * D.K + i];
     }
@@ -373,21 +421,26 @@ __global__ void __launch_bounds__(1024) fkv_attn_combine_kernel(FkvDims D, FkvLa
 
 // Resident warps of the split kernel, minus headroom of ~1/8 of the CTA slots so
 // the recall kernels (other streams) can be scheduled while attention runs.
+static constexpr int kAttnSmem = kAttnWarpsPerCta * kStages * kSlabBytes;
+
 cudaError_t attn_resident_warps(int* warps) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e == cudaSuccess)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fkv_attn_split_kernel, kAttnWarpsPerCta * 32, 0);
+        e = cudaFuncSetAttribute(fkv_attn_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem);
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fkv_attn_split_kernel, kAttnWarpsPerCta * 32,
+                                                          kAttnSmem);
     const int ctas = sms * per_sm;
     *warps = (ctas - ctas / 8) * kAttnWarpsPerCta;
     return e;
 }
 
 cudaError_t launch_attn_split(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                              int phase, cudaStream_t s) {
+                              int phase, const CUtensorMap& tmap, const uint16_t* arena, cudaStream_t s) {
     const int ctas = (D.attn_warps + kAttnWarpsPerCta - 1) / kAttnWarpsPerCta;
-    fkv_attn_split_kernel<<<ctas, kAttnWarpsPerCta * 32, 0, s>>>(D, L, X, q, phase);
+    fkv_attn_split_kernel<<<ctas, kAttnWarpsPerCta * 32, kAttnSmem, s>>>(D, L, X, q, phase, tmap, arena);
     return cudaGetLastError();
 }
 

@@ -3,6 +3,7 @@
 // Layout of one layer's state in the device arena and the host pool
 // (DESIGN.md §4).  All kernels receive a FkvDims and a FkvLayer by value.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -117,13 +118,14 @@ cudaError_t launch_append(const FkvDims& D, const FkvLayer& L, const uint16_t* k
 cudaError_t launch_summarize(const FkvDims& D, const FkvLayer& L, int page_begin, int page_end,
                              cudaStream_t s);
 cudaError_t launch_score(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                         int max_n_off, cudaStream_t s);
+                         int max_n_off, int pending, cudaStream_t s);
 cudaError_t launch_finalize(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                            int32_t* pages_out, uint8_t* corrected_out, int lpt, cudaStream_t s);
+                            const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
+                            uint8_t* corrected_out, int lpt, cudaStream_t s);
 cudaError_t launch_recall(const FkvDims& D, const FkvLayer& L, int sync_mode, cudaStream_t s);
 cudaError_t attn_resident_warps(int* warps);  // SMs x resident warps/SM of the split kernel
 cudaError_t launch_attn_split(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                              int phase, cudaStream_t s);
+                              int phase, const CUtensorMap& tmap, const uint16_t* arena, cudaStream_t s);
 cudaError_t launch_attn_combine(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                                 float* out, cudaStream_t s);
 }  // namespace fkv

@@ -24,7 +24,7 @@ EXPORTED = [
     "freekv_get_selection", "freekv_get_resident", "freekv_get_fetch", "freekv_get_summaries",
     "freekv_get_context", "freekv_get_dims", "freekv_synchronize", "freekv_destroy",
     "freekv_last_error", "freekv_abi_version", "freekv_profile_begin", "freekv_profile_end",
-    "freekv_step_graph_capture", "freekv_step_graph_launch",
+    "freekv_step_graph_capture", "freekv_step_graph_launch", "freekv_step_graph_profile",
 ]
 KERNEL_CLASSES = ["append", "score", "select_finalize", "recall_sync", "recall_bg", "attn_split", "attn_combine"]
 
@@ -123,7 +123,8 @@ def load_library():
             "freekv_synchronize": [vp],
             "freekv_profile_begin": [vp, i32],
             "freekv_profile_end": [vp, vp, vp],
-            "freekv_step_graph_capture": [vp, vp, vp, vp, vp],
+            "freekv_step_graph_capture": [vp, vp, vp, vp, vp, i32],
+            "freekv_step_graph_profile": [vp, vp, vp],
             "freekv_step_graph_launch": [vp],
         }
         for name, args in sigs.items():
@@ -211,15 +212,22 @@ class FreeKV:
         _check(self.L.freekv_decode_step(self.h, layer, q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(),
                                          out.data_ptr()))
 
-    def step_graph_capture(self, q_all, k_all, v_all, out_all):
+    def step_graph_capture(self, q_all, k_all, v_all, out_all, profile=False):
         """Capture one decode step of every layer reading q_all [L][nb][n_qo][d], k_all/v_all
         [L][nb][1][n_kv][d] and writing out_all [L][nb][n_qo][d] (fixed device buffers)."""
         _check(self.L.freekv_step_graph_capture(self.h, q_all.data_ptr(), k_all.data_ptr(), v_all.data_ptr(),
-                                                out_all.data_ptr()))
+                                                out_all.data_ptr(), int(profile)))
         self._graph_bufs = (q_all, k_all, v_all, out_all)
 
     def step_graph_launch(self):
         _check(self.L.freekv_step_graph_launch(self.h))
+
+    def step_graph_profile(self):
+        """Per kernel class (ms, launches) of the last replay of a profile-mode step graph."""
+        ms = np.zeros(len(KERNEL_CLASSES), np.float32)
+        n = np.zeros(len(KERNEL_CLASSES), np.int32)
+        _check(self.L.freekv_step_graph_profile(self.h, _np_ptr(ms), _np_ptr(n)))
+        return {c: (float(ms[i]), int(n[i])) for i, c in enumerate(KERNEL_CLASSES)}
 
     def synchronize(self):
         _check(self.L.freekv_synchronize(self.h))

@@ -18,6 +18,7 @@ ap.add_argument("--n_qo", type=int, default=32)
 ap.add_argument("--n_kv", type=int, default=8)
 ap.add_argument("--event_rate", type=float, default=0.05)
 ap.add_argument("--no-profile", action="store_true")
+ap.add_argument("--graph", action="store_true", help="whole-step graph replay with in-graph event profiling")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 nb, nq, nk, d, p = a.batch, a.n_qo, a.n_kv, 128, 32
@@ -47,6 +48,30 @@ for i in range(a.warmup):
     for l in range(a.layers):
         fkv.decode_step(l, Q[i, l], Kn[i, l], Vn[i, l], out)
 fkv.synchronize()
+if a.graph:
+    qb, kb, vb = torch.empty_like(Q[0]), torch.empty_like(Kn[0]), torch.empty_like(Vn[0])
+    ob = torch.empty(a.layers, nb, nq, d, dtype=torch.float32, device=dev)
+    fkv.step_graph_capture(qb, kb, vb, ob, profile=not a.no_profile)
+    acc = {}
+    tot = 0.0
+    for i in range(a.warmup, T):
+        with torch.cuda.stream(s):
+            qb.copy_(Q[i]); kb.copy_(Kn[i]); vb.copy_(Vn[i])
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        fkv.step_graph_launch()
+        e1.record(s)
+        fkv.synchronize()
+        tot += e0.elapsed_time(e1)
+        if not a.no_profile:
+            for k, (t, n) in fkv.step_graph_profile().items():
+                x = acc.setdefault(k, [0.0, 0])
+                x[0] += t
+                x[1] += n
+    res = {"us_per_layer_graph_synced": tot * 1e3 / (a.steps * a.layers)}
+    res["kernels_us_in_graph"] = {k: round(v[0] / max(v[1], 1) * 1e3, 2) for k, v in acc.items()}
+    print(json.dumps(res))
+    sys.exit(0)
 if not a.no_profile:
     fkv.profile_begin(a.steps * a.layers * 8 + 16)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
