@@ -70,7 +70,8 @@ struct freekv_handle {
 namespace {
 
 constexpr size_t kAlign = 256;
-constexpr int kMaxAttnWarps = 148 * 16;  // partial-record capacity; the grid uses min(resident warps, this)
+constexpr int kMaxAttnWarps = 148 * 16;
+constexpr int kFinalizeThreads = 1024;  // must match select.cu kThreads  // partial-record capacity; the grid uses min(resident warps, this)
 size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
 
 struct Sizes {
@@ -80,7 +81,7 @@ struct Sizes {
         o_pend_cnt,
         o_pend_pages, o_pend_slot, o_pend_front, o_flags, o_cbar, o_fetch_page, o_fetch_slot, o_n_fetch, o_ctx,
         o_n_off;
-    size_t o_scores, o_part_o, o_part_ml;
+    size_t o_scores, o_part_o, o_part_ml, o_page_rows, o_page_cnt, o_page_valid;
 };
 
 freekv_status validate(const freekv_config* c, FkvDims* D) {
@@ -170,6 +171,9 @@ Sizes compute_sizes(const freekv_config* c, const FkvDims& D) {
     s.o_scores = take(U * D.G * D.n_page_max * 4);
     s.o_part_o = take((size_t)2 * kMaxAttnWarps * D.G * D.d * 4);
     s.o_part_ml = take((size_t)2 * kMaxAttnWarps * D.G * 2 * 4);
+    s.o_page_rows = take(U * D.P_max * 4);
+    s.o_page_cnt = take(U * 4);
+    s.o_page_valid = take(U * D.P_max);
     s.scratch_bytes = o;
     s.dev_bytes = s.layer_bytes * c->n_layers + s.scratch_bytes;
     s.host_layer_bytes = (size_t)D.nb * D.n_page_host * D.n_kv * pe_b;
@@ -408,15 +412,23 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         L.ctx = (int32_t*)(base + s.o_ctx);
         L.n_off = (int32_t*)(base + s.o_n_off);
         L.host = (uint16_t*)(hd + s.host_layer_bytes * l);
+        L.arena = (const uint16_t*)dev;
     }
     uint8_t* sb = dev + s.layer_bytes * cfg->n_layers;
     h->X.scores = (float*)(sb + s.o_scores);
     h->X.part_o = (float*)(sb + s.o_part_o);
     h->X.part_ml = (float*)(sb + s.o_part_ml);
+    h->X.page_rows = (int32_t*)(sb + s.o_page_rows);
+    h->X.page_cnt = (int32_t*)(sb + s.o_page_cnt);
+    h->X.page_valid = (uint8_t*)(sb + s.o_page_valid);
     {
         int P2 = 1;
         while (P2 < D.n_page_host) P2 <<= 1;
-        h->lpt = P2 <= 1024 ? 1 : P2 / 1024;
+        h->lpt = P2 <= kFinalizeThreads ? 1 : P2 / kFinalizeThreads;
+        if (h->lpt > 8) {
+            delete h;
+            return fail(FREEKV_EUNSUPPORTED, "max_ctx_tokens / page_size > 8192 pages");
+        }
     }
     {
         int warps = 0;
@@ -431,6 +443,10 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         long long T = std::min<long long>({(long long)warps, (long long)kMaxAttnWarps, V, 254LL * D.U});
         while (T > 1 && T * V >= (1LL << 31)) T /= 2;
         h->D.attn_warps = (int)std::max(1LL, T);
+    }
+    {
+        const char* fr = getenv("FREEKV_DEBUG_FULL_REFRESH");
+        h->D.full_refresh = (fr && fr[0] == '1') ? 1 : 0;
     }
     {
         const char* sr = getenv("FREEKV_SERIAL_RECALL");

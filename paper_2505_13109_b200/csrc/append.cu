@@ -34,6 +34,12 @@ __global__ void __launch_bounds__(128) fkv_summarize_kernel(FkvDims D, FkvLayer 
 cudaError_t launch_append(const FkvDims& D, const FkvLayer& L, const uint16_t* k, const uint16_t* v,
                           int n_new, cudaStream_t s) {
     const size_t smem = page_elems(D) * sizeof(uint16_t);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(fkv_append_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+        configured = true;
+    }
     fkv_append_kernel<<<D.U, 256, smem, s>>>(D, L, k, v, n_new);
     return cudaGetLastError();
 }

@@ -25,6 +25,8 @@
 // each warp always has 8 KiB in flight.  P is split into bf16 hi + lo parts
 // (two PV MMAs) so its rounding stays ~2^-17, far inside the 2e-3 output
 // tolerance (readings A-19/A-21).
+#include <cstdlib>
+
 #include "fkv_internal.cuh"
 
 namespace fkv {
@@ -102,7 +104,7 @@ __device__ __forceinline__ const uint16_t* page_ptr(const FkvDims& D, const FkvL
 // 128-byte swizzle (16-byte chunk c of row r lives at chunk c ^ (r % 8)).  The
 // fragment mapping below is chosen so every quarter-warp LDS.128 hits 8
 // distinct chunks (conflict-free) under that swizzle.
-constexpr int kStages = 3;          // slab stages per warp (2 slabs in flight while one is consumed)
+constexpr int kMaxStages = 4;       // slab stages per warp (template parameter NST <= kMaxStages)
 constexpr int kBoxBytes = 16 * 128; // 16 rows x 64 channels bf16
 constexpr int kSlabBytes = 4 * kBoxBytes;
 
@@ -135,69 +137,77 @@ __device__ __forceinline__ void issue_slab(const CUtensorMap* map, uint8_t* st, 
     tma_load_2d(st + 3 * kBoxBytes, map, 64, row + p, bar);
 }
 
-__device__ __forceinline__ void compute_slab(const uint8_t* st, int valid, const uint4 (&qa)[2][2], float sc, int g,
-                                             int t, float& m_run, float& l_run, float (&oacc)[8][4]) {
-    // ---- S = Q K^T for two n-tiles of 8 tokens.  Lane (g, t) holds, per 64-channel box b,
-    // channels 64b + 16t .. +16 of token row nt*8 + g (chunks 2t, 2t+1, swizzled by row % 8 = g)
-    float s[2][4];
+__device__ __forceinline__ uint32_t movmatrix_trans(uint32_t a) {
+    uint32_t d;
+    asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(a));
+    return d;
+}
+
+// One 16-token slab.  S^T = K Q^T on mma.m16n8k16 with M = 16 tokens, N = 8 heads
+// (no padded rows), so lane (g, t) holds S for tokens g and g+8 of heads 2t and
+// 2t+1: the per-head softmax state (max, rescale factor) is held by exactly the
+// lanes that hold O^T's columns for those heads, and P^T's MMA fragment is one
+// movmatrix.trans of the packed probabilities.
+__device__ __forceinline__ void compute_slab(const uint8_t* st, int valid, const uint4 (&qb)[2][2], float sc, int g,
+                                             int t, float (&m_run)[2], float (&l_run)[2], float (&oacc)[8][4]) {
+    // ---- S^T: A = K rows g (tokens 0-7) and g+8 (tokens 8-15), 16 channels per k-step;
+    // lane t reads chunks 2t, 2t+1 of each 64-channel box (swizzled by row % 8 = g)
+    float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) s[nt][k] = 0.0f;
-        const int r = nt * 8 + g;
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-            const uint8_t* rowp = st + b * kBoxBytes + r * 128;
-            const uint4 k0 = lds128(rowp + (((2 * t) ^ g) << 4));
-            const uint4 k1 = lds128(rowp + (((2 * t + 1) ^ g) << 4));
-            mma16816(s[nt], qa[b][0].x, 0u, qa[b][0].y, 0u, k0.x, k0.y);
-            mma16816(s[nt], qa[b][0].z, 0u, qa[b][0].w, 0u, k0.z, k0.w);
-            mma16816(s[nt], qa[b][1].x, 0u, qa[b][1].y, 0u, k1.x, k1.y);
-            mma16816(s[nt], qa[b][1].z, 0u, qa[b][1].w, 0u, k1.z, k1.w);
-        }
+    for (int b = 0; b < 2; ++b) {
+        const uint8_t* r0 = st + b * kBoxBytes + g * 128;
+        const uint8_t* r8 = r0 + 8 * 128;
+        const uint4 a0 = lds128(r0 + (((2 * t) ^ g) << 4));
+        const uint4 a1 = lds128(r0 + (((2 * t + 1) ^ g) << 4));
+        const uint4 c0 = lds128(r8 + (((2 * t) ^ g) << 4));
+        const uint4 c1 = lds128(r8 + (((2 * t + 1) ^ g) << 4));
+        mma16816(s, a0.x, c0.x, a0.y, c0.y, qb[b][0].x, qb[b][0].y);
+        mma16816(s, a0.z, c0.z, a0.w, c0.w, qb[b][0].z, qb[b][0].w);
+        mma16816(s, a1.x, c1.x, a1.y, c1.y, qb[b][1].x, qb[b][1].y);
+        mma16816(s, a1.z, c1.z, a1.w, c1.w, qb[b][1].z, qb[b][1].w);
     }
-    // ---- online softmax (row = head g; the 4 lanes of a quad share a row)
-    float x[2][2];
-    float smax = -INFINITY;
+    // s[0], s[1]: token g, heads 2t, 2t+1; s[2], s[3]: token g+8
+    float x[4];
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
+    for (int e = 0; e < 4; ++e) {
+        const int tok = g + (e >> 1) * 8;
+        x[e] = tok < valid ? s[e] * sc : -INFINITY;
+    }
+    float mx0 = fmaxf(x[0], x[2]), mx1 = fmaxf(x[1], x[3]);
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const int tok = nt * 8 + 2 * t + e;
-            x[nt][e] = tok < valid ? s[nt][e] * sc : -INFINITY;
-            smax = fmaxf(smax, x[nt][e]);
-        }
-    smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, 1));
-    smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, 2));
-    const float m_new = fmaxf(m_run, smax);
-    const float alpha = (m_new == -INFINITY) ? 1.0f : exp2f(m_run - m_new);
-    float pv[2][2];
-    float psum = 0.0f;
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            pv[nt][e] = (m_new == -INFINITY) ? 0.0f : exp2f(x[nt][e] - m_new);
-            psum += pv[nt][e];
-        }
-    l_run = l_run * alpha + psum;
-    m_run = m_new;
-    const float a0 = __shfl_sync(0xffffffffu, alpha, (2 * t) * 4);
-    const float a1 = __shfl_sync(0xffffffffu, alpha, (2 * t + 1) * 4);
+    for (int o = 4; o < 32; o <<= 1) {  // over the 8 lanes g with the same t
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+    }
+    const float mn0 = fmaxf(m_run[0], mx0), mn1 = fmaxf(m_run[1], mx1);
+    const float al0 = (mn0 == -INFINITY) ? 1.0f : exp2f(m_run[0] - mn0);
+    const float al1 = (mn1 == -INFINITY) ? 1.0f : exp2f(m_run[1] - mn1);
+    float pv[4];
+    pv[0] = (mn0 == -INFINITY) ? 0.0f : exp2f(x[0] - mn0);
+    pv[1] = (mn1 == -INFINITY) ? 0.0f : exp2f(x[1] - mn1);
+    pv[2] = (mn0 == -INFINITY) ? 0.0f : exp2f(x[2] - mn0);
+    pv[3] = (mn1 == -INFINITY) ? 0.0f : exp2f(x[3] - mn1);
+    l_run[0] = l_run[0] * al0 + pv[0] + pv[2];
+    l_run[1] = l_run[1] * al1 + pv[1] + pv[3];
+    m_run[0] = mn0;
+    m_run[1] = mn1;
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {
-        oacc[mt][0] *= a0;
-        oacc[mt][1] *= a1;
-        oacc[mt][2] *= a0;
-        oacc[mt][3] *= a1;
+        oacc[mt][0] *= al0;
+        oacc[mt][1] *= al1;
+        oacc[mt][2] *= al0;
+        oacc[mt][3] *= al1;
     }
-    // ---- P^T fragments, hi + lo bf16 split
-    const uint32_t bh0 = pack_bf16(pv[0][0], pv[0][1]);
-    const uint32_t bh1 = pack_bf16(pv[1][0], pv[1][1]);
-    const __nv_bfloat162 h0 = *reinterpret_cast<const __nv_bfloat162*>(&bh0);
-    const __nv_bfloat162 h1 = *reinterpret_cast<const __nv_bfloat162*>(&bh1);
-    const uint32_t bl0 = pack_bf16(pv[0][0] - __low2float(h0), pv[0][1] - __high2float(h0));
-    const uint32_t bl1 = pack_bf16(pv[1][0] - __low2float(h1), pv[1][1] - __high2float(h1));
+    // ---- P^T fragments (hi + lo bf16 split): pack (token g, heads 2t, 2t+1) then transpose the
+    // 8x8 (token x head) tiles so lane (g, t) holds P[tokens 2t, 2t+1][head g]
+    const uint32_t ph0 = pack_bf16(pv[0], pv[1]);
+    const uint32_t ph8 = pack_bf16(pv[2], pv[3]);
+    const __nv_bfloat162 h0 = *reinterpret_cast<const __nv_bfloat162*>(&ph0);
+    const __nv_bfloat162 h8 = *reinterpret_cast<const __nv_bfloat162*>(&ph8);
+    const uint32_t pl0 = pack_bf16(pv[0] - __low2float(h0), pv[1] - __high2float(h0));
+    const uint32_t pl8 = pack_bf16(pv[2] - __low2float(h8), pv[3] - __high2float(h8));
+    const uint32_t bh0 = movmatrix_trans(ph0), bh1 = movmatrix_trans(ph8);
+    const uint32_t bl0 = movmatrix_trans(pl0), bl1 = movmatrix_trans(pl8);
     // ---- V fragments: lane (g, t) reads tokens 2t, 2t+1, 2t+8, 2t+9 and, in box g / 4, the
     // chunks g % 4 (m-tiles 0-3) and g % 4 + 4 (m-tiles 4-7), swizzled by row % 8
     uint4 vr[4][2];
@@ -233,11 +243,13 @@ __device__ __forceinline__ long long range_start(long long w, long long V, long 
 // half runs while the synchronous recall of the corrected units is in flight);
 // 2 = corrected units only (after that recall).  Each unit is attended in exactly
 // one phase, so every partial record is written once per step.
-__global__ void __launch_bounds__(kAttnWarpsPerCta * 32) fkv_attn_split_kernel(FkvDims D, FkvLayer L, FkvScratch X,
+template <int NST>
+__global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2) fkv_attn_split_kernel(FkvDims D, FkvLayer L, FkvScratch X,
                                                                                const uint16_t* __restrict__ q,
                                                                                int phase,
                                                                                const __grid_constant__ CUtensorMap tmap,
                                                                                const uint16_t* arena) {
+    constexpr int kStages = NST;
     extern __shared__ __align__(1024) uint8_t s_stage[];  // [warps][kStages][8 KiB]
     __shared__ __align__(8) uint64_t bar[kAttnWarpsPerCta][kStages];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -255,7 +267,7 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32) fkv_attn_split_kernel(F
     uint32_t phase_bits = 0u;  // parity of each stage's next completion
     const long long V = (long long)D.U * D.P_max;
     const long long s0 = range_start(w, V, T), s1 = range_start(w + 1, V, T);
-    const int G = D.G, spp = D.p >> 4;
+    const int G = D.G, spp = D.p >> 4, lspp = spp == 1 ? 0 : (spp == 2 ? 1 : 2);
     const float sc = D.attn_c;
     int k_rec = 0;
     for (long long seg = s0; seg < s1; ++k_rec) {
@@ -264,19 +276,9 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32) fkv_attn_split_kernel(F
         const int pa = (int)(seg - (long long)u * D.P_max);
         seg = seg_end;
         if (phase != 0 && ((L.flags[u] != 0) != (phase == 2))) continue;  // attended in the other phase
-        const UnitMeta M = load_meta(D, L, u);
-        const int pb = min((int)(seg_end - (long long)u * D.P_max), M.n_pages);
+        const int32_t* prow = X.page_rows + (size_t)u * D.P_max;  // written by the select kernel
+        const int pb = min((int)(seg_end - (long long)u * D.P_max), X.page_cnt[u]);
         const int b = u / D.n_kv, m = u % D.n_kv;
-        const int x0 = pa * spp, nx = pb > pa ? (pb - pa) * spp : 0;
-        // prologue: first kStages slabs of this segment in flight
-        if (lane == 0) {
-#pragma unroll
-            for (int i = 0; i < kStages; ++i) {
-                int row;
-                if (i < nx && slab_info(D, L, u, M, x0 + i, arena, row) > 0)
-                    issue_slab(&tmap, ring + i * kSlabBytes, &bar[warp][i], row, D.p);
-            }
-        }
         // Q fragments: lane (g, t) holds Q[head g][64b + 16t + 8e .. +8] (heads >= G are zero)
         uint4 qa[2][2];
         {
@@ -294,33 +296,68 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32) fkv_attn_split_kernel(F
         for (int i = 0; i < 8; ++i)
 #pragma unroll
             for (int k = 0; k < 4; ++k) oacc[i][k] = 0.0f;
-        float m_run = -INFINITY, l_run = 0.0f;
-        for (int i = 0; i < nx; ++i) {
-            const int stg = i % kStages;
-            int row;
-            const int valid = slab_info(D, L, u, M, x0 + i, arena, row);
-            if (valid > 0) {
-                mbar_wait(&bar[warp][stg], (phase_bits >> stg) & 1u);
-                phase_bits ^= 1u << stg;
-                compute_slab(ring + stg * kSlabBytes, valid, qa, sc, g, t, m_run, l_run, oacc);
+        float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.0f, 0.0f};  // heads 2t, 2t+1
+        // the segment's pages in chunks of <= 32 (one page-table entry per lane)
+        for (int cb = pa; cb < pb; cb += 32) {
+            const int np = min(32, pb - cb);
+            // page table of the segment, one page per lane: first K row in the arena tensor and
+            // valid tokens -- one batch of independent loads instead of a dependent load per slab
+            int my_row = 0, my_valid = 0;
+            if (lane < np) {
+                my_row = prow[cb + lane];
+                my_valid = X.page_valid[(size_t)u * D.P_max + cb + lane];
             }
-            __syncwarp();  // every lane is done with this stage before it is refilled
-            if (lane == 0 && i + kStages < nx) {
-                int row2;
-                if (slab_info(D, L, u, M, x0 + i + kStages, arena, row2) > 0) {
+            const int nx = np * spp;
+            auto slab_of = [&](int x, int& row) {  // warp-uniform; spp = 1 << lspp
+                const int pi = x >> lspp, sl = x & (spp - 1);
+                row = __shfl_sync(0xffffffffu, my_row, pi) + sl * 16;
+                return __shfl_sync(0xffffffffu, my_valid, pi) - sl * 16;
+            };
+            // prologue: first kStages slabs of this segment in flight
+            int rows[kStages], valids[kStages];
+#pragma unroll
+            for (int i = 0; i < kStages; ++i) valids[i] = i < nx ? slab_of(i, rows[i]) : 0;
+            if (lane == 0) {
+#pragma unroll
+                for (int i = 0; i < kStages; ++i)
+                    if (valids[i] > 0) issue_slab(&tmap, ring + i * kSlabBytes, &bar[warp][i], rows[i], D.p);
+            }
+            for (int i = 0; i < nx; ++i) {
+                const int stg = i % kStages;
+                int row;
+                const int valid = slab_of(i, row);
+                int row2 = 0, valid2 = 0;
+                if (i + kStages < nx) valid2 = slab_of(i + kStages, row2);
+                if (valid > 0) {
+                    mbar_wait(&bar[warp][stg], (phase_bits >> stg) & 1u);
+                    phase_bits ^= 1u << stg;
+                    compute_slab(ring + stg * kSlabBytes, valid, qa, sc, g, t, m_run, l_run, oacc);
+                }
+                __syncwarp();  // every lane is done with this stage before it is refilled
+                if (lane == 0 && valid2 > 0) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     issue_slab(&tmap, ring + stg * kSlabBytes, &bar[warp][stg], row2, D.p);
                 }
             }
         }
-        // ---- partial record (w, k_rec) of unit u: unnormalised, relative to m_run
-        float l_tot = l_run;
-        l_tot += __shfl_xor_sync(0xffffffffu, l_tot, 1);
-        l_tot += __shfl_xor_sync(0xffffffffu, l_tot, 2);
+        // ---- partial record (w, k_rec) of unit u: unnormalised, relative to m_run.  Lane (g, t)
+        // holds heads 2t, 2t+1; l is summed over the 8 lanes g of the same t
+        float l0 = l_run[0], l1 = l_run[1];
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+            l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+            l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+        }
         const size_t rec = (size_t)w * 2 + k_rec;
-        if (t == 0 && g < G) {
-            X.part_ml[(rec * G + g) * 2 + 0] = m_run;
-            X.part_ml[(rec * G + g) * 2 + 1] = l_tot;
+        if (g == 0) {
+            if (2 * t < G) {
+                X.part_ml[(rec * G + 2 * t) * 2 + 0] = m_run[0];
+                X.part_ml[(rec * G + 2 * t) * 2 + 1] = l0;
+            }
+            if (2 * t + 1 < G) {
+                X.part_ml[(rec * G + 2 * t + 1) * 2 + 0] = m_run[1];
+                X.part_ml[(rec * G + 2 * t + 1) * 2 + 1] = l1;
+            }
         }
         // logical channel (mt, g) lives at physical 64(g/4) + 8(g%4) + 32(mt/4) + 2(mt%4); (mt, g+8) at +1
         const int base0 = 64 * (g >> 2) + 8 * (g & 3);
@@ -348,6 +385,7 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32) fkv_attn_split_kernel(F
 // issues the loads of a batch of records at once and merges them with an
 // online max, so the kernel costs ~2 global round trips.
 constexpr int kCombBatch = 12;
+constexpr int kMaxRecs = 256;  // records per unit (host guarantees P_max * T / V + 2 <= 256)
 
 __global__ void __launch_bounds__(1024) fkv_attn_combine_kernel(FkvDims D, FkvLayer L, FkvScratch X,
                                                                 const uint16_t* __restrict__ q,
@@ -364,6 +402,14 @@ __global__ void __launch_bounds__(1024) fkv_attn_combine_kernel(FkvDims D, FkvLa
         rp = L.pend_pages[(size_t)u * D.K + threadIdx.x];
         rs = L.pend_slot[(size_t)u * D.K + threadIdx.x];
     }
+    // record indices, computed once (integer division is ~30 instructions)
+    __shared__ int s_rec[kMaxRecs];
+    for (int r = threadIdx.x; r < nr && r < kMaxRecs; r += blockDim.x) {
+        const unsigned w = (unsigned)(w_first + r);
+        const unsigned a = w * V / T;
+        s_rec[r] = (int)(w * 2 + ((a / D.P_max == (unsigned)u) ? 0 : 1));
+    }
+    __syncthreads();
     const int h = threadIdx.x / kHeadDim, c = threadIdx.x % kHeadDim;
     if (h < G) {
         const size_t row = (size_t)b * D.n_qo + m * G + h;
@@ -377,9 +423,7 @@ __global__ void __launch_bounds__(1024) fkv_attn_combine_kernel(FkvDims D, FkvLa
                 vl[i] = 0.0f;
                 vo[i] = 0.0f;
                 if (r0 + i < nr) {
-                    const unsigned w = (unsigned)(w_first + r0 + i);
-                    const unsigned a = w * V / T;
-                    const size_t rec = (size_t)w * 2 + ((a / D.P_max == (unsigned)u) ? 0 : 1);
+                    const size_t rec = (size_t)s_rec[r0 + i];
                     vm[i] = X.part_ml[(rec * G + h) * 2 + 0];
                     vl[i] = X.part_ml[(rec * G + h) * 2 + 1];
                     vo[i] = X.part_o[(rec * G + h) * kHeadDim + c];
@@ -421,26 +465,59 @@ __global__ void __launch_bounds__(1024) fkv_attn_combine_kernel(FkvDims D, FkvLa
 
 // Resident warps of the split kernel, minus headroom of ~1/8 of the CTA slots so
 // the recall kernels (other streams) can be scheduled while attention runs.
-static constexpr int kAttnSmem = kAttnWarpsPerCta * kStages * kSlabBytes;
+static int attn_stages() {
+    static int st = 0;
+    if (!st) {
+        const char* e = getenv("FREEKV_ATTN_STAGES");
+        st = (e && (e[0] == '2' || e[0] == '4')) ? e[0] - '0' : 3;
+    }
+    return st;
+}
 
-cudaError_t attn_resident_warps(int* warps) {
+template <int NST>
+static cudaError_t attn_setup(int* warps) {
+    const int smem = kAttnWarpsPerCta * NST * kSlabBytes;
     int dev = 0, sms = 0, per_sm = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(fkv_attn_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem);
+        e = cudaFuncSetAttribute(fkv_attn_split_kernel<NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    // every kernel of the path prefers the max-shared carveout, so consecutive kernels never
+    // force an L1/shared-memory reconfiguration of the SMs
     if (e == cudaSuccess)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fkv_attn_split_kernel, kAttnWarpsPerCta * 32,
-                                                          kAttnSmem);
+        e = cudaFuncSetAttribute(fkv_attn_split_kernel<NST>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(fkv_attn_combine_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared);
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fkv_attn_split_kernel<NST>,
+                                                          kAttnWarpsPerCta * 32, smem);
+    // leave ~1/8 of the CTA slots free so the recall kernels (other streams) get SMs
     const int ctas = sms * per_sm;
     *warps = (ctas - ctas / 8) * kAttnWarpsPerCta;
     return e;
 }
 
+// Resident warps of the split kernel (stage count from FREEKV_ATTN_STAGES: 2, 3 or 4).
+cudaError_t attn_resident_warps(int* warps) {
+    switch (attn_stages()) {
+        case 2: return attn_setup<2>(warps);
+        case 4: return attn_setup<4>(warps);
+        default: return attn_setup<3>(warps);
+    }
+}
+
 cudaError_t launch_attn_split(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                               int phase, const CUtensorMap& tmap, const uint16_t* arena, cudaStream_t s) {
     const int ctas = (D.attn_warps + kAttnWarpsPerCta - 1) / kAttnWarpsPerCta;
-    fkv_attn_split_kernel<<<ctas, kAttnWarpsPerCta * 32, kAttnSmem, s>>>(D, L, X, q, phase, tmap, arena);
+    const int nst = attn_stages();
+    const int smem = kAttnWarpsPerCta * nst * kSlabBytes;
+    switch (nst) {
+        case 2: fkv_attn_split_kernel<2><<<ctas, kAttnWarpsPerCta * 32, smem, s>>>(D, L, X, q, phase, tmap, arena); break;
+        case 4: fkv_attn_split_kernel<4><<<ctas, kAttnWarpsPerCta * 32, smem, s>>>(D, L, X, q, phase, tmap, arena); break;
+        default: fkv_attn_split_kernel<3><<<ctas, kAttnWarpsPerCta * 32, smem, s>>>(D, L, X, q, phase, tmap, arena); break;
+    }
     return cudaGetLastError();
 }
 

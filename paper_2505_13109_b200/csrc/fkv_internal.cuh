@@ -25,6 +25,7 @@ struct FkvDims {
     int max_ctx;
     int U;            // nb * n_kv
     int mode;
+    int full_refresh; // diagnostics (env FREEKV_DEBUG_FULL_REFRESH=1): no slot reuse, all pages re-fetched
     float tau;
     float score_r;    // CFR-3: fl32(log2(e)/sqrt(d))
     float attn_c;     // log2(e)/sqrt(d) for attention softmax (not CFR)
@@ -55,10 +56,14 @@ struct FkvLayer {
     int32_t* ctx;         // [U]     context length Lc (tokens)
     int32_t* n_off;       // [U]     pages [0, n_off) are offloaded; candidates [n_sink, n_off)
     uint16_t* host;       // device-mapped host pool of this layer: [nb][n_page_host][n_kv][2][p][d]
+    const uint16_t* arena;  // base of the device arena (row 0 of the attention TMA tensor)
 };
 
 struct FkvScratch {
     float* scores;        // [U][G][n_page_max]
+    int32_t* page_rows;   // [U][P_max] attention page list of this step: arena row of the page's K block
+    uint8_t* page_valid;  // [U][P_max] valid tokens of each listed page
+    int32_t* page_cnt;    // [U]
     float* part_o;        // [2 * attn_warps][G][d]   per-warp, per-unit-segment partial outputs
     float* part_ml;       // [2 * attn_warps][G][2]   (running max, running sum)
 };

@@ -55,6 +55,12 @@ __global__ void __launch_bounds__(128) fkv_recall_kernel(FkvDims D, FkvLayer L, 
 }
 
 cudaError_t launch_recall(const FkvDims& D, const FkvLayer& L, int sync_mode, cudaStream_t s) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(fkv_recall_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+        configured = true;
+    }
     // one CTA per (unit, fetch slot): a corrected unit's pages all stream over PCIe at once
     // (latency-critical before attention); CTAs beyond n_fetch exit immediately
     fkv_recall_kernel<<<dim3(D.U, D.K), 128, 0, s>>>(D, L, sync_mode);

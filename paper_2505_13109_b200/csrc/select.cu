@@ -36,22 +36,16 @@ __device__ __forceinline__ float cexp2_cfr(float x) {
 }
 
 // ----------------------------------------------------------- a2: scoring
-// Thread per page, warp per 32-page summary block.  Each warp pulls its whole
-// 16 KiB block (32 pages x {min,max} x 128 channels, bf16) into shared memory
-// with ONE cp.async.bulk (TMA engine, mbarrier completion), so every warp has
-// its full working set in flight at once; q is staged meanwhile.  Lanes then
-// read their page's 16-byte channel chunks conflict-free.
-// CFR-2 in the two-FMA form: for c ascending,
-//   u = fma(max(q_c,0), mx_c, u); u = fma(min(q_c,0), mn_c, u)
-// -- exactly one of the two changes u, by fl(u + q_c * m_c) with an exact
-// product, so u equals the recipe's sequential sum up to the sign of zero.
 constexpr int kScoreWarps = 4;
 constexpr int kSummBlockBytes = 32 * 2 * kHeadDim * 2;  // 16 KiB: 32 pages x {min,max} x 128 ch
 
+// CFR-2 per channel c and head h: u = fma(q_c, m_c, u) with m_c = mx_c if q_c >= 0 else
+// mn_c (exact product, one rounding -- exactly the recipe's fl(u + t)).  The select is a
+// LOP3 on a precomputed sign mask, so each head's dependent chain is one FMA per channel.
 template <int G>
 __device__ __forceinline__ void score_channels(const uint4* blk, int c8_begin, int lane,
-                                               const float (*qp)[(G + 3) / 4 * 4],
-                                               const float (*qn)[(G + 3) / 4 * 4], float (&acc)[G]) {
+                                               const float (*qv)[(G + 3) / 4 * 4],
+                                               const uint32_t (*qm)[(G + 3) / 4 * 4], float (&acc)[G]) {
     constexpr int GP = (G + 3) / 4 * 4;
 #pragma unroll 2
     for (int c8 = c8_begin; c8 < c8_begin + 4; ++c8) {
@@ -64,19 +58,19 @@ __device__ __forceinline__ void score_channels(const uint4* blk, int c8_begin, i
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
                 const int c = c8 * 8 + 2 * w + half;
-                const float mn = half ? bf16_hi(mnw[w]) : bf16_lo(mnw[w]);
-                const float mx = half ? bf16_hi(mxw[w]) : bf16_lo(mxw[w]);
+                const uint32_t mnb = half ? (mnw[w] & 0xffff0000u) : (mnw[w] << 16);
+                const uint32_t mxb = half ? (mxw[w] & 0xffff0000u) : (mxw[w] << 16);
 #pragma unroll
                 for (int h4 = 0; h4 < GP; h4 += 4) {
-                    const float4 p4 = *reinterpret_cast<const float4*>(&qp[c][h4]);
-                    const float4 n4 = *reinterpret_cast<const float4*>(&qn[c][h4]);
-                    const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
-                    const float nv[4] = {n4.x, n4.y, n4.z, n4.w};
+                    const float4 q4 = *reinterpret_cast<const float4*>(&qv[c][h4]);
+                    const uint4 m4 = *reinterpret_cast<const uint4*>(&qm[c][h4]);
+                    const float qq[4] = {q4.x, q4.y, q4.z, q4.w};
+                    const uint32_t mm[4] = {m4.x, m4.y, m4.z, m4.w};
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         if (h4 + e < G) {
-                            acc[h4 + e] = __fmaf_rn(pv[e], mx, acc[h4 + e]);
-                            acc[h4 + e] = __fmaf_rn(nv[e], mn, acc[h4 + e]);
+                            const float sel = __uint_as_float((mxb & mm[e]) | (mnb & ~mm[e]));
+                            acc[h4 + e] = __fmaf_rn(qq[e], sel, acc[h4 + e]);
                         }
                     }
                 }
@@ -103,8 +97,8 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims 
                                                                         const uint16_t* __restrict__ q, int pending) {
     constexpr int GP = (G + 3) / 4 * 4;
     extern __shared__ __align__(128) uint8_t s_raw[];
-    __shared__ __align__(16) float qp[kHeadDim][GP];
-    __shared__ __align__(16) float qn[kHeadDim][GP];
+    __shared__ __align__(16) float qv[kHeadDim][GP];      // q_c per head
+    __shared__ __align__(16) uint32_t qm[kHeadDim][GP];   // ~0 if q_c >= 0 (take max) else 0 (take min)
     __shared__ __align__(8) uint64_t bar[kScoreWarps][kRing];
     const int u = blockIdx.x, b = u / D.n_kv, m = u % D.n_kv;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -130,8 +124,8 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims 
         const int h = i / kHeadDim, c = i % kHeadDim;
         float x = 0.0f;
         if (h < G) x = bf16f(q[((size_t)b * D.n_qo + m * G + h) * kHeadDim + c]);
-        qp[c][h] = fmaxf(x, 0.0f);
-        qn[c][h] = fminf(x, 0.0f);
+        qv[c][h] = x;
+        qm[c][h] = x >= 0.0f ? 0xffffffffu : 0u;  // CFR-2: q_c >= 0 (incl. -0) uses the max
     }
     __syncthreads();
     if (!active) return;
@@ -143,7 +137,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims 
         const int slot = k % kRing;
         mbar_wait(&bar[warp][slot], (uint32_t)(k / kRing) & 1u);
         score_channels<G>(reinterpret_cast<const uint4*>(ring + slot * kChunkBytes) - (k * 4) * 2 * 32, k * 4,
-                          lane, qp, qn, acc);
+                          lane, qv, qm, acc);
         if (k + kRing < 4) {
             __syncwarp();  // all lanes are done with this slot
             if (lane == 0) {
@@ -175,6 +169,9 @@ constexpr int kWarps = kThreads / 32;
 
 template <int LPT>
 __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D, FkvLayer L,
+                                                                       int32_t* __restrict__ page_rows,
+                                                                       uint8_t* __restrict__ page_valid,
+                                                                       int32_t* __restrict__ page_cnt,
                                                                        const float* __restrict__ scores,
                                                                        const uint16_t* __restrict__ q,
                                                                        const uint16_t* __restrict__ k_new,
@@ -193,6 +190,8 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
     __shared__ int s_sel[kMaxK];
     __shared__ int s_res[kMaxK], s_res_slot[kMaxK];
     __shared__ int s_isfetch[kMaxK];
+    __shared__ int s_pslot[kMaxK];
+    __shared__ int s_flag;
     __shared__ int s_free[2 * kMaxK];
     __shared__ unsigned char s_used[2 * kMaxK];
     __shared__ uint32_t s_qa[kMaxG * kHeadDim / 2], s_qb[kMaxG * kHeadDim / 2];
@@ -202,8 +201,10 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
 
     // ---- a9 (fused, decode path): append this step's token before anything reads ctx
     int n_off = L.n_off[u];
+    int Lc_now = L.ctx[u];
     if (k_new) {
-        const int ctx0 = L.ctx[u];
+        const int ctx0 = Lc_now;
+        Lc_now = ctx0 + 1;
         append_unit(D, L, u, ctx0, k_new, v_new, 1, s_page);
         n_off = max(n_off, frontier_for(D, ctx0 + 1));
         if (tid == 0) {
@@ -223,7 +224,9 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
             s_qb[i] = qb32[i];
         }
     }
-    const int res_valid = L.res_valid[u];
+    // debug mode 3 (FREEKV_DEBUG_FULL_REFRESH): forget the resident set every step, so every
+    // unit re-fetches all K pages synchronously -- the GEN-X recall-bandwidth stress case
+    const int res_valid = D.full_refresh ? 0 : L.res_valid[u];
     for (int i = tid; i < K; i += kThreads) {
         s_res[i] = res_valid ? L.res_pages[(size_t)u * K + i] : -1;
         s_res_slot[i] = res_valid ? L.res_slot[(size_t)u * K + i] : -1;
@@ -245,30 +248,38 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
     }
     __syncthreads();
 
-    // ---- a1: correction (CFR-10), threads 0..G-1, sequential channel sums
-    if (tid < G) {
-        const uint16_t* qa = reinterpret_cast<const uint16_t*>(s_qa) + tid * kHeadDim;
-        const uint16_t* qb = reinterpret_cast<const uint16_t*>(s_qb) + tid * kHeadDim;
-        float dot = 0.0f, n1 = 0.0f, n2 = 0.0f;
-#pragma unroll 16
-        for (int c = 0; c < kHeadDim; ++c) {
+    // ---- a1: correction (CFR-10): lanes 0..G-1 of the last warp run the sequential channel
+    // sums in 4 chunks of 32 channels, interleaved with the radix passes below (where the
+    // other warps wait on warp 0's digit scan) so they never lengthen the critical path
+    const bool cos_lane = warp == kWarps - 1 && lane < G;
+    float c_dot = 0.0f, c_n1 = 0.0f, c_n2 = 0.0f;
+    auto cos_chunk = [&](int part) {
+        const uint16_t* qa = reinterpret_cast<const uint16_t*>(s_qa) + lane * kHeadDim;
+        const uint16_t* qb = reinterpret_cast<const uint16_t*>(s_qb) + lane * kHeadDim;
+#pragma unroll 8
+        for (int c = part * 32; c < part * 32 + 32; ++c) {
             const float x = bf16f(qa[c]), y = bf16f(qb[c]);
-            dot = __fmaf_rn(x, y, dot);  // exact product, one rounding = fl(dot + x*y)
-            n1 = __fmaf_rn(x, x, n1);
-            n2 = __fmaf_rn(y, y, n2);
+            c_dot = __fmaf_rn(x, y, c_dot);  // exact product, one rounding = fl(dot + x*y)
+            c_n1 = __fmaf_rn(x, x, c_n1);
+            c_n2 = __fmaf_rn(y, y, c_n2);
         }
-        s_cos[tid] = (n1 == 0.0f || n2 == 0.0f) ? 0.0f : __fdiv_rn(dot, __fmul_rn(__fsqrt_rn(n1), __fsqrt_rn(n2)));
-    }
+        if (part == 3)
+            s_cos[lane] = (c_n1 == 0.0f || c_n2 == 0.0f)
+                              ? 0.0f
+                              : __fdiv_rn(c_dot, __fmul_rn(__fsqrt_rn(c_n1), __fsqrt_rn(c_n2)));
+    };
 
     int cnt;
     if (rank_all) {
         for (int i = tid; i < K; i += kThreads) s_sel[i] = i < n_cand ? n_sink + i : -1;
+        if (cos_lane)
+            for (int part = 0; part < 4; ++part) cos_chunk(part);
         cnt = n_cand > 0 ? n_cand : 0;
         __syncthreads();
     } else {
         const float* su = s_sc;
         const int jb = tid * LPT;
-        // ---- CFR-4: max per head
+        // ---- CFR-4: max per head (exact, order-free); the G heads' shuffles interleave
         float M[kMaxG];
 #pragma unroll
         for (int g = 0; g < kMaxG; ++g) {
@@ -279,25 +290,29 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
                     const int j = jb + l;
                     if (j >= n_sink && j < n_off) M[g] = fmaxf(M[g], su[g * srow + j]);
                 }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) M[g] = fmaxf(M[g], __shfl_xor_sync(0xffffffffu, M[g], o));
-                if (lane == 0) s_redm[warp][g] = M[g];
             }
         }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int g = 0; g < kMaxG; ++g) M[g] = fmaxf(M[g], __shfl_xor_sync(0xffffffffu, M[g], o));
+        if (lane == 0)
+#pragma unroll
+            for (int g = 0; g < kMaxG; ++g) s_redm[warp][g] = M[g];
         __syncthreads();
 #pragma unroll
-        for (int g = 0; g < kMaxG; ++g) {
-            if (g < G) {
-                float v = s_redm[lane][g];
+        for (int g = 0; g < kMaxG; ++g) M[g] = lane < kWarps ? s_redm[lane][g] : -INFINITY;
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-                M[g] = v;
-            }
-        }
-        // ---- CFR-5/6: e = cexp2(s - m); Z = pairwise tree in page-id order
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int g = 0; g < kMaxG; ++g) M[g] = fmaxf(M[g], __shfl_xor_sync(0xffffffffu, M[g], o));
+        // ---- CFR-5/6: e = cexp2(s - m); Z = pairwise tree in page-id order: thread-local tree over
+        // its LPT contiguous leaves, xor butterfly over the 32 lanes, butterfly over the warp
+        // partials (lanes >= kWarps hold +0 leaves, which leave a pairwise tree's value unchanged)
         float Z[kMaxG];
 #pragma unroll
         for (int g = 0; g < kMaxG; ++g) {
+            Z[g] = 0.0f;
             if (g < G) {
                 float e[LPT];
 #pragma unroll
@@ -309,22 +324,23 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
                 for (int w = 1; w < LPT; w <<= 1)
 #pragma unroll
                     for (int l = 0; l < LPT; l += 2 * w) e[l] = __fadd_rn(e[l], e[l + w]);
-                float v = e[0];
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
-                if (lane == 0) s_redz[warp][g] = v;
+                Z[g] = e[0];
             }
         }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+            for (int g = 0; g < kMaxG; ++g) Z[g] = __fadd_rn(Z[g], __shfl_xor_sync(0xffffffffu, Z[g], o));
+        if (lane == 0)
+#pragma unroll
+            for (int g = 0; g < kMaxG; ++g) s_redz[warp][g] = Z[g];
         __syncthreads();
 #pragma unroll
-        for (int g = 0; g < kMaxG; ++g) {
-            if (g < G) {
-                float v = s_redz[lane][g];
+        for (int g = 0; g < kMaxG; ++g) Z[g] = lane < kWarps ? s_redz[lane][g] : 0.0f;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
-                Z[g] = v;
-            }
-        }
+        for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+            for (int g = 0; g < kMaxG; ++g) Z[g] = __fadd_rn(Z[g], __shfl_xor_sync(0xffffffffu, Z[g], o));
         // ---- CFR-7/8: p = e / Z; pooled = sequential sum over g; CFR-9 keys
         uint32_t key[LPT];
         bool cand[LPT];
@@ -360,6 +376,7 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
             }
             for (int i = tid; i < 256; i += kThreads) s_hist[(pass + 1) & 1][i] = 0;
             __syncthreads();
+            if (cos_lane) cos_chunk(pass);
             if (warp == 0) {
                 int bins[8], lsum = 0;
 #pragma unroll
@@ -436,6 +453,7 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
         else if (D.mode == 2 || D.tau <= 0.0f) flag = 0;
         else flag = mean < D.tau;
         if (!res_valid) flag = 1;
+        s_flag = flag;
         L.flags[u] = (uint8_t)flag;
         L.cbar[u] = mean;
         L.pend_front[u] = n_off;
@@ -450,14 +468,14 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
             for (int i = 0; i < K; ++i)
                 if (s_res[i] == Sa) {
                     f = 0;
-                    L.pend_slot[(size_t)u * K + tid] = s_res_slot[i];
+                    s_pslot[tid] = s_res_slot[i];
                 }
         }
         s_isfetch[tid] = f;
         if (s_res[tid] >= 0) s_used[s_res_slot[tid]] = 1;
         L.pend_pages[(size_t)u * K + tid] = Sa;
         if (pages_out) pages_out[(size_t)u * K + tid] = Sa;
-        if (Sa < 0) L.pend_slot[(size_t)u * K + tid] = -1;
+        if (Sa < 0) s_pslot[tid] = -1;
     }
     __syncthreads();
     if (warp == 0) {
@@ -478,7 +496,7 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
             if (fe) {
                 const int r = nf + __popc(bal & ((1u << lane) - 1u));
                 const int slot = s_free[r];
-                L.pend_slot[(size_t)u * K + a] = slot;
+                s_pslot[a] = slot;
                 L.fetch_page[(size_t)u * K + r] = s_sel[a];
                 L.fetch_slot[(size_t)u * K + r] = slot;
             }
@@ -488,6 +506,50 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
             L.n_fetch[u] = nf;
             L.pend_cnt[u] = cnt;
         }
+    }
+    __syncthreads();
+    for (int i = tid; i < K; i += kThreads) L.pend_slot[(size_t)u * K + i] = s_pslot[i];
+    // ---- this step's attention page list (row a7), one entry per page: arena row of the
+    // page's K block and its valid tokens -- sink pages, the pages in use (S_i if corrected,
+    // the resident set otherwise), local pages [f*p, Lc) (reading A-9)
+    {
+        const int flag = s_flag;
+        const int Lc = Lc_now;
+        const int p = D.p;
+        const int sink_tok = min(D.S_tok, Lc);
+        const int n_sp = (sink_tok + p - 1) / p;
+        int n_sel = 0;
+        if (flag) {
+            n_sel = cnt;
+        } else {
+            for (int i = 0; i < K; ++i) n_sel += s_res[i] >= 0;
+        }
+        const int f = flag ? n_off : L.res_front[u];
+        const int n_last = (Lc - 1) / p;
+        const int n_loc = (Lc > f * p) ? (n_last - f + 1) : 0;
+        const size_t pe = page_elems(D);
+        const int total = n_sp + n_sel + n_loc;
+        for (int i = tid; i < total; i += kThreads) {
+            const uint16_t* base;
+            int valid;
+            if (i < n_sp) {
+                base = L.sink + ((size_t)u * D.n_sink + i) * pe;
+                valid = min(p, sink_tok - i * p);
+            } else if (i < n_sp + n_sel) {
+                const int a = i - n_sp;
+                const int slot = flag ? s_pslot[a] : s_res_slot[a];
+                base = L.slots + ((size_t)u * 2 * K + slot) * pe;
+                valid = p;
+            } else {
+                const int j = f + (i - n_sp - n_sel);
+                base = L.ring + ((size_t)u * D.R_loc + (j % D.R_loc)) * pe;
+                valid = min(p, Lc - j * p);
+            }
+            const int row = (int)((base - L.arena) / kHeadDim);
+            page_rows[(size_t)u * D.P_max + i] = row;
+            page_valid[(size_t)u * D.P_max + i] = (uint8_t)valid;
+        }
+        if (tid == 0) page_cnt[u] = total;
     }
 }
 
@@ -501,6 +563,8 @@ static void launch_score_g(const FkvDims& D, const FkvLayer& L, float* scores, c
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(fkv_score_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(fkv_score_kernel<G>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
         configured = true;
     }
     fkv_score_kernel<G><<<dim3(D.U, gy), per_cta, smem, s>>>(D, L, scores, q, pending);
@@ -530,15 +594,18 @@ static cudaError_t launch_fin(const FkvDims& D, const FkvLayer& L, const FkvScra
     if (smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(fkv_select_finalize_kernel<LPT>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(fkv_select_finalize_kernel<LPT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return e;
         configured = smem;
     }
-    fkv_select_finalize_kernel<LPT><<<D.U, kThreads, smem, s>>>(D, L, X.scores, q, k_new, v_new, pages_out,
-                                                                corrected_out);
+    fkv_select_finalize_kernel<LPT><<<D.U, kThreads, smem, s>>>(D, L, X.page_rows, X.page_valid, X.page_cnt, X.scores, q, k_new,
+                                                                v_new, pages_out, corrected_out);
     return cudaGetLastError();
 }
 
-// lpt = leaves per thread of the 1024-thread tree; 1024 * lpt >= next_pow2(n_off) for every n_off the
+// lpt = leaves per thread of the kThreads-thread tree; kThreads * lpt >= next_pow2(n_off) for every n_off the
 // handle can reach (a larger zero-padded tree gives the same Z, CFR-6).  k_new/v_new non-NULL fuses
 // this step's single-token append (row a9) into the kernel.
 cudaError_t launch_finalize(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
@@ -550,6 +617,8 @@ cudaError_t launch_finalize(const FkvDims& D, const FkvLayer& L, const FkvScratc
         case 2: return launch_fin<2>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, s);
         case 4: return launch_fin<4>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, s);
         case 8: return launch_fin<8>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, s);
+        case 16: return launch_fin<16>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, s);
+        case 32: return launch_fin<32>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, s);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -1,0 +1,9 @@
+python -c "import __graft_entry__ as g; g.build()"
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest15.log 2>&1; echo "rc=$?" >> gpurun_out/pytest15.log
+timeout 300 python tools/kbench.py --layers 4 --steps 20 --warmup 5 --graph > gpurun_out/kb15_graph.json 2>&1
+timeout 300 python tools/kbench.py --layers 4 --steps 20 --warmup 5 --graph --no-profile > gpurun_out/kb15_graph_noprof.json 2>&1
+FREEKV_DEBUG_FULL_REFRESH=1 timeout 300 python tools/kbench.py --layers 4 --steps 10 --warmup 3 --graph > gpurun_out/kb15_genx.json 2>&1
+K2="python tools/kbench.py --layers 2 --steps 2 --warmup 5 --no-profile"
+timeout 300 $K2 > gpurun_out/kb15_plain.log 2>&1 && \
+timeout 600 ncu -k regex:fkv_ --cache-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__cycles_active.avg,sm__cycles_active.max --clock-control none -s 70 -c 28 --csv --log-file gpurun_out/kb15_launches.csv $K2 > gpurun_out/ncu15.log 2>&1
+echo "rc=$?" >> gpurun_out/ncu15.log
