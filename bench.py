@@ -44,7 +44,7 @@ METRIC = "decode-step µs/layer and tokens/s at 32K ctx; attn HBM GB/s; recall G
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--steps", type=int, default=256)
     ap.add_argument("--warmup", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
@@ -73,7 +73,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except Exception:
@@ -82,6 +82,10 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+
+    def mark(self):
+        """Start of the timed region: later samples are the ones reported (if any arrive)."""
+        self.first = len(self.lines)
 
     def stop(self):
         if self.proc is None:
@@ -93,7 +97,8 @@ class ClockSampler:
             self.proc.kill()
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines[getattr(self, "first", 0):] or self.lines
+        for ln in lines:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 8:
                 continue
@@ -219,6 +224,11 @@ def run_ours(args, c, rank, world, local_rank):
         if world > 1:
             torch.distributed.barrier()
 
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    t_wait = time.time()
+    while not clocks.lines and time.time() - t_wait < 3.0:  # let nvidia-smi start sampling
+        time.sleep(0.05)
     step = 0
     for _ in range(args.warmup):
         one_step(step)
@@ -231,8 +241,7 @@ def run_ours(args, c, rank, world, local_rank):
         fkv.synchronize()
     run = one_step if args.eager else graph_step
     # ---- timed region (device time, CUDA events on the compute stream)
-    clocks = ClockSampler(local_rank)
-    clocks.start()
+    clocks.mark()
     barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -334,32 +343,32 @@ def run_oracle_sample(c, seconds, seed):
     import synth
     from oracle import oracle as O
     n_kv, n_qo, d, p = c["n_kv"], c["n_qo"], 128, 32
-    steps_max = 64
-    ocfg = O.OracleConfig(n_layers=1, batch=1, n_qo=n_qo, n_kv=n_kv, head_dim=d, page_size=p,
+    nb = c["batch"]
+    steps_max = 256
+    ocfg = O.OracleConfig(n_layers=1, batch=nb, n_qo=n_qo, n_kv=n_kv, head_dim=d, page_size=p,
                           budget_tokens=c["budget"], sink_tokens=c["sink"], window_tokens=c["window"],
                           max_ctx_tokens=c["ctx"] + steps_max + 1, tau=c["tau"])
     eng = O.OracleEngine(ocfg)
     K = ocfg.K
-    k, v = synth.gen_prefill(1, n_kv, d, p, c["ctx"], c["sink"] // p, K, seed, 0)
+    k, v = synth.gen_prefill(nb, n_kv, d, p, c["ctx"], c["sink"] // p, K, seed, 0)
     eng.append(0, synth.bf16_bits(k), synth.bf16_bits(v))
     del k, v
-    qp = synth.QueryProcess(1, n_qo, n_kv, d, seed, 0, event_rate=c["event_rate"])
-    pre = []
-    for i in range(steps_max):
-        q, _ = qp.next()
-        kn, vn = synth.gen_decode_kv(1, n_kv, d, p, c["ctx"] + i, seed, 0)
-        pre.append((synth.bf16_bits(q), synth.bf16_bits(kn), synth.bf16_bits(vn)))
+    qp = synth.QueryProcess(nb, n_qo, n_kv, d, seed, 0, event_rate=c["event_rate"])
     t0 = time.perf_counter()
     n = 0
+    busy = 0.0
     while n < steps_max and (time.perf_counter() - t0) < seconds:
-        eng.step(0, *pre[n])
+        q, _ = qp.next()
+        kn, vn = synth.gen_decode_kv(nb, n_kv, d, p, c["ctx"] + n, seed, 0)
+        a = (synth.bf16_bits(q), synth.bf16_bits(kn), synth.bf16_bits(vn))
+        t1 = time.perf_counter()
+        eng.step(0, *a)  # O-1..O-6 of one layer for the whole batch
+        busy += time.perf_counter() - t1
         n += 1
-    dt = time.perf_counter() - t0
-    per_unit_layer_step = dt / (n * n_kv)
-    full_step = per_unit_layer_step * c["batch"] * n_kv * c["n_layers"]
-    return {"value": c["batch"] / full_step, "unit": "tokens/s", "cores": O.num_threads(), "kind": "oracle",
-            "sample": f"1 layer x {n_kv} units (batch row 0) x {n} decode steps at ctx {c['ctx']}, "
-                      f"{dt:.1f}s; extrapolated linearly to {c['batch']}x{n_kv} units x {c['n_layers']} layers",
+    full_step = busy / n * c["n_layers"]
+    return {"value": nb / full_step, "unit": "tokens/s", "cores": O.num_threads(), "kind": "oracle",
+            "sample": f"1 layer x {nb * n_kv} units (whole batch) x {n} decode steps at ctx {c['ctx']}, "
+                      f"{busy:.1f}s of oracle time; x{c['n_layers']} layers per token step",
             "us_per_layer": full_step / c["n_layers"] * 1e6}
 
 

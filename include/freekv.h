@@ -182,6 +182,11 @@ freekv_status freekv_get_dims(freekv_handle* h, int32_t* K, int32_t* n_page_max,
 freekv_status freekv_profile_begin(freekv_handle* h, int32_t max_launches);
 freekv_status freekv_profile_end(freekv_handle* h, float* ms /*[7]*/, int32_t* launches /*[7]*/);
 
+/* Diagnostics: with FREEKV_TRACE=1 in the environment at freekv_init, kernels write
+ * %globaltimer stamps [class 8][entity 4096][stamp 8] (ns); this copies n <= 262144
+ * of them to host memory `out` and clears the buffer.  Blocking. */
+freekv_status freekv_debug_trace(freekv_handle* h, uint64_t* out, size_t n);
+
 /* Wait for all work of the handle (both streams); surfaces async errors. */
 freekv_status freekv_synchronize(freekv_handle* h);
 void freekv_destroy(freekv_handle* h);

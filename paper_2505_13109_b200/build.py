@@ -14,8 +14,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-I" + os.path.join(HERE, "..", "include")]
 
-SOURCES = ["api.cu", "append.cu", "select.cu", "recall.cu", "attn.cu"]
-HEADERS = ["fkv_internal.cuh"]
+SOURCES = ["api.cu", "append.cu", "select.cu", "select_fused.cu", "recall.cu", "attn.cu"]
+HEADERS = ["fkv_internal.cuh", "append_unit.cuh"]
 
 
 def _mtime(p):

@@ -54,6 +54,9 @@ struct freekv_handle {
     std::vector<int> ctx_host;
     std::vector<int> recall_pending;
     int lpt = 1;  // leaves per thread of the finalize tree (fixed per handle, CFR-6)
+    int sel_cluster = 8, sel_lptm = 1;  // fused select: CTAs per unit, max leaves per thread
+    bool fused_select = false;          // FREEKV_SELECT=fused selects the one-launch cluster kernel
+    bool pdl = true;                    // programmatic dependent launch (FREEKV_PDL=0 disables)
     bool serial_recall = false;  // diagnostics: FREEKV_SERIAL_RECALL=1 runs background recall on the compute stream
     // profiling (freekv_profile_begin/end)
     bool prof = false;
@@ -104,6 +107,8 @@ freekv_status validate(const freekv_config* c, FkvDims* D) {
         return fail(FREEKV_EINVAL, "(budget - sink - window) % page_size != 0 (K = (B-S-W)/p, reading A-6)");
     const int K = (c->budget_tokens - c->sink_tokens - c->window_tokens) / p;
     if (K < 1 || K > 256) return fail(FREEKV_EUNSUPPORTED, "K = (B-S-W)/p must be in [1, 256]");
+    if (c->sink_tokens / p + K + c->window_tokens / p + 2 > 254)
+        return fail(FREEKV_EUNSUPPORTED, "attention pages per unit (S/p + K + W/p + 2) must be <= 254");
     if (c->max_ctx_tokens <= 0) return fail(FREEKV_EINVAL, "max_ctx_tokens must be positive");
     const int n_page_host = c->max_ctx_tokens / p + 1;
     if (n_page_host > 8192) return fail(FREEKV_EUNSUPPORTED, "max_ctx_tokens / page_size > 8191 pages");
@@ -169,8 +174,8 @@ Sizes compute_sizes(const freekv_config* c, const FkvDims& D) {
     s.layer_bytes = o;
     o = 0;
     s.o_scores = take(U * D.G * D.n_page_max * 4);
-    s.o_part_o = take((size_t)2 * kMaxAttnWarps * D.G * D.d * 4);
-    s.o_part_ml = take((size_t)2 * kMaxAttnWarps * D.G * 2 * 4);
+    s.o_part_o = take((size_t)4 * kMaxAttnWarps * D.G * D.d * 4);
+    s.o_part_ml = take((size_t)4 * kMaxAttnWarps * D.G * 2 * 4);
     s.o_page_rows = take(U * D.P_max * 4);
     s.o_page_cnt = take(U * 4);
     s.o_page_valid = take(U * D.P_max);
@@ -232,15 +237,23 @@ freekv_status do_select(freekv_handle* h, int layer, const void* q, int32_t* pag
         FKV_CUDA(cudaStreamWaitEvent(s, h->ev_recall[layer], cudaEventWaitExternal));
     else if (h->recall_pending[layer])
         FKV_CUDA(cudaStreamWaitEvent(s, h->ev_recall[layer], 0));
-    const int mno = h->capturing ? max_n_off(h->D, h->D.max_ctx) : max_n_off(h->D, h->ctx_host[layer] + pending);
-    if (h->capturing || mno - h->D.n_sink > h->D.K)
-        FKV_CUDA(timed(h, K_SCORE, s, [&] {
-            return launch_score(h->D, h->layers[layer], h->X, (const uint16_t*)q, mno, pending, s);
+    if (h->fused_select) {
+        FKV_CUDA(timed(h, K_FINALIZE, s, [&] {
+            return launch_select_fused(h->D, h->layers[layer], h->X, (const uint16_t*)q, (const uint16_t*)k_new,
+                                       (const uint16_t*)v_new, pages_out, corr_out, h->sel_cluster, h->sel_lptm, s);
         }));
-    FKV_CUDA(timed(h, K_FINALIZE, s, [&] {
-        return launch_finalize(h->D, h->layers[layer], h->X, (const uint16_t*)q, (const uint16_t*)k_new,
-                               (const uint16_t*)v_new, pages_out, corr_out, h->lpt, s);
-    }));
+    } else {
+        const int mno =
+            h->capturing ? max_n_off(h->D, h->D.max_ctx) : max_n_off(h->D, h->ctx_host[layer] + pending);
+        if (h->capturing || mno - h->D.n_sink > h->D.K)
+            FKV_CUDA(timed(h, K_SCORE, s, [&] {
+                return launch_score(h->D, h->layers[layer], h->X, (const uint16_t*)q, mno, pending, s);
+            }));
+        FKV_CUDA(timed(h, K_FINALIZE, s, [&] {
+            return launch_finalize(h->D, h->layers[layer], h->X, (const uint16_t*)q, (const uint16_t*)k_new,
+                                   (const uint16_t*)v_new, pages_out, corr_out, h->lpt, h->pdl, s);
+        }));
+    }
     if (k_new && !h->capturing) h->ctx_host[layer] += 1;
     return FREEKV_OK;
 }
@@ -266,10 +279,10 @@ freekv_status do_recall(freekv_handle* h, int layer, cudaStream_t s) {
 freekv_status do_attn(freekv_handle* h, int layer, const void* q, float* out, cudaStream_t s) {
     if (!q || !out) return fail(FREEKV_EINVAL, "q/out is NULL");
     FKV_CUDA(timed(h, K_ATTN_SPLIT, s, [&] {
-        return launch_attn_split(h->D, h->layers[layer], h->X, (const uint16_t*)q, 0, h->tmap_kv, h->arena, s);
+        return launch_attn_split(h->D, h->layers[layer], h->X, (const uint16_t*)q, 0, h->tmap_kv, h->arena, false, s);
     }));
     FKV_CUDA(timed(h, K_ATTN_COMBINE, s, [&] {
-        return launch_attn_combine(h->D, h->layers[layer], h->X, (const uint16_t*)q, out, s);
+        return launch_attn_combine(h->D, h->layers[layer], h->X, (const uint16_t*)q, out, 0, h->pdl, s);
     }));
     return FREEKV_OK;
 }
@@ -286,7 +299,7 @@ freekv_status do_step_tail(freekv_handle* h, int layer, const void* q, float* ou
     FkvLayer& L = h->layers[layer];
     FKV_CUDA(cudaEventRecord(h->ev_select[layer], cs));
     FKV_CUDA(cudaStreamWaitEvent(h->ss, h->ev_select[layer], 0));
-    FKV_CUDA(timed(h, K_RECALL_SYNC, h->ss, [&] { return launch_recall(D, L, 1, h->ss); }));
+    FKV_CUDA(timed(h, K_RECALL_SYNC, h->ss, [&] { return launch_recall(D, L, 1, h->ss, h->X.trace); }));
     if (h->capturing)  // external record first: the internal record below joins every ss node back into cs
         FKV_CUDA(cudaEventRecordWithFlags(h->ev_sync_x[layer], h->ss, cudaEventRecordExternal));
     FKV_CUDA(cudaEventRecord(h->ev_sync[layer], h->ss));
@@ -297,15 +310,15 @@ freekv_status do_step_tail(freekv_handle* h, int layer, const void* q, float* ou
         h->recall_pending[layer] = 1;
     } else {
         FKV_CUDA(cudaStreamWaitEvent(h->rs, h->ev_sync[layer], 0));
-        FKV_CUDA(timed(h, K_RECALL_BG, h->rs, [&] { return launch_recall(D, L, 0, h->rs); }));
+        FKV_CUDA(timed(h, K_RECALL_BG, h->rs, [&] { return launch_recall(D, L, 0, h->rs, h->X.trace); }));
         FKV_CUDA(cudaEventRecord(h->ev_recall[layer], h->rs));
         h->recall_pending[layer] = 1;
     }
-    FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] { return launch_attn_split(D, L, h->X, (const uint16_t*)q, 1, h->tmap_kv, h->arena, cs); }));
+    FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] { return launch_attn_split(D, L, h->X, (const uint16_t*)q, 1, h->tmap_kv, h->arena, h->pdl, cs); }));
     FKV_CUDA(cudaStreamWaitEvent(cs, h->ev_sync[layer], 0));
-    FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] { return launch_attn_split(D, L, h->X, (const uint16_t*)q, 2, h->tmap_kv, h->arena, cs); }));
+    FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] { return launch_attn_split(D, L, h->X, (const uint16_t*)q, 2, h->tmap_kv, h->arena, false, cs); }));
     FKV_CUDA(timed(h, K_ATTN_COMBINE, cs, [&] {
-        return launch_attn_combine(D, L, h->X, (const uint16_t*)q, out, cs);
+        return launch_attn_combine(D, L, h->X, (const uint16_t*)q, out, 1, h->pdl, cs);
     }));
     return FREEKV_OK;
 }
@@ -425,6 +438,14 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         int P2 = 1;
         while (P2 < D.n_page_host) P2 <<= 1;
         h->lpt = P2 <= kFinalizeThreads ? 1 : P2 / kFinalizeThreads;
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        h->sel_cluster = (P2 >= 2048 && D.U * 8 < 2 * sms) ? 16 : 8;  // few units: wider clusters
+        h->sel_lptm = std::max(1, P2 / (h->sel_cluster * 128));
+        const char* fs = getenv("FREEKV_SELECT");
+        h->fused_select = fs && fs[0] == 'f';
+        const char* pd = getenv("FREEKV_PDL");
+        h->pdl = !(pd && pd[0] == '0');
         if (h->lpt > 8) {
             delete h;
             return fail(FREEKV_EUNSUPPORTED, "max_ctx_tokens / page_size > 8192 pages");
@@ -443,6 +464,17 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         long long T = std::min<long long>({(long long)warps, (long long)kMaxAttnWarps, V, 254LL * D.U});
         while (T > 1 && T * V >= (1LL << 31)) T /= 2;
         h->D.attn_warps = (int)std::max(1LL, T);
+    }
+    h->X.trace = nullptr;
+    {
+        const char* tr = getenv("FREEKV_TRACE");
+        if (tr && tr[0] == '1') {
+            const size_t n = (size_t)8 * 4096 * 8;
+            if (cudaMalloc(&h->X.trace, n * 8) != cudaSuccess || cudaMemset(h->X.trace, 0, n * 8) != cudaSuccess) {
+                freekv_destroy(h);
+                return fail(FREEKV_ECUDA, "trace buffer");
+            }
+        }
     }
     {
         const char* fr = getenv("FREEKV_DEBUG_FULL_REFRESH");
@@ -657,6 +689,17 @@ freekv_status freekv_synchronize(freekv_handle* h) {
     return sync_both(h);
 }
 
+freekv_status freekv_debug_trace(freekv_handle* h, uint64_t* out, size_t n) {
+    if (!h) return fail(FREEKV_EINVAL, "handle is NULL");
+    if (!h->X.trace) return fail(FREEKV_ESTATE, "tracing is off (set FREEKV_TRACE=1 before freekv_init)");
+    freekv_status st = sync_both(h);
+    if (st != FREEKV_OK) return st;
+    const size_t cap = (size_t)8 * 4096 * 8;
+    FKV_CUDA(cudaMemcpy(out, h->X.trace, std::min(n, cap) * 8, cudaMemcpyDeviceToHost));
+    FKV_CUDA(cudaMemset(h->X.trace, 0, cap * 8));
+    return FREEKV_OK;
+}
+
 static void drop_graphs(freekv_handle* h) {
     if (h->g_compute) cudaGraphExecDestroy(h->g_compute);
     if (h->g_recall) cudaGraphExecDestroy(h->g_recall);
@@ -779,6 +822,7 @@ void freekv_destroy(freekv_handle* h) {
         if (e) cudaEventDestroy(e);
     for (auto e : h->prof_pool) cudaEventDestroy(e);
     if (h->ss) cudaStreamDestroy(h->ss);
+    if (h->X.trace) cudaFree(h->X.trace);
     delete h;
 }
 

@@ -104,7 +104,7 @@ __device__ __forceinline__ const uint16_t* page_ptr(const FkvDims& D, const FkvL
 // 128-byte swizzle (16-byte chunk c of row r lives at chunk c ^ (r % 8)).  The
 // fragment mapping below is chosen so every quarter-warp LDS.128 hits 8
 // distinct chunks (conflict-free) under that swizzle.
-constexpr int kMaxStages = 4;       // slab stages per warp (template parameter NST <= kMaxStages)
+// slab stages per warp: template parameter NST (2, 3 or 4), FREEKV_ATTN_STAGES
 constexpr int kBoxBytes = 16 * 128; // 16 rows x 64 channels bf16
 constexpr int kSlabBytes = 4 * kBoxBytes;
 
@@ -239,6 +239,38 @@ __device__ __forceinline__ void compute_slab(const uint8_t* st, int valid, const
 
 __device__ __forceinline__ long long range_start(long long w, long long V, long long T) { return w * V / T; }
 
+// Units attended in `phase`: all (0), unflagged (1), corrected (2).  Phases 1/2 lay only
+// their own units end to end, so each phase's warps share exactly that phase's pages.
+__device__ __forceinline__ bool in_phase(const FkvLayer& L, int u, int phase) {
+    return phase == 0 || ((L.flags[u] != 0) == (phase == 2));
+}
+
+// Warp-cooperative: number of phase units, and the units of ranks r0 and r0 + 1.
+__device__ __forceinline__ int phase_units(const FkvDims& D, const FkvLayer& L, int phase, int r0, int lane,
+                                           int& u0, int& u1) {
+    u0 = u1 = -1;
+    if (phase == 0) {
+        u0 = r0;
+        u1 = r0 + 1;
+        return D.U;
+    }
+    int cnt = 0;
+    for (int base = 0; base < D.U; base += 32) {
+        const int u = base + lane;
+        const bool f = u < D.U && in_phase(L, u, phase);
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        const int before = __popc(bal & ((1u << lane) - 1u));
+        if (f && cnt + before == r0) u0 = u;
+        if (f && cnt + before == r0 + 1) u1 = u;
+        cnt += __popc(bal);
+    }
+    // broadcast the (single) owners
+    const unsigned h0 = __ballot_sync(0xffffffffu, u0 >= 0), h1 = __ballot_sync(0xffffffffu, u1 >= 0);
+    u0 = h0 ? __shfl_sync(0xffffffffu, u0, __ffs(h0) - 1) : -1;
+    u1 = h1 ? __shfl_sync(0xffffffffu, u1, __ffs(h1) - 1) : -1;
+    return cnt;
+}
+
 // phase: 0 = every unit; 1 = unflagged units only (their pages are resident, so this
 // half runs while the synchronous recall of the corrected units is in flight);
 // 2 = corrected units only (after that recall).  Each unit is attended in exactly
@@ -256,7 +288,10 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2) fkv_a
     const int g = lane >> 2, t = lane & 3;
     const int w = blockIdx.x * kAttnWarpsPerCta + warp;
     const int T = D.attn_warps;
+    pdl_trigger();  // the next kernel (attention phase 2 / combine) may start its prologue
     if (w >= T) return;
+    const int tcls = 4 + phase;  // trace class 4/5/6 = attention phase 0/1/2
+    if (lane == 0) trace_stamp(X.trace, tcls, w, 0);
     uint8_t* ring = s_stage + warp * (kStages * kSlabBytes);
     if (lane == 0) {
 #pragma unroll
@@ -265,19 +300,31 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2) fkv_a
     }
     __syncwarp();
     uint32_t phase_bits = 0u;  // parity of each stage's next completion
-    const long long V = (long long)D.U * D.P_max;
-    const long long s0 = range_start(w, V, T), s1 = range_start(w + 1, V, T);
+    pdl_wait();  // the select kernel's page lists and flags are complete
     const int G = D.G, spp = D.p >> 4, lspp = spp == 1 ? 0 : (spp == 2 ? 1 : 2);
     const float sc = D.attn_c;
+    // this phase's virtual page list: its units end to end, P_max pages each
+    int nu = D.U;
+    if (phase != 0) {
+        int d0, d1;
+        nu = phase_units(D, L, phase, 0, lane, d0, d1);
+    }
+    const long long V = (long long)nu * D.P_max;
+    const int Tp = (int)min((long long)T, V);  // warps of this phase: every one owns >= 1 page
+    if (w >= Tp) return;
+    const long long s0 = range_start(w, V, Tp), s1 = range_start(w + 1, V, Tp);
+    int ua = -1, ub = -1;  // units of ranks s0 / P_max and s0 / P_max + 1
+    if (s0 < s1) phase_units(D, L, phase, (int)(s0 / D.P_max), lane, ua, ub);
+    const int rec_base = phase == 2 ? T : 0;  // records of phase 2 live after phase 1's
     int k_rec = 0;
     for (long long seg = s0; seg < s1; ++k_rec) {
-        const int u = (int)(seg / D.P_max);
-        const long long seg_end = min(s1, (long long)(u + 1) * D.P_max);
-        const int pa = (int)(seg - (long long)u * D.P_max);
+        const int r = (int)(seg / D.P_max);
+        const int u = k_rec == 0 ? ua : ub;
+        const long long seg_end = min(s1, (long long)(r + 1) * D.P_max);
+        const int pa = (int)(seg - (long long)r * D.P_max);
         seg = seg_end;
-        if (phase != 0 && ((L.flags[u] != 0) != (phase == 2))) continue;  // attended in the other phase
         const int32_t* prow = X.page_rows + (size_t)u * D.P_max;  // written by the select kernel
-        const int pb = min((int)(seg_end - (long long)u * D.P_max), X.page_cnt[u]);
+        const int pb = min((int)(seg_end - (long long)r * D.P_max), X.page_cnt[u]);
         const int b = u / D.n_kv, m = u % D.n_kv;
         // Q fragments: lane (g, t) holds Q[head g][64b + 16t + 8e .. +8] (heads >= G are zero)
         uint4 qa[2][2];
@@ -308,6 +355,7 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2) fkv_a
                 my_valid = X.page_valid[(size_t)u * D.P_max + cb + lane];
             }
             const int nx = np * spp;
+            if (lane == 0) trace_stamp(X.trace, tcls, w, 1);
             auto slab_of = [&](int x, int& row) {  // warp-uniform; spp = 1 << lspp
                 const int pi = x >> lspp, sl = x & (spp - 1);
                 row = __shfl_sync(0xffffffffu, my_row, pi) + sl * 16;
@@ -331,6 +379,7 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2) fkv_a
                 if (valid > 0) {
                     mbar_wait(&bar[warp][stg], (phase_bits >> stg) & 1u);
                     phase_bits ^= 1u << stg;
+                    if (i == 0 && lane == 0) trace_stamp(X.trace, tcls, w, 2);
                     compute_slab(ring + stg * kSlabBytes, valid, qa, sc, g, t, m_run, l_run, oacc);
                 }
                 __syncwarp();  // every lane is done with this stage before it is refilled
@@ -340,6 +389,7 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2) fkv_a
                 }
             }
         }
+        if (lane == 0) trace_stamp(X.trace, tcls, w, 3);
         // ---- partial record (w, k_rec) of unit u: unnormalised, relative to m_run.  Lane (g, t)
         // holds heads 2t, 2t+1; l is summed over the 8 lanes g of the same t
         float l0 = l_run[0], l1 = l_run[1];
@@ -348,7 +398,7 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2) fkv_a
             l0 += __shfl_xor_sync(0xffffffffu, l0, o);
             l1 += __shfl_xor_sync(0xffffffffu, l1, o);
         }
-        const size_t rec = (size_t)w * 2 + k_rec;
+        const size_t rec = (size_t)(rec_base + w) * 2 + k_rec;
         if (g == 0) {
             if (2 * t < G) {
                 X.part_ml[(rec * G + 2 * t) * 2 + 0] = m_run[0];
@@ -376,6 +426,7 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2) fkv_a
             }
         }
     }
+    if (lane == 0) trace_stamp(X.trace, tcls, w, 4);
 }
 
 // Merge a unit's partial records and commit the speculative advance (row a8).
@@ -389,13 +440,36 @@ constexpr int kMaxRecs = 256;  // records per unit (host guarantees P_max * T / 
 
 __global__ void __launch_bounds__(1024) fkv_attn_combine_kernel(FkvDims D, FkvLayer L, FkvScratch X,
                                                                 const uint16_t* __restrict__ q,
-                                                                float* __restrict__ out) {
+                                                                float* __restrict__ out, int split) {
+    if (threadIdx.x == 0) trace_stamp(X.trace, 7, blockIdx.x, 0);
     const int u = blockIdx.x, b = u / D.n_kv, m = u % D.n_kv, G = D.G;
-    const unsigned T = (unsigned)D.attn_warps, V = (unsigned)(D.U * D.P_max);
-    const unsigned x0 = (unsigned)u * D.P_max, x1 = x0 + D.P_max;
+    // rank of u among the units of its attention phase (split: by correction flag)
+    __shared__ int s_rank, s_n;
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        const int my_phase = split ? (L.flags[u] ? 2 : 1) : 0;
+        int cnt = 0, rank = 0;
+        for (int base = 0; base < D.U; base += 32) {
+            const int v = base + lane;
+            const bool f = v < D.U && (my_phase == 0 || ((L.flags[v] != 0) == (my_phase == 2)));
+            const unsigned bal = __ballot_sync(0xffffffffu, f);
+            if (base <= u && u < base + 32) rank = cnt + __popc(bal & ((1u << (u - base)) - 1u));
+            cnt += __popc(bal);
+        }
+        if (lane == 0) {
+            s_rank = rank;
+            s_n = cnt;
+        }
+    }
+    __syncthreads();
+    const int rec_base = (split && L.flags[u]) ? D.attn_warps : 0;
+    const unsigned V = (unsigned)(s_n * D.P_max);
+    const unsigned T = min((unsigned)D.attn_warps, V);  // the phase's warp count (see the split kernel)
+    const unsigned x0 = (unsigned)s_rank * D.P_max, x1 = x0 + D.P_max;
     const int w_first = (int)(((x0 + 1) * T + V - 1) / V) - 1;
     const int w_last = (int)((x1 * T + V - 1) / V) - 1;
     const int nr = w_last - w_first + 1;
+    pdl_wait();  // the attention phases' partial records are complete
     // commit loads first (independent of the merge)
     int rp = 0, rs = 0;
     if (threadIdx.x < D.K) {
@@ -407,7 +481,7 @@ __global__ void __launch_bounds__(1024) fkv_attn_combine_kernel(FkvDims D, FkvLa
     for (int r = threadIdx.x; r < nr && r < kMaxRecs; r += blockDim.x) {
         const unsigned w = (unsigned)(w_first + r);
         const unsigned a = w * V / T;
-        s_rec[r] = (int)(w * 2 + ((a / D.P_max == (unsigned)u) ? 0 : 1));
+        s_rec[r] = (int)((rec_base + w) * 2 + ((a / D.P_max == (unsigned)s_rank) ? 0 : 1));
     }
     __syncthreads();
     const int h = threadIdx.x / kHeadDim, c = threadIdx.x % kHeadDim;
@@ -460,6 +534,7 @@ __global__ void __launch_bounds__(1024) fkv_attn_combine_kernel(FkvDims D, FkvLa
         L.res_front[u] = L.pend_front[u];
         L.res_cnt[u] = L.pend_cnt[u];
         L.res_valid[u] = 1;
+        trace_stamp(X.trace, 7, blockIdx.x, 1);
     }
 }
 
@@ -509,22 +584,26 @@ cudaError_t attn_resident_warps(int* warps) {
 }
 
 cudaError_t launch_attn_split(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                              int phase, const CUtensorMap& tmap, const uint16_t* arena, cudaStream_t s) {
+                              int phase, const CUtensorMap& tmap, const uint16_t* arena, bool pdl, cudaStream_t s) {
     const int ctas = (D.attn_warps + kAttnWarpsPerCta - 1) / kAttnWarpsPerCta;
     const int nst = attn_stages();
     const int smem = kAttnWarpsPerCta * nst * kSlabBytes;
     switch (nst) {
-        case 2: fkv_attn_split_kernel<2><<<ctas, kAttnWarpsPerCta * 32, smem, s>>>(D, L, X, q, phase, tmap, arena); break;
-        case 4: fkv_attn_split_kernel<4><<<ctas, kAttnWarpsPerCta * 32, smem, s>>>(D, L, X, q, phase, tmap, arena); break;
-        default: fkv_attn_split_kernel<3><<<ctas, kAttnWarpsPerCta * 32, smem, s>>>(D, L, X, q, phase, tmap, arena); break;
+        case 2:
+            return launch_ex(fkv_attn_split_kernel<2>, dim3(ctas), dim3(kAttnWarpsPerCta * 32), smem, s, pdl, D, L, X, q,
+                             phase, tmap, arena);
+        case 4:
+            return launch_ex(fkv_attn_split_kernel<4>, dim3(ctas), dim3(kAttnWarpsPerCta * 32), smem, s, pdl, D, L, X, q,
+                             phase, tmap, arena);
+        default:
+            return launch_ex(fkv_attn_split_kernel<3>, dim3(ctas), dim3(kAttnWarpsPerCta * 32), smem, s, pdl, D, L, X, q,
+                             phase, tmap, arena);
     }
-    return cudaGetLastError();
 }
 
 cudaError_t launch_attn_combine(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                                float* out, cudaStream_t s) {
-    fkv_attn_combine_kernel<<<D.U, D.G * kHeadDim, 0, s>>>(D, L, X, q, out);
-    return cudaGetLastError();
+                                float* out, int split, bool pdl, cudaStream_t s) {
+    return launch_ex(fkv_attn_combine_kernel, dim3(D.U), dim3(D.G * kHeadDim), 0, s, pdl, D, L, X, q, out, split);
 }
 
 }  // namespace fkv

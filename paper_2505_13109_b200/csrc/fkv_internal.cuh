@@ -63,9 +63,10 @@ struct FkvScratch {
     float* scores;        // [U][G][n_page_max]
     int32_t* page_rows;   // [U][P_max] attention page list of this step: arena row of the page's K block
     uint8_t* page_valid;  // [U][P_max] valid tokens of each listed page
+    unsigned long long* trace;  // diagnostics (FREEKV_TRACE=1): %globaltimer stamps, else NULL
     int32_t* page_cnt;    // [U]
-    float* part_o;        // [2 * attn_warps][G][d]   per-warp, per-unit-segment partial outputs
-    float* part_ml;       // [2 * attn_warps][G][2]   (running max, running sum)
+    float* part_o;        // [2 phases][attn_warps][2 segments][G][d] per-warp, per-unit-segment partial outputs
+    float* part_ml;       // [2 phases][attn_warps][2 segments][G][2] (running max, running sum)
 };
 
 __host__ __device__ inline size_t page_elems(const FkvDims& D) { return (size_t)2 * D.p * D.d; }
@@ -80,6 +81,23 @@ __device__ __forceinline__ size_t summ_chunk_offset(const FkvDims& D, int u, int
 __device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
 __device__ __forceinline__ float bf16f(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
+
+// Programmatic dependent launch (PDL): a kernel launched with programmatic stream
+// serialization may start while its predecessor drains; it runs its prologue, then
+// waits for the predecessor's completion (and memory) at pdl_wait().
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// trace slots: [kernel class 0..7][entity < 4096][stamp < 8]
+constexpr int kTraceEnt = 4096, kTraceStamps = 8;
+__device__ __forceinline__ void trace_stamp(unsigned long long* tr, int cls, int ent, int i) {
+    if (tr && ent < kTraceEnt) tr[((size_t)cls * kTraceEnt + ent) * kTraceStamps + i] = gtimer();
+}
 
 // ---- TMA bulk copy (cp.async.bulk, SASS UBLKCP) + mbarrier helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -114,6 +132,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                             Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = pdl ? attr : nullptr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 }  // namespace fkv
 
 // kernel launchers (defined in the .cu files), return cudaGetLastError()
@@ -124,13 +158,17 @@ cudaError_t launch_summarize(const FkvDims& D, const FkvLayer& L, int page_begin
                              cudaStream_t s);
 cudaError_t launch_score(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                          int max_n_off, int pending, cudaStream_t s);
+cudaError_t launch_select_fused(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
+                                const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
+                                uint8_t* corrected_out, int cluster, int lptm, cudaStream_t s);
 cudaError_t launch_finalize(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                             const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
-                            uint8_t* corrected_out, int lpt, cudaStream_t s);
-cudaError_t launch_recall(const FkvDims& D, const FkvLayer& L, int sync_mode, cudaStream_t s);
+                            uint8_t* corrected_out, int lpt, bool pdl, cudaStream_t s);
+cudaError_t launch_recall(const FkvDims& D, const FkvLayer& L, int sync_mode, cudaStream_t s,
+                          unsigned long long* trace = nullptr);
 cudaError_t attn_resident_warps(int* warps);  // SMs x resident warps/SM of the split kernel
 cudaError_t launch_attn_split(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                              int phase, const CUtensorMap& tmap, const uint16_t* arena, cudaStream_t s);
+                              int phase, const CUtensorMap& tmap, const uint16_t* arena, bool pdl, cudaStream_t s);
 cudaError_t launch_attn_combine(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                                float* out, cudaStream_t s);
+                                float* out, int split, bool pdl, cudaStream_t s);
 }  // namespace fkv

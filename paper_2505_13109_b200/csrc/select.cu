@@ -94,18 +94,22 @@ constexpr int kRing = 3;
 template <int G>
 __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims D, FkvLayer L,
                                                                         float* __restrict__ scores,
-                                                                        const uint16_t* __restrict__ q, int pending) {
+                                                                        const uint16_t* __restrict__ q, int pending,
+                                                                        unsigned long long* __restrict__ trace) {
     constexpr int GP = (G + 3) / 4 * 4;
     extern __shared__ __align__(128) uint8_t s_raw[];
     __shared__ __align__(16) float qv[kHeadDim][GP];      // q_c per head
     __shared__ __align__(16) uint32_t qm[kHeadDim][GP];   // ~0 if q_c >= 0 (take max) else 0 (take min)
     __shared__ __align__(8) uint64_t bar[kScoreWarps][kRing];
+    pdl_trigger();  // the select-finalize kernel may start its prologue now
     const int u = blockIdx.x, b = u / D.n_kv, m = u % D.n_kv;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_off = max(L.n_off[u], frontier_for(D, L.ctx[u] + pending));
     if ((int)blockIdx.y * kScoreWarps * 32 >= n_off) return;  // uniform: no candidate in this CTA
     const int blk = blockIdx.y * kScoreWarps + warp;
     const bool active = blk * 32 < n_off && blk * 32 + 31 >= D.n_sink;
+    const int tent = blockIdx.x * gridDim.y + blockIdx.y;
+    if (threadIdx.x == 0) trace_stamp(trace, 0, tent, 0);
     uint8_t* ring = s_raw + warp * (kRing * kChunkBytes);
     const uint8_t* src = reinterpret_cast<const uint8_t*>(L.summ + summ_chunk_offset(D, u, blk * 32, 0, 0));
     if (lane == 0) {
@@ -128,6 +132,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims 
         qm[c][h] = x >= 0.0f ? 0xffffffffu : 0u;  // CFR-2: q_c >= 0 (incl. -0) uses the max
     }
     __syncthreads();
+    if (threadIdx.x == 0) trace_stamp(trace, 0, tent, 1);
     if (!active) return;
     float acc[G];
 #pragma unroll
@@ -136,6 +141,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims 
     for (int k = 0; k < 4; ++k) {
         const int slot = k % kRing;
         mbar_wait(&bar[warp][slot], (uint32_t)(k / kRing) & 1u);
+        if (k == 0 && threadIdx.x == 0) trace_stamp(trace, 0, tent, 2);
         score_channels<G>(reinterpret_cast<const uint4*>(ring + slot * kChunkBytes) - (k * 4) * 2 * 32, k * 4,
                           lane, qv, qm, acc);
         if (k + kRing < 4) {
@@ -153,6 +159,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims 
         for (int h = 0; h < G; ++h)
             scores[((size_t)u * G + h) * D.n_page_max + j] = __fmul_rn(acc[h], D.score_r);  // CFR-3
     }
+    if (threadIdx.x == 0) trace_stamp(trace, 0, tent, 3);
 }
 
 // ------------------------------------------------------ a9 + a1 + a3 + a4
@@ -167,11 +174,12 @@ constexpr int kMaxK = 256;
 constexpr int kThreads = 1024;
 constexpr int kWarps = kThreads / 32;
 
-template <int LPT>
+template <int LPT, int GM>
 __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D, FkvLayer L,
                                                                        int32_t* __restrict__ page_rows,
                                                                        uint8_t* __restrict__ page_valid,
                                                                        int32_t* __restrict__ page_cnt,
+                                                                       unsigned long long* __restrict__ trace,
                                                                        const float* __restrict__ scores,
                                                                        const uint16_t* __restrict__ q,
                                                                        const uint16_t* __restrict__ k_new,
@@ -199,7 +207,11 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
     uint4* s_page = reinterpret_cast<uint4*>(s_dyn);                                   // append staging
     float* s_sc = reinterpret_cast<float*>(s_dyn + page_elems(D) * sizeof(uint16_t));  // [G][n_page_max]
 
-    // ---- a9 (fused, decode path): append this step's token before anything reads ctx
+    if (tid == 0) trace_stamp(trace, 1, u, 0);
+    pdl_trigger();  // attention may start its prologue
+    // ---- a9 (fused, decode path): append this step's token.  Runs while the score kernel
+    // drains (PDL): it only touches the ring / the page completing now (not a candidate of
+    // this step) / the host pool; ctx and n_off are published after pdl_wait().
     int n_off = L.n_off[u];
     int Lc_now = L.ctx[u];
     if (k_new) {
@@ -207,13 +219,10 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
         Lc_now = ctx0 + 1;
         append_unit(D, L, u, ctx0, k_new, v_new, 1, s_page);
         n_off = max(n_off, frontier_for(D, ctx0 + 1));
-        if (tid == 0) {
-            L.ctx[u] = ctx0 + 1;
-            L.n_off[u] = n_off;
-        }
     }
     const int n_cand = n_off - n_sink;
     const bool rank_all = n_cand <= K;  // A-11: all candidates selected, no ranking
+    if (tid == 0) trace_stamp(trace, 1, u, 1);
 
     // ---- stage everything the CTA reads (one round trip): q_i, q_{i-1}, resident set, scores
     {
@@ -227,6 +236,8 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
     // debug mode 3 (FREEKV_DEBUG_FULL_REFRESH): forget the resident set every step, so every
     // unit re-fetches all K pages synchronously -- the GEN-X recall-bandwidth stress case
     const int res_valid = D.full_refresh ? 0 : L.res_valid[u];
+    const int res_front = L.res_front[u];  // hoisted: used by the page list at the end
+    const int res_cnt = L.res_cnt[u];
     for (int i = tid; i < K; i += kThreads) {
         s_res[i] = res_valid ? L.res_pages[(size_t)u * K + i] : -1;
         s_res_slot[i] = res_valid ? L.res_slot[(size_t)u * K + i] : -1;
@@ -234,15 +245,20 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
     for (int i = tid; i < 2 * K; i += kThreads) s_used[i] = 0;
     for (int i = tid; i < 256; i += kThreads) s_hist[0][i] = 0;
     const size_t srow = (size_t)D.n_page_max;
+    pdl_wait();  // the score kernel has completed: its scores are visible, ctx may be published
+    if (k_new && tid == 0) {
+        L.ctx[u] = Lc_now;
+        L.n_off[u] = n_off;
+    }
     if (!rank_all) {
         const float* sg = scores + (size_t)u * G * srow;
         for (int j = n_sink + tid; j < n_off; j += kThreads) {
-            float v[kMaxG];  // all heads' loads in flight together
+            float v[GM];  // all heads' loads in flight together
 #pragma unroll
-            for (int g = 0; g < kMaxG; ++g)
+            for (int g = 0; g < GM; ++g)
                 if (g < G) v[g] = sg[g * srow + j];
 #pragma unroll
-            for (int g = 0; g < kMaxG; ++g)
+            for (int g = 0; g < GM; ++g)
                 if (g < G) s_sc[g * srow + j] = v[g];
         }
     }
@@ -277,12 +293,13 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
         cnt = n_cand > 0 ? n_cand : 0;
         __syncthreads();
     } else {
+        if (tid == 0) trace_stamp(trace, 1, u, 2);
         const float* su = s_sc;
         const int jb = tid * LPT;
         // ---- CFR-4: max per head (exact, order-free); the G heads' shuffles interleave
-        float M[kMaxG];
+        float M[GM];
 #pragma unroll
-        for (int g = 0; g < kMaxG; ++g) {
+        for (int g = 0; g < GM; ++g) {
             M[g] = -INFINITY;
             if (g < G) {
 #pragma unroll
@@ -295,23 +312,23 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-            for (int g = 0; g < kMaxG; ++g) M[g] = fmaxf(M[g], __shfl_xor_sync(0xffffffffu, M[g], o));
+            for (int g = 0; g < GM; ++g) M[g] = fmaxf(M[g], __shfl_xor_sync(0xffffffffu, M[g], o));
         if (lane == 0)
 #pragma unroll
-            for (int g = 0; g < kMaxG; ++g) s_redm[warp][g] = M[g];
+            for (int g = 0; g < GM; ++g) s_redm[warp][g] = M[g];
         __syncthreads();
 #pragma unroll
-        for (int g = 0; g < kMaxG; ++g) M[g] = lane < kWarps ? s_redm[lane][g] : -INFINITY;
+        for (int g = 0; g < GM; ++g) M[g] = lane < kWarps ? s_redm[lane][g] : -INFINITY;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-            for (int g = 0; g < kMaxG; ++g) M[g] = fmaxf(M[g], __shfl_xor_sync(0xffffffffu, M[g], o));
+            for (int g = 0; g < GM; ++g) M[g] = fmaxf(M[g], __shfl_xor_sync(0xffffffffu, M[g], o));
         // ---- CFR-5/6: e = cexp2(s - m); Z = pairwise tree in page-id order: thread-local tree over
         // its LPT contiguous leaves, xor butterfly over the 32 lanes, butterfly over the warp
         // partials (lanes >= kWarps hold +0 leaves, which leave a pairwise tree's value unchanged)
-        float Z[kMaxG];
+        float Z[GM];
 #pragma unroll
-        for (int g = 0; g < kMaxG; ++g) {
+        for (int g = 0; g < GM; ++g) {
             Z[g] = 0.0f;
             if (g < G) {
                 float e[LPT];
@@ -330,17 +347,18 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1)
 #pragma unroll
-            for (int g = 0; g < kMaxG; ++g) Z[g] = __fadd_rn(Z[g], __shfl_xor_sync(0xffffffffu, Z[g], o));
+            for (int g = 0; g < GM; ++g) Z[g] = __fadd_rn(Z[g], __shfl_xor_sync(0xffffffffu, Z[g], o));
         if (lane == 0)
 #pragma unroll
-            for (int g = 0; g < kMaxG; ++g) s_redz[warp][g] = Z[g];
+            for (int g = 0; g < GM; ++g) s_redz[warp][g] = Z[g];
         __syncthreads();
 #pragma unroll
-        for (int g = 0; g < kMaxG; ++g) Z[g] = lane < kWarps ? s_redz[lane][g] : 0.0f;
+        for (int g = 0; g < GM; ++g) Z[g] = lane < kWarps ? s_redz[lane][g] : 0.0f;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1)
 #pragma unroll
-            for (int g = 0; g < kMaxG; ++g) Z[g] = __fadd_rn(Z[g], __shfl_xor_sync(0xffffffffu, Z[g], o));
+            for (int g = 0; g < GM; ++g) Z[g] = __fadd_rn(Z[g], __shfl_xor_sync(0xffffffffu, Z[g], o));
+        if (tid == 0) trace_stamp(trace, 1, u, 3);
         // ---- CFR-7/8: p = e / Z; pooled = sequential sum over g; CFR-9 keys
         uint32_t key[LPT];
         bool cand[LPT];
@@ -351,7 +369,7 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
             float pi = 0.0f;
             if (cand[l]) {
 #pragma unroll
-                for (int g = 0; g < kMaxG; ++g) {
+                for (int g = 0; g < GM; ++g) {
                     if (g < G) {
                         const float pg = __fdiv_rn(cexp2_cfr(__fsub_rn(su[g * srow + j], M[g])), Z[g]);
                         pi = g == 0 ? pg : __fadd_rn(pi, pg);
@@ -405,6 +423,7 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
             prefix |= (uint32_t)s_dig[pass] << shift;
             mask |= 0xFFu << shift;
         }
+        if (tid == 0) trace_stamp(trace, 1, u, 4);
         const uint32_t T = prefix;  // K-th largest key; take k_rem of the keys equal to T (lowest ids)
         // ---- one packed block scan of (#gt, #eq) in page-id order
         unsigned n_gt = 0, n_eq = 0;
@@ -444,6 +463,7 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
     }
 
     // ---- flag (CFR-10 pooling, A-12, A-13)
+    if (tid == 0) trace_stamp(trace, 1, u, 5);
     if (tid == 0) {
         float acc = s_cos[0];
         for (int g = 1; g < G; ++g) acc = __fadd_rn(acc, s_cos[g]);
@@ -459,17 +479,23 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
         L.pend_front[u] = n_off;
         if (corrected_out) corrected_out[u] = (uint8_t)flag;
     }
-    // ---- a4: delta vs resident (A-18) and slot assignment (slot double-buffering)
+    // ---- a4: delta vs resident (A-18) and slot assignment (slot double-buffering).  Membership
+    // of S_i's pages in R via a page -> index table in the (now dead) score staging area;
+    // entries are validated against s_res, so stale table contents are harmless.
+    uint16_t* s_idx = reinterpret_cast<uint16_t*>(s_sc);
+    for (int i = tid; i < K; i += kThreads)
+        if (s_res[i] >= 0) s_idx[s_res[i]] = (uint16_t)i;
+    __syncthreads();
     if (tid < K) {
         int f = 0;
         const int Sa = tid < cnt ? s_sel[tid] : -1;
         if (Sa >= 0) {
             f = 1;
-            for (int i = 0; i < K; ++i)
-                if (s_res[i] == Sa) {
-                    f = 0;
-                    s_pslot[tid] = s_res_slot[i];
-                }
+            const int i = s_idx[Sa];
+            if (i < K && s_res[i] == Sa) {
+                f = 0;
+                s_pslot[tid] = s_res_slot[i];
+            }
         }
         s_isfetch[tid] = f;
         if (s_res[tid] >= 0) s_used[s_res_slot[tid]] = 1;
@@ -518,13 +544,8 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
         const int p = D.p;
         const int sink_tok = min(D.S_tok, Lc);
         const int n_sp = (sink_tok + p - 1) / p;
-        int n_sel = 0;
-        if (flag) {
-            n_sel = cnt;
-        } else {
-            for (int i = 0; i < K; ++i) n_sel += s_res[i] >= 0;
-        }
-        const int f = flag ? n_off : L.res_front[u];
+        const int n_sel = flag ? cnt : res_cnt;
+        const int f = flag ? n_off : res_front;
         const int n_last = (Lc - 1) / p;
         const int n_loc = (Lc > f * p) ? (n_last - f + 1) : 0;
         const size_t pe = page_elems(D);
@@ -551,11 +572,12 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
         }
         if (tid == 0) page_cnt[u] = total;
     }
+    if (tid == 0) trace_stamp(trace, 1, u, 6);
 }
 
 template <int G>
 static void launch_score_g(const FkvDims& D, const FkvLayer& L, float* scores, const uint16_t* q, int max_n_off,
-                           int pending, cudaStream_t s) {
+                           int pending, unsigned long long* trace, cudaStream_t s) {
     const int per_cta = kScoreWarps * 32;
     const int gy = (max_n_off + per_cta - 1) / per_cta;
     if (gy <= 0) return;
@@ -567,42 +589,53 @@ static void launch_score_g(const FkvDims& D, const FkvLayer& L, float* scores, c
                              cudaSharedmemCarveoutMaxShared);
         configured = true;
     }
-    fkv_score_kernel<G><<<dim3(D.U, gy), per_cta, smem, s>>>(D, L, scores, q, pending);
+    fkv_score_kernel<G><<<dim3(D.U, gy), per_cta, smem, s>>>(D, L, scores, q, pending, trace);
 }
 
 cudaError_t launch_score(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                          int max_n_off, int pending, cudaStream_t s) {
     switch (D.G) {
-        case 1: launch_score_g<1>(D, L, X.scores, q, max_n_off, pending, s); break;
-        case 2: launch_score_g<2>(D, L, X.scores, q, max_n_off, pending, s); break;
-        case 3: launch_score_g<3>(D, L, X.scores, q, max_n_off, pending, s); break;
-        case 4: launch_score_g<4>(D, L, X.scores, q, max_n_off, pending, s); break;
-        case 5: launch_score_g<5>(D, L, X.scores, q, max_n_off, pending, s); break;
-        case 6: launch_score_g<6>(D, L, X.scores, q, max_n_off, pending, s); break;
-        case 7: launch_score_g<7>(D, L, X.scores, q, max_n_off, pending, s); break;
-        case 8: launch_score_g<8>(D, L, X.scores, q, max_n_off, pending, s); break;
+        case 1: launch_score_g<1>(D, L, X.scores, q, max_n_off, pending, X.trace, s); break;
+        case 2: launch_score_g<2>(D, L, X.scores, q, max_n_off, pending, X.trace, s); break;
+        case 3: launch_score_g<3>(D, L, X.scores, q, max_n_off, pending, X.trace, s); break;
+        case 4: launch_score_g<4>(D, L, X.scores, q, max_n_off, pending, X.trace, s); break;
+        case 5: launch_score_g<5>(D, L, X.scores, q, max_n_off, pending, X.trace, s); break;
+        case 6: launch_score_g<6>(D, L, X.scores, q, max_n_off, pending, X.trace, s); break;
+        case 7: launch_score_g<7>(D, L, X.scores, q, max_n_off, pending, X.trace, s); break;
+        case 8: launch_score_g<8>(D, L, X.scores, q, max_n_off, pending, X.trace, s); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
 }
 
-template <int LPT>
-static cudaError_t launch_fin(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                              const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
-                              uint8_t* corrected_out, size_t smem, cudaStream_t s) {
+// GM = group-size bucket (1, 2, 4, 8) >= G: the per-head loops and shuffles run GM wide
+template <int LPT, int GM>
+static cudaError_t launch_fin_g(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
+                                const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
+                                uint8_t* corrected_out, size_t smem, bool pdl, cudaStream_t s) {
     static size_t configured = 0;
     if (smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(fkv_select_finalize_kernel<LPT>,
+        cudaError_t e = cudaFuncSetAttribute(fkv_select_finalize_kernel<LPT, GM>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(fkv_select_finalize_kernel<LPT>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                     cudaSharedmemCarveoutMaxShared);
+            e = cudaFuncSetAttribute(fkv_select_finalize_kernel<LPT, GM>,
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return e;
         configured = smem;
     }
-    fkv_select_finalize_kernel<LPT><<<D.U, kThreads, smem, s>>>(D, L, X.page_rows, X.page_valid, X.page_cnt, X.scores, q, k_new,
-                                                                v_new, pages_out, corrected_out);
-    return cudaGetLastError();
+    return launch_ex(fkv_select_finalize_kernel<LPT, GM>, dim3(D.U), dim3(kThreads), smem, s, pdl, D, L, X.page_rows,
+                     X.page_valid, X.page_cnt, X.trace, (const float*)X.scores, q, k_new, v_new, pages_out,
+                     corrected_out);
+}
+
+template <int LPT>
+static cudaError_t launch_fin(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
+                              const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
+                              uint8_t* corrected_out, size_t smem, bool pdl, cudaStream_t s) {
+    if (D.G <= 1) return launch_fin_g<LPT, 1>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, s);
+    if (D.G <= 2) return launch_fin_g<LPT, 2>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, s);
+    if (D.G <= 4) return launch_fin_g<LPT, 4>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, s);
+    return launch_fin_g<LPT, 8>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, s);
 }
 
 // lpt = leaves per thread of the kThreads-thread tree; kThreads * lpt >= next_pow2(n_off) for every n_off the
@@ -610,15 +643,13 @@ static cudaError_t launch_fin(const FkvDims& D, const FkvLayer& L, const FkvScra
 // this step's single-token append (row a9) into the kernel.
 cudaError_t launch_finalize(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                             const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
-                            uint8_t* corrected_out, int lpt, cudaStream_t s) {
+                            uint8_t* corrected_out, int lpt, bool pdl, cudaStream_t s) {
     const size_t smem = page_elems(D) * sizeof(uint16_t) + (size_t)D.G * D.n_page_max * sizeof(float);
     switch (lpt) {
-        case 1: return launch_fin<1>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, s);
-        case 2: return launch_fin<2>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, s);
-        case 4: return launch_fin<4>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, s);
-        case 8: return launch_fin<8>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, s);
-        case 16: return launch_fin<16>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, s);
-        case 32: return launch_fin<32>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, s);
+        case 1: return launch_fin<1>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, s);
+        case 2: return launch_fin<2>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, s);
+        case 4: return launch_fin<4>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, s);
+        case 8: return launch_fin<8>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, s);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -24,7 +24,7 @@ EXPORTED = [
     "freekv_get_selection", "freekv_get_resident", "freekv_get_fetch", "freekv_get_summaries",
     "freekv_get_context", "freekv_get_dims", "freekv_synchronize", "freekv_destroy",
     "freekv_last_error", "freekv_abi_version", "freekv_profile_begin", "freekv_profile_end",
-    "freekv_step_graph_capture", "freekv_step_graph_launch", "freekv_step_graph_profile",
+    "freekv_step_graph_capture", "freekv_step_graph_launch", "freekv_step_graph_profile", "freekv_debug_trace",
 ]
 KERNEL_CLASSES = ["append", "score", "select_finalize", "recall_sync", "recall_bg", "attn_split", "attn_combine"]
 
@@ -125,6 +125,7 @@ def load_library():
             "freekv_profile_end": [vp, vp, vp],
             "freekv_step_graph_capture": [vp, vp, vp, vp, vp, i32],
             "freekv_step_graph_profile": [vp, vp, vp],
+            "freekv_debug_trace": [vp, vp, sz],
             "freekv_step_graph_launch": [vp],
         }
         for name, args in sigs.items():
@@ -240,6 +241,12 @@ class FreeKV:
         n = np.zeros(len(KERNEL_CLASSES), np.int32)
         _check(self.L.freekv_profile_end(self.h, _np_ptr(ms), _np_ptr(n)))
         return {c: (float(ms[i]), int(n[i])) for i, c in enumerate(KERNEL_CLASSES)}
+
+    def debug_trace(self):
+        """[8][4096][8] uint64 %globaltimer stamps (ns) of the kernels since the last call."""
+        out = np.zeros((8, 4096, 8), np.uint64)
+        _check(self.L.freekv_debug_trace(self.h, _np_ptr(out), out.size))
+        return out
 
     # -- inspection (blocking) -------------------------------------------------
     def get_selection(self, layer):

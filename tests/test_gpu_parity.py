@@ -196,3 +196,16 @@ def test_step_graph_matches_eager():
             assert torch.equal(oa, ob[l]), (i, l)
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("select_impl", ["fused"])
+def test_parity_fused_cluster_select(select_impl, monkeypatch):
+    """The one-launch cluster select path (FREEKV_SELECT=fused) gives the same bits."""
+    monkeypatch.setenv("FREEKV_SELECT", select_impl)
+    run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=4)
+    run_parity(G=7, n_kv=1, batch=1, page=16, sink=64, window=64, budget=640, L0=9000, steps=3, n_layers=1)
+
+
+def test_parity_without_pdl(monkeypatch):
+    monkeypatch.setenv("FREEKV_PDL", "0")
+    run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=4)

@@ -1,0 +1,5 @@
+python -c "import __graft_entry__ as g; g.build()"
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest23.log 2>&1; echo "rc=$?" >> gpurun_out/pytest23.log
+timeout 600 python tools/trace_step.py > gpurun_out/trace23.json 2> gpurun_out/trace23.err
+timeout 300 python tools/kbench.py --layers 4 --steps 20 --warmup 5 --graph --no-profile > gpurun_out/kb23_pdl.json 2>&1
+FREEKV_PDL=0 timeout 300 python tools/kbench.py --layers 4 --steps 20 --warmup 5 --graph --no-profile > gpurun_out/kb23_nopdl.json 2>&1
