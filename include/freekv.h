@@ -155,7 +155,7 @@ freekv_status freekv_step_graph_launch(freekv_handle* h);
  * nodes; after a replay has completed, this returns per kernel class the summed
  * device milliseconds and launch counts of that replay (classes as in
  * freekv_profile_end).  Blocking. */
-freekv_status freekv_step_graph_profile(freekv_handle* h, float* ms /*[7]*/, int32_t* launches /*[7]*/);
+freekv_status freekv_step_graph_profile(freekv_handle* h, float* ms /*[11]*/, int32_t* launches /*[11]*/);
 
 /* Inspection (blocking; host outputs).  All arrays u-major. */
 freekv_status freekv_get_selection(freekv_handle* h, int32_t layer, int32_t* pages /*[U][K]*/,
@@ -176,11 +176,14 @@ freekv_status freekv_get_dims(freekv_handle* h, int32_t* K, int32_t* n_page_max,
  * it is launched on (at most max_launches launches are recorded).
  * profile_end synchronises and returns, per kernel class, the summed device
  * milliseconds and the launch count.  Classes: 0 append, 1 score, 2 select
- * finalize, 3 synchronous recall, 4 background recall, 5 attention split,
- * 6 attention combine + commit. */
-#define FREEKV_NUM_KERNEL_CLASSES 7
+ * finalize, 3 synchronous recall, 4 background recall, 5 attention split (all
+ * units, or phase 1: units with resident pages), 6 attention combine + commit,
+ * 7 attention split phase 2 (corrected units), 8 step prologue (pipelined step:
+ * append + correction check + page lists), 9 background score, 10 background
+ * select (pipelined step). */
+#define FREEKV_NUM_KERNEL_CLASSES 11
 freekv_status freekv_profile_begin(freekv_handle* h, int32_t max_launches);
-freekv_status freekv_profile_end(freekv_handle* h, float* ms /*[7]*/, int32_t* launches /*[7]*/);
+freekv_status freekv_profile_end(freekv_handle* h, float* ms /*[11]*/, int32_t* launches /*[11]*/);
 
 /* Diagnostics: with FREEKV_TRACE=1 in the environment at freekv_init, kernels write
  * %globaltimer stamps [class 8][entity 4096][stamp 8] (ns); this copies n <= 262144

@@ -43,6 +43,7 @@ static freekv_status fail(freekv_status st, const std::string& msg) {
 
 struct freekv_handle {
     alignas(64) CUtensorMap tmap_kv;  // the device arena as a 2D tensor of 256-byte rows (TMA)
+    alignas(64) CUtensorMap tmap_host;  // the device-mapped host pool, same row geometry (direct mode)
     const uint16_t* arena = nullptr;
     freekv_config cfg;
     FkvDims D;
@@ -50,7 +51,9 @@ struct freekv_handle {
     FkvScratch X;
     cudaStream_t cs = nullptr, rs = nullptr;
     cudaStream_t ss = nullptr;  // library-owned high-priority stream for the synchronous recall
-    std::vector<cudaEvent_t> ev_select, ev_recall, ev_sync, ev_sync_x;
+    std::vector<cudaEvent_t> ev_select, ev_recall, ev_sync, ev_sync_x, ev_pre, ev_fl;
+    FkvScratch Xb;               // scratch of the background select (own score buffer)
+    bool pipelined = true;       // pipelined step (FREEKV_PIPELINE=0 disables; needs direct mode)
     std::vector<int> ctx_host;
     std::vector<int> recall_pending;
     int lpt = 1;  // leaves per thread of the finalize tree (fixed per handle, CFR-6)
@@ -74,7 +77,7 @@ namespace {
 
 constexpr size_t kAlign = 256;
 constexpr int kMaxAttnWarps = 148 * 16;
-constexpr int kFinalizeThreads = 1024;  // must match select.cu kThreads  // partial-record capacity; the grid uses min(resident warps, this)
+constexpr int kFinalizeThreads = 512;  // must match select.cu kThreads  // partial-record capacity; the grid uses min(resident warps, this)
 size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
 
 struct Sizes {
@@ -84,7 +87,7 @@ struct Sizes {
         o_pend_cnt,
         o_pend_pages, o_pend_slot, o_pend_front, o_flags, o_cbar, o_fetch_page, o_fetch_slot, o_n_fetch, o_ctx,
         o_n_off;
-    size_t o_scores, o_part_o, o_part_ml, o_page_rows, o_page_cnt, o_page_valid;
+    size_t o_scores, o_scores_bg, o_part_o, o_part_ml, o_page_rows, o_page_cnt, o_page_valid, o_page_dst;
 };
 
 freekv_status validate(const freekv_config* c, FkvDims* D) {
@@ -174,11 +177,13 @@ Sizes compute_sizes(const freekv_config* c, const FkvDims& D) {
     s.layer_bytes = o;
     o = 0;
     s.o_scores = take(U * D.G * D.n_page_max * 4);
+    s.o_scores_bg = take(U * D.G * D.n_page_max * 4);
     s.o_part_o = take((size_t)4 * kMaxAttnWarps * D.G * D.d * 4);
     s.o_part_ml = take((size_t)4 * kMaxAttnWarps * D.G * 2 * 4);
     s.o_page_rows = take(U * D.P_max * 4);
     s.o_page_cnt = take(U * 4);
     s.o_page_valid = take(U * D.P_max);
+    s.o_page_dst = take(U * D.P_max * 4);
     s.scratch_bytes = o;
     s.dev_bytes = s.layer_bytes * c->n_layers + s.scratch_bytes;
     s.host_layer_bytes = (size_t)D.nb * D.n_page_host * D.n_kv * pe_b;
@@ -196,7 +201,8 @@ cudaStream_t pick(freekv_handle* h, void* s) { return s ? (cudaStream_t)s : h->c
 
 int max_n_off(const FkvDims& D, int ctx) { return std::max(D.n_sink, ctx / D.p - D.n_win); }
 
-enum { K_APPEND = 0, K_SCORE, K_FINALIZE, K_RECALL_SYNC, K_RECALL_BG, K_ATTN_SPLIT, K_ATTN_COMBINE };
+enum { K_APPEND = 0, K_SCORE, K_FINALIZE, K_RECALL_SYNC, K_RECALL_BG, K_ATTN_SPLIT, K_ATTN_COMBINE, K_ATTN_P2,
+       K_PREP, K_SCORE_BG, K_FINALIZE_BG };
 
 template <class F>
 cudaError_t timed(freekv_handle* h, int cls, cudaStream_t s, F&& launch) {
@@ -247,11 +253,11 @@ freekv_status do_select(freekv_handle* h, int layer, const void* q, int32_t* pag
             h->capturing ? max_n_off(h->D, h->D.max_ctx) : max_n_off(h->D, h->ctx_host[layer] + pending);
         if (h->capturing || mno - h->D.n_sink > h->D.K)
             FKV_CUDA(timed(h, K_SCORE, s, [&] {
-                return launch_score(h->D, h->layers[layer], h->X, (const uint16_t*)q, mno, pending, s);
+                return launch_score(h->D, h->layers[layer], h->X, (const uint16_t*)q, mno, pending, 0, s);
             }));
         FKV_CUDA(timed(h, K_FINALIZE, s, [&] {
             return launch_finalize(h->D, h->layers[layer], h->X, (const uint16_t*)q, (const uint16_t*)k_new,
-                                   (const uint16_t*)v_new, pages_out, corr_out, h->lpt, h->pdl, s);
+                                   (const uint16_t*)v_new, pages_out, corr_out, h->lpt, h->pdl, 0, s);
         }));
     }
     if (k_new && !h->capturing) h->ctx_host[layer] += 1;
@@ -279,24 +285,54 @@ freekv_status do_recall(freekv_handle* h, int layer, cudaStream_t s) {
 freekv_status do_attn(freekv_handle* h, int layer, const void* q, float* out, cudaStream_t s) {
     if (!q || !out) return fail(FREEKV_EINVAL, "q/out is NULL");
     FKV_CUDA(timed(h, K_ATTN_SPLIT, s, [&] {
-        return launch_attn_split(h->D, h->layers[layer], h->X, (const uint16_t*)q, 0, h->tmap_kv, h->arena, false, s);
+        return launch_attn_split(h->D, h->layers[layer], h->X, (const uint16_t*)q, 0, h->tmap_kv, h->tmap_host,
+                                 h->arena, false, s);
     }));
     FKV_CUDA(timed(h, K_ATTN_COMBINE, s, [&] {
-        return launch_attn_combine(h->D, h->layers[layer], h->X, (const uint16_t*)q, out, 0, h->pdl, s);
+        return launch_attn_combine(h->D, h->layers[layer], h->X, (const uint16_t*)q, out, 0, 0, h->pdl, s);
     }));
     return FREEKV_OK;
 }
 
-// Composite step tail (decode_step and the step graph): the
-// corrected units' synchronous recall runs on the high-priority stream ss while the
-// attention of every other unit (whose pages are resident) runs on the compute
-// stream; the corrected units are attended once their pages have landed.  The
-// background recall (rs) follows the synchronous one so it never competes with it
-// for the host link.
+// Composite step tail (decode_step and the step graph).
+//
+// Direct mode (default): the corrected units' fetched pages are read by the attention
+// kernel straight from the host pool and written back into their slots, so the
+// synchronous recall and the second attention phase disappear from the critical
+// path; the background recall (unflagged units, for step i+1) runs on rs.
+//
+// Recall mode (FREEKV_CORR=recall): the corrected units' synchronous recall runs on
+// the high-priority stream ss while the attention of every other unit (whose pages
+// are resident) runs on the compute stream; the corrected units are attended once
+// their pages have landed.  The background recall follows the synchronous one.
 freekv_status do_step_tail(freekv_handle* h, int layer, const void* q, float* out) {
     cudaStream_t cs = h->cs;
     const FkvDims& D = h->D;
     FkvLayer& L = h->layers[layer];
+    if (D.direct) {
+        FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] {
+            return launch_attn_split(D, L, h->X, (const uint16_t*)q, 0, h->tmap_kv, h->tmap_host, h->arena, h->pdl,
+                                     cs);
+        }));
+        FKV_CUDA(timed(h, K_ATTN_COMBINE, cs, [&] {
+            return launch_attn_combine(D, L, h->X, (const uint16_t*)q, out, 0, 0, h->pdl, cs);
+        }));
+        // the background recall of this layer starts after its attention (an event node between
+        // select and attention would break their PDL edge, and the host link is then free for
+        // the attention's own host reads); it overlaps the next layers
+        if (h->capturing) {
+            FKV_CUDA(cudaEventRecordWithFlags(h->ev_select[layer], cs, cudaEventRecordExternal));
+        } else if (h->serial_recall) {
+            FKV_CUDA(timed(h, K_RECALL_BG, cs, [&] { return launch_recall(D, L, 0, cs, h->X.trace); }));
+        } else {
+            FKV_CUDA(cudaEventRecord(h->ev_select[layer], cs));
+            FKV_CUDA(cudaStreamWaitEvent(h->rs, h->ev_select[layer], 0));
+            FKV_CUDA(timed(h, K_RECALL_BG, h->rs, [&] { return launch_recall(D, L, 0, h->rs, h->X.trace); }));
+            FKV_CUDA(cudaEventRecord(h->ev_recall[layer], h->rs));
+            h->recall_pending[layer] = 1;
+        }
+        return FREEKV_OK;
+    }
     FKV_CUDA(cudaEventRecord(h->ev_select[layer], cs));
     FKV_CUDA(cudaStreamWaitEvent(h->ss, h->ev_select[layer], 0));
     FKV_CUDA(timed(h, K_RECALL_SYNC, h->ss, [&] { return launch_recall(D, L, 1, h->ss, h->X.trace); }));
@@ -314,12 +350,97 @@ freekv_status do_step_tail(freekv_handle* h, int layer, const void* q, float* ou
         FKV_CUDA(cudaEventRecord(h->ev_recall[layer], h->rs));
         h->recall_pending[layer] = 1;
     }
-    FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] { return launch_attn_split(D, L, h->X, (const uint16_t*)q, 1, h->tmap_kv, h->arena, h->pdl, cs); }));
-    FKV_CUDA(cudaStreamWaitEvent(cs, h->ev_sync[layer], 0));
-    FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] { return launch_attn_split(D, L, h->X, (const uint16_t*)q, 2, h->tmap_kv, h->arena, false, cs); }));
-    FKV_CUDA(timed(h, K_ATTN_COMBINE, cs, [&] {
-        return launch_attn_combine(D, L, h->X, (const uint16_t*)q, out, 1, h->pdl, cs);
+    FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] {
+        return launch_attn_split(D, L, h->X, (const uint16_t*)q, 1, h->tmap_kv, h->tmap_host, h->arena, h->pdl, cs);
     }));
+    FKV_CUDA(cudaStreamWaitEvent(cs, h->ev_sync[layer], 0));
+    FKV_CUDA(timed(h, K_ATTN_P2, cs, [&] {
+        return launch_attn_split(D, L, h->X, (const uint16_t*)q, 2, h->tmap_kv, h->tmap_host, h->arena, false, cs);
+    }));
+    FKV_CUDA(timed(h, K_ATTN_COMBINE, cs, [&] {
+        return launch_attn_combine(D, L, h->X, (const uint16_t*)q, out, 1, 0, h->pdl, cs);
+    }));
+    return FREEKV_OK;
+}
+
+// Background half of the pipelined step of one layer (rs): select S_i for the units
+// that attended their resident set (score + select, which = 1; the select kernel
+// commits R := S_i, q_prev := q_i for them), then recall S_i \ R into free slots
+// for step i+1.  Nothing of the current step waits on it.
+cudaError_t bg_chain(freekv_handle* h, int layer, cudaStream_t s) {
+    const FkvDims& D = h->D;
+    FkvLayer& L = h->layers[layer];
+    const uint16_t* q = L.q_prev;  // q_i, stored there by this step's prep kernel
+    const int mno = h->capturing ? max_n_off(D, D.max_ctx) : max_n_off(D, h->ctx_host[layer]);
+    cudaError_t e = cudaSuccess;
+    if (h->capturing || mno - D.n_sink > D.K)
+        e = timed(h, K_SCORE_BG, s, [&] { return launch_score(D, L, h->Xb, (const uint16_t*)q, mno, 0, 1, s); });
+    if (e == cudaSuccess)
+        e = timed(h, K_FINALIZE_BG, s, [&] {
+            return launch_finalize(D, L, h->Xb, (const uint16_t*)q, nullptr, nullptr, nullptr, nullptr, h->lpt, h->pdl,
+                                   1, s);
+        });
+    if (e == cudaSuccess) e = timed(h, K_RECALL_BG, s, [&] { return launch_recall(D, L, 0, s, h->X.trace); });
+    return e;
+}
+
+// Pipelined decode step of one layer (default), PAPER.md P:223-226,
+// speculative retrieval takes selection and recall off the critical
+// path:
+//   cs: prep (append, correction flags, page lists over R) -> attention of the
+//       speculative units -> [join] -> combine (+ commit of corrected units)
+//   ss: score + select of the corrected units (which = 2) -> their attention, which
+//       reads the pages they lack straight from the host pool and caches them
+//   rs: bg_chain, right after the prep (the next step's prep of this layer waits
+//       for it); its HBM-bound score overlaps the HBM-bound attention
+freekv_status do_step_pipelined(freekv_handle* h, int layer, const void* q, const void* k_new, const void* v_new,
+                                float* out) {
+    cudaStream_t cs = h->cs, ss = h->ss;
+    const FkvDims& D = h->D;
+    FkvLayer& L = h->layers[layer];
+    if (!q || !out) return fail(FREEKV_EINVAL, "q/out is NULL");
+    // the previous step's background half of this layer (R, q_prev, slots)
+    if (h->capturing)
+        FKV_CUDA(cudaStreamWaitEvent(cs, h->ev_recall[layer], cudaEventWaitExternal));
+    else if (h->recall_pending[layer])
+        FKV_CUDA(cudaStreamWaitEvent(cs, h->ev_recall[layer], 0));
+    FKV_CUDA(timed(h, K_PREP, cs, [&] {
+        return launch_prep(D, L, h->X, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new, nullptr,
+                           cs);
+    }));
+    if (!h->capturing) h->ctx_host[layer] += 1;
+    // background half right after the prep: its HBM-bound score runs beside this layer's
+    // HBM-bound attention instead of beside the next layer's latency-bound prologue
+    if (h->capturing) {  // the recall graph runs bg_chain after this node
+        FKV_CUDA(cudaEventRecordWithFlags(h->ev_select[layer], cs, cudaEventRecordExternal));
+    } else if (!h->serial_recall) {
+        FKV_CUDA(cudaEventRecord(h->ev_select[layer], cs));
+        FKV_CUDA(cudaStreamWaitEvent(h->rs, h->ev_select[layer], 0));
+        FKV_CUDA(bg_chain(h, layer, h->rs));
+        FKV_CUDA(cudaEventRecord(h->ev_recall[layer], h->rs));
+        h->recall_pending[layer] = 1;
+    }
+    FKV_CUDA(cudaEventRecord(h->ev_pre[layer], cs));
+    FKV_CUDA(cudaStreamWaitEvent(ss, h->ev_pre[layer], 0));
+    const int mno = h->capturing ? max_n_off(D, D.max_ctx) : max_n_off(D, h->ctx_host[layer]);
+    if (h->capturing || mno - D.n_sink > D.K)
+        FKV_CUDA(timed(h, K_SCORE, ss, [&] { return launch_score(D, L, h->X, (const uint16_t*)q, mno, 0, 2, ss); }));
+    FKV_CUDA(timed(h, K_FINALIZE, ss, [&] {
+        return launch_finalize(D, L, h->X, (const uint16_t*)q, nullptr, nullptr, nullptr, nullptr, h->lpt, h->pdl, 2,
+                               ss);
+    }));
+    FKV_CUDA(timed(h, K_ATTN_P2, ss, [&] {
+        return launch_attn_split(D, L, h->X, (const uint16_t*)q, 2, h->tmap_kv, h->tmap_host, h->arena, h->pdl, ss);
+    }));
+    FKV_CUDA(cudaEventRecord(h->ev_fl[layer], ss));
+    FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] {
+        return launch_attn_split(D, L, h->X, (const uint16_t*)q, 1, h->tmap_kv, h->tmap_host, h->arena, h->pdl, cs);
+    }));
+    FKV_CUDA(cudaStreamWaitEvent(cs, h->ev_fl[layer], 0));
+    FKV_CUDA(timed(h, K_ATTN_COMBINE, cs, [&] {
+        return launch_attn_combine(D, L, h->X, (const uint16_t*)q, out, 1, 2, false, cs);
+    }));
+    if (!h->capturing && h->serial_recall) FKV_CUDA(bg_chain(h, layer, cs));
     return FREEKV_OK;
 }
 
@@ -398,6 +519,20 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
             return fail(FREEKV_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
         }
         h->arena = (const uint16_t*)dev;
+        // the host pool with the same row geometry: corrected units' fetched pages are read by the
+        // attention kernel straight from here (direct mode); needs < 2^31 rows
+        const cuuint64_t hrows = (cuuint64_t)(s.host_bytes / (kHeadDim * 2));
+        const char* cm = getenv("FREEKV_CORR");
+        h->D.direct = (hrows < (1ull << 31) && !(cm && cm[0] == 'r')) ? 1 : 0;
+        if (h->D.direct) {
+            const cuuint64_t hdims[2] = {(cuuint64_t)kHeadDim, hrows};
+            cr = ((PFN_cuTensorMapEncodeTiled)fn)(
+                &h->tmap_host, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, host_dev, hdims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (cr != CUDA_SUCCESS) h->D.direct = 0;
+        }
+        if (!h->D.direct) h->tmap_host = h->tmap_kv;  // never dereferenced for host rows
     }
     h->layers.resize(cfg->n_layers);
     for (int l = 0; l < cfg->n_layers; ++l) {
@@ -425,6 +560,7 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         L.ctx = (int32_t*)(base + s.o_ctx);
         L.n_off = (int32_t*)(base + s.o_n_off);
         L.host = (uint16_t*)(hd + s.host_layer_bytes * l);
+        L.host_row0 = (int)(s.host_layer_bytes * l / (kHeadDim * 2));
         L.arena = (const uint16_t*)dev;
     }
     uint8_t* sb = dev + s.layer_bytes * cfg->n_layers;
@@ -434,6 +570,9 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
     h->X.page_rows = (int32_t*)(sb + s.o_page_rows);
     h->X.page_cnt = (int32_t*)(sb + s.o_page_cnt);
     h->X.page_valid = (uint8_t*)(sb + s.o_page_valid);
+    h->X.page_dst = (int32_t*)(sb + s.o_page_dst);
+    h->Xb = h->X;
+    h->Xb.scores = (float*)(sb + s.o_scores_bg);
     {
         int P2 = 1;
         while (P2 < D.n_page_host) P2 <<= 1;
@@ -444,9 +583,12 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         h->sel_lptm = std::max(1, P2 / (h->sel_cluster * 128));
         const char* fs = getenv("FREEKV_SELECT");
         h->fused_select = fs && fs[0] == 'f';
+        if (h->fused_select) h->D.direct = 0;  // the cluster select writes slot rows only
+        const char* pp = getenv("FREEKV_PIPELINE");
+        h->pipelined = h->D.direct && !(pp && pp[0] == '0');
         const char* pd = getenv("FREEKV_PDL");
         h->pdl = !(pd && pd[0] == '0');
-        if (h->lpt > 8) {
+        if (h->lpt > 16) {
             delete h;
             return fail(FREEKV_EUNSUPPORTED, "max_ctx_tokens / page_size > 8192 pages");
         }
@@ -461,7 +603,9 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         // T <= V (every warp owns >= 1 page), T * V < 2^31 (32-bit range math), and at most
         // ~254 records per unit (combine kernel capacity)
         const long long V = (long long)D.U * D.P_max;
-        long long T = std::min<long long>({(long long)warps, (long long)kMaxAttnWarps, V, 254LL * D.U});
+        const char* mp = getenv("FREEKV_ATTN_MIN_PAGES");  // pages per warp (>= 1): fewer, longer warps
+        const long long minp = std::max(1, mp ? atoi(mp) : 1);
+        long long T = std::min<long long>({(long long)warps, (long long)kMaxAttnWarps, V / minp, 254LL * D.U});
         while (T > 1 && T * V >= (1LL << 31)) T /= 2;
         h->D.attn_warps = (int)std::max(1LL, T);
     }
@@ -469,13 +613,14 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
     {
         const char* tr = getenv("FREEKV_TRACE");
         if (tr && tr[0] == '1') {
-            const size_t n = (size_t)8 * 4096 * 8;
+            const size_t n = (size_t)kTraceClasses * kTraceEnt * kTraceStamps;
             if (cudaMalloc(&h->X.trace, n * 8) != cudaSuccess || cudaMemset(h->X.trace, 0, n * 8) != cudaSuccess) {
                 freekv_destroy(h);
                 return fail(FREEKV_ECUDA, "trace buffer");
             }
         }
     }
+    h->Xb.trace = h->X.trace;
     {
         const char* fr = getenv("FREEKV_DEBUG_FULL_REFRESH");
         h->D.full_refresh = (fr && fr[0] == '1') ? 1 : 0;
@@ -490,6 +635,8 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
     h->ev_recall.resize(cfg->n_layers);
     h->ev_sync.resize(cfg->n_layers);
     h->ev_sync_x.resize(cfg->n_layers);
+    h->ev_pre.resize(cfg->n_layers);
+    h->ev_fl.resize(cfg->n_layers);
     {
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -502,7 +649,9 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         if (cudaEventCreateWithFlags(&h->ev_select[l], cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&h->ev_recall[l], cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&h->ev_sync[l], cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&h->ev_sync_x[l], cudaEventDisableTiming) != cudaSuccess) {
+            cudaEventCreateWithFlags(&h->ev_sync_x[l], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->ev_pre[l], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->ev_fl[l], cudaEventDisableTiming) != cudaSuccess) {
             freekv_destroy(h);
             return fail(FREEKV_ECUDA, "cudaEventCreate failed");
         }
@@ -565,6 +714,7 @@ freekv_status freekv_decode_step(freekv_handle* h, int32_t layer, const void* q,
     cudaStream_t s = h->cs;
     if (!k_new || !v_new) return fail(FREEKV_EINVAL, "k_new/v_new is NULL");
     if (h->ctx_host[layer] + 1 > h->D.max_ctx) return fail(FREEKV_ERANGE, "context would exceed max_ctx_tokens");
+    if (h->pipelined) return do_step_pipelined(h, layer, q, k_new, v_new, out);
     if (h->D.n_win >= 1) {
         if ((st = do_select(h, layer, q, nullptr, nullptr, s, k_new, v_new)) != FREEKV_OK) return st;
     } else {  // W = 0: the page completed by this token is a candidate now -> append first
@@ -694,7 +844,7 @@ freekv_status freekv_debug_trace(freekv_handle* h, uint64_t* out, size_t n) {
     if (!h->X.trace) return fail(FREEKV_ESTATE, "tracing is off (set FREEKV_TRACE=1 before freekv_init)");
     freekv_status st = sync_both(h);
     if (st != FREEKV_OK) return st;
-    const size_t cap = (size_t)8 * 4096 * 8;
+    const size_t cap = (size_t)kTraceClasses * kTraceEnt * kTraceStamps;
     FKV_CUDA(cudaMemcpy(out, h->X.trace, std::min(n, cap) * 8, cudaMemcpyDeviceToHost));
     FKV_CUDA(cudaMemset(h->X.trace, 0, cap * 8));
     return FREEKV_OK;
@@ -731,6 +881,10 @@ freekv_status freekv_step_graph_capture(freekv_handle* h, const void* q_all, con
         const uint8_t* q = (const uint8_t*)q_all + q_stride * l;
         const uint8_t* k = (const uint8_t*)k_all + kv_stride * l;
         const uint8_t* v = (const uint8_t*)v_all + kv_stride * l;
+        if (h->pipelined) {
+            st = do_step_pipelined(h, l, q, k, v, out_all + o_stride * l);
+            continue;
+        }
         if (D.n_win >= 1) {
             st = do_select(h, l, q, nullptr, nullptr, h->cs, k, v);
         } else {
@@ -744,8 +898,12 @@ freekv_status freekv_step_graph_capture(freekv_handle* h, const void* q_all, con
     if (e == cudaSuccess && st == FREEKV_OK) {
         e = cudaStreamBeginCapture(h->rs, cudaStreamCaptureModeThreadLocal);
         for (int l = 0; l < h->cfg.n_layers && e == cudaSuccess; ++l) {
-            e = cudaStreamWaitEvent(h->rs, h->ev_sync_x[l], cudaEventWaitExternal);
-            if (e == cudaSuccess) e = timed(h, K_RECALL_BG, h->rs, [&] { return launch_recall(D, h->layers[l], 0, h->rs); });
+            // direct / pipelined mode: after this layer's attention; recall mode: after its synchronous recall
+            e = cudaStreamWaitEvent(h->rs, D.direct ? h->ev_select[l] : h->ev_sync_x[l], cudaEventWaitExternal);
+            if (e == cudaSuccess && h->pipelined)
+                e = bg_chain(h, l, h->rs);
+            else if (e == cudaSuccess)
+                e = timed(h, K_RECALL_BG, h->rs, [&] { return launch_recall(D, h->layers[l], 0, h->rs, h->X.trace); });
             if (e == cudaSuccess) e = cudaEventRecordWithFlags(h->ev_recall[l], h->rs, cudaEventRecordExternal);
         }
         e2 = cudaStreamEndCapture(h->rs, &gr);
@@ -819,6 +977,10 @@ void freekv_destroy(freekv_handle* h) {
     for (auto e : h->ev_sync)
         if (e) cudaEventDestroy(e);
     for (auto e : h->ev_sync_x)
+        if (e) cudaEventDestroy(e);
+    for (auto e : h->ev_pre)
+        if (e) cudaEventDestroy(e);
+    for (auto e : h->ev_fl)
         if (e) cudaEventDestroy(e);
     for (auto e : h->prof_pool) cudaEventDestroy(e);
     if (h->ss) cudaStreamDestroy(h->ss);

@@ -25,6 +25,7 @@
 // each warp always has 8 KiB in flight.  P is split into bf16 hi + lo parts
 // (two PV MMAs) so its rounding stays ~2^-17, far inside the 2e-3 output
 // tolerance (readings A-19/A-21).
+#include <algorithm>
 #include <cstdlib>
 
 #include "fkv_internal.cuh"
@@ -127,6 +128,22 @@ __device__ __forceinline__ int slab_info(const FkvDims& D, const FkvLayer& L, in
     const uint16_t* base = page_ptr(D, L, u, M, pi, pv);
     row = (int)((base - arena) / kHeadDim) + slab * 16;
     return pv - slab * 16;
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int y, const void* smem) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(x),
+                 "r"(y), "r"(smem_u32(smem))
+                 : "memory");
+}
+
+// direct mode: write a slab that was read from the host pool back into its slot
+// (arena rows [row, row+16) and [row+p, row+p+16)); one bulk group per slab
+__device__ __forceinline__ void store_slab(const CUtensorMap* map, const uint8_t* st, int row, int p) {
+    tma_store_2d(map, 0, row, st + 0 * kBoxBytes);
+    tma_store_2d(map, 64, row, st + 1 * kBoxBytes);
+    tma_store_2d(map, 0, row + p, st + 2 * kBoxBytes);
+    tma_store_2d(map, 64, row + p, st + 3 * kBoxBytes);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
 __device__ __forceinline__ void issue_slab(const CUtensorMap* map, uint8_t* st, uint64_t* bar, int row, int p) {
@@ -280,6 +297,7 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2) fkv_a
                                                                                const uint16_t* __restrict__ q,
                                                                                int phase,
                                                                                const __grid_constant__ CUtensorMap tmap,
+                                                                               const __grid_constant__ CUtensorMap tmap_h,
                                                                                const uint16_t* arena) {
     constexpr int kStages = NST;
     extern __shared__ __align__(1024) uint8_t s_stage[];  // [warps][kStages][8 KiB]
@@ -349,18 +367,21 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2) fkv_a
             const int np = min(32, pb - cb);
             // page table of the segment, one page per lane: first K row in the arena tensor and
             // valid tokens -- one batch of independent loads instead of a dependent load per slab
-            int my_row = 0, my_valid = 0;
+            int my_row = 0, my_valid = 0, my_dst = 0;
             if (lane < np) {
                 my_row = prow[cb + lane];
                 my_valid = X.page_valid[(size_t)u * D.P_max + cb + lane];
+                if (my_valid & 0x80) my_dst = X.page_dst[(size_t)u * D.P_max + cb + lane];
             }
+            const unsigned host_mask = __ballot_sync(0xffffffffu, my_valid & 0x80);  // pages read from the host pool
             const int nx = np * spp;
             if (lane == 0) trace_stamp(X.trace, tcls, w, 1);
             auto slab_of = [&](int x, int& row) {  // warp-uniform; spp = 1 << lspp
                 const int pi = x >> lspp, sl = x & (spp - 1);
                 row = __shfl_sync(0xffffffffu, my_row, pi) + sl * 16;
-                return __shfl_sync(0xffffffffu, my_valid, pi) - sl * 16;
+                return (__shfl_sync(0xffffffffu, my_valid, pi) & 0x7f) - sl * 16;
             };
+            auto is_host = [&](int x) { return (host_mask >> (x >> lspp)) & 1u; };
             // prologue: first kStages slabs of this segment in flight
             int rows[kStages], valids[kStages];
 #pragma unroll
@@ -368,7 +389,8 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2) fkv_a
             if (lane == 0) {
 #pragma unroll
                 for (int i = 0; i < kStages; ++i)
-                    if (valids[i] > 0) issue_slab(&tmap, ring + i * kSlabBytes, &bar[warp][i], rows[i], D.p);
+                    if (valids[i] > 0)
+                        issue_slab(is_host(i) ? &tmap_h : &tmap, ring + i * kSlabBytes, &bar[warp][i], rows[i], D.p);
             }
             for (int i = 0; i < nx; ++i) {
                 const int stg = i % kStages;
@@ -376,6 +398,7 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2) fkv_a
                 const int valid = slab_of(i, row);
                 int row2 = 0, valid2 = 0;
                 if (i + kStages < nx) valid2 = slab_of(i + kStages, row2);
+                const int dst = host_mask ? __shfl_sync(0xffffffffu, my_dst, i >> lspp) + (i & (spp - 1)) * 16 : 0;
                 if (valid > 0) {
                     mbar_wait(&bar[warp][stg], (phase_bits >> stg) & 1u);
                     phase_bits ^= 1u << stg;
@@ -383,11 +406,19 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2) fkv_a
                     compute_slab(ring + stg * kSlabBytes, valid, qa, sc, g, t, m_run, l_run, oacc);
                 }
                 __syncwarp();  // every lane is done with this stage before it is refilled
-                if (lane == 0 && valid2 > 0) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    issue_slab(&tmap, ring + stg * kSlabBytes, &bar[warp][stg], row2, D.p);
+                if (lane == 0) {
+                    if (valid > 0 && is_host(i)) {
+                        store_slab(&tmap, ring + stg * kSlabBytes, dst, D.p);  // recall fused: cache the page
+                        if (valid2 > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    }
+                    if (valid2 > 0) {
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        issue_slab(is_host(i + kStages) ? &tmap_h : &tmap, ring + stg * kSlabBytes, &bar[warp][stg],
+                                   row2, D.p);
+                    }
                 }
             }
+            if (host_mask && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         }
         if (lane == 0) trace_stamp(X.trace, tcls, w, 3);
         // ---- partial record (w, k_rec) of unit u: unnormalised, relative to m_run.  Lane (g, t)
@@ -432,16 +463,23 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2) fkv_a
 // Merge a unit's partial records and commit the speculative advance (row a8).
 // The records of unit u are the contiguous warps w_first..w_last whose page
 // ranges intersect [u*P_max, (u+1)*P_max) (every warp owns >= 1 page, T <= V;
-// 32-bit range math, T * V < 2^31 is guaranteed on the host).  Thread (h, c)
-// issues the loads of a batch of records at once and merges them with an
-// online max, so the kernel costs ~2 global round trips.
-constexpr int kCombBatch = 12;
+// 32-bit range math, T * V < 2^31 is guaranteed on the host).  A record is
+// G x 128 floats; thread (rg, e) owns float4 e of it and merges the records
+// r = rg (mod RG) with an online max, all of its loads in flight at once (one
+// round trip for up to kCombBatch records per group); the RG partial states
+// are then merged through shared memory.
+constexpr int kCombThreads = 512;
+constexpr int kCombBatch = 8;
 constexpr int kMaxRecs = 256;  // records per unit (host guarantees P_max * T / V + 2 <= 256)
 
-__global__ void __launch_bounds__(1024) fkv_attn_combine_kernel(FkvDims D, FkvLayer L, FkvScratch X,
-                                                                const uint16_t* __restrict__ q,
-                                                                float* __restrict__ out, int split) {
+__global__ void __launch_bounds__(kCombThreads, 2) fkv_attn_combine_kernel(FkvDims D, FkvLayer L, FkvScratch X,
+                                                                        const uint16_t* __restrict__ q,
+                                                                        float* __restrict__ out, int split,
+                                                                        int commit) {
     if (threadIdx.x == 0) trace_stamp(X.trace, 7, blockIdx.x, 0);
+    // everything below reads state of this step: with PDL the kernel may start while the
+    // select kernel (two launches back) is still running, so nothing is read before this
+    pdl_wait();  // the attention's partial records (and the select kernel's lists) are complete
     const int u = blockIdx.x, b = u / D.n_kv, m = u % D.n_kv, G = D.G;
     // rank of u among the units of its attention phase (split: by correction flag)
     __shared__ int s_rank, s_n;
@@ -469,13 +507,6 @@ __global__ void __launch_bounds__(1024) fkv_attn_combine_kernel(FkvDims D, FkvLa
     const int w_first = (int)(((x0 + 1) * T + V - 1) / V) - 1;
     const int w_last = (int)((x1 * T + V - 1) / V) - 1;
     const int nr = w_last - w_first + 1;
-    pdl_wait();  // the attention phases' partial records are complete
-    // commit loads first (independent of the merge)
-    int rp = 0, rs = 0;
-    if (threadIdx.x < D.K) {
-        rp = L.pend_pages[(size_t)u * D.K + threadIdx.x];
-        rs = L.pend_slot[(size_t)u * D.K + threadIdx.x];
-    }
     // record indices, computed once (integer division is ~30 instructions)
     __shared__ int s_rec[kMaxRecs];
     for (int r = threadIdx.x; r < nr && r < kMaxRecs; r += blockDim.x) {
@@ -483,24 +514,33 @@ __global__ void __launch_bounds__(1024) fkv_attn_combine_kernel(FkvDims D, FkvLa
         const unsigned a = w * V / T;
         s_rec[r] = (int)((rec_base + w) * 2 + ((a / D.P_max == (unsigned)s_rank) ? 0 : 1));
     }
+    const int E = G * (kHeadDim / 4);  // float4 per record
+    const int RG = kCombThreads / E;   // record groups
+    const int e = threadIdx.x % E, rg = threadIdx.x / E, h = e / (kHeadDim / 4);
+    int rp = 0, rs = 0;
+    if (threadIdx.x < D.K) {
+        rp = L.pend_pages[(size_t)u * D.K + threadIdx.x];
+        rs = L.pend_slot[(size_t)u * D.K + threadIdx.x];
+    }
     __syncthreads();
-    const int h = threadIdx.x / kHeadDim, c = threadIdx.x % kHeadDim;
-    if (h < G) {
-        const size_t row = (size_t)b * D.n_qo + m * G + h;
-        const uint16_t qv = q[row * kHeadDim + c];
-        float M = -INFINITY, Ls = 0.0f, O = 0.0f;
-        for (int r0 = 0; r0 < nr; r0 += kCombBatch) {
-            float vo[kCombBatch], vm[kCombBatch], vl[kCombBatch];
+    float M = -INFINITY, Ls = 0.0f;
+    float4 O = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    const float4* po = reinterpret_cast<const float4*>(X.part_o);
+    if (rg < RG) {
+        for (int r0 = rg; r0 < nr; r0 += kCombBatch * RG) {
+            float vm[kCombBatch], vl[kCombBatch];
+            float4 vo[kCombBatch];
 #pragma unroll
             for (int i = 0; i < kCombBatch; ++i) {
+                const int r = r0 + i * RG;
                 vm[i] = -INFINITY;
                 vl[i] = 0.0f;
-                vo[i] = 0.0f;
-                if (r0 + i < nr) {
-                    const size_t rec = (size_t)s_rec[r0 + i];
+                vo[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                if (r < nr) {
+                    const size_t rec = (size_t)s_rec[r];
                     vm[i] = X.part_ml[(rec * G + h) * 2 + 0];
                     vl[i] = X.part_ml[(rec * G + h) * 2 + 1];
-                    vo[i] = X.part_o[(rec * G + h) * kHeadDim + c];
+                    vo[i] = po[rec * E + e];
                 }
             }
             float Mb = M;
@@ -509,19 +549,58 @@ __global__ void __launch_bounds__(1024) fkv_attn_combine_kernel(FkvDims D, FkvLa
             if (Mb != -INFINITY) {
                 const float sc = exp2f(M - Mb);  // M = -inf -> 0
                 Ls *= sc;
-                O *= sc;
+                O.x *= sc;
+                O.y *= sc;
+                O.z *= sc;
+                O.w *= sc;
 #pragma unroll
                 for (int i = 0; i < kCombBatch; ++i) {
                     const float wgt = vm[i] == -INFINITY ? 0.0f : exp2f(vm[i] - Mb);
                     Ls += wgt * vl[i];
-                    O += wgt * vo[i];
+                    O.x += wgt * vo[i].x;
+                    O.y += wgt * vo[i].y;
+                    O.z += wgt * vo[i].z;
+                    O.w += wgt * vo[i].w;
                 }
                 M = Mb;
             }
         }
-        out[row * kHeadDim + c] = O / Ls;
-        L.q_prev[row * kHeadDim + c] = qv;  // q_prev := q_i
     }
+    // merge the RG group states: group g > 0 publishes, group 0 folds them in
+    __shared__ float4 s_o[kCombThreads];
+    __shared__ float s_m[kCombThreads], s_l[kCombThreads];
+    if (rg > 0 && rg < RG) {
+        s_o[threadIdx.x] = O;
+        s_m[threadIdx.x] = M;
+        s_l[threadIdx.x] = Ls;
+    }
+    __syncthreads();
+    const bool do_commit = commit == 0 || L.flags[u] != 0;
+    if (rg == 0) {
+        float Mb = M;
+        for (int g2 = 1; g2 < RG; ++g2) Mb = fmaxf(Mb, s_m[g2 * E + e]);
+        float wgt = M == -INFINITY ? 0.0f : exp2f(M - Mb);
+        float Lt = wgt * Ls;
+        float4 Ot = make_float4(wgt * O.x, wgt * O.y, wgt * O.z, wgt * O.w);
+        for (int g2 = 1; g2 < RG; ++g2) {
+            const float mg = s_m[g2 * E + e];
+            const float wg = mg == -INFINITY ? 0.0f : exp2f(mg - Mb);
+            const float4 og = s_o[g2 * E + e];
+            Lt += wg * s_l[g2 * E + e];
+            Ot.x += wg * og.x;
+            Ot.y += wg * og.y;
+            Ot.z += wg * og.z;
+            Ot.w += wg * og.w;
+        }
+        const size_t row = (size_t)b * D.n_qo + m * G + h;
+        const int c4 = e % (kHeadDim / 4);
+        reinterpret_cast<float4*>(out + row * kHeadDim)[c4] = make_float4(Ot.x / Lt, Ot.y / Lt, Ot.z / Lt, Ot.w / Lt);
+        // q_prev := q_i (4 bf16 = 8 bytes per thread)
+        if (do_commit)
+            reinterpret_cast<uint2*>(L.q_prev + row * kHeadDim)[c4] =
+                reinterpret_cast<const uint2*>(q + row * kHeadDim)[c4];
+    }
+    if (!do_commit) return;
     if (threadIdx.x < D.K) {
         L.res_pages[(size_t)u * D.K + threadIdx.x] = rp;
         L.res_slot[(size_t)u * D.K + threadIdx.x] = rs;
@@ -568,9 +647,13 @@ static cudaError_t attn_setup(int* warps) {
     if (e == cudaSuccess)
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fkv_attn_split_kernel<NST>,
                                                           kAttnWarpsPerCta * 32, smem);
-    // leave ~1/8 of the CTA slots free so the recall kernels (other streams) get SMs
-    const int ctas = sms * per_sm;
-    *warps = (ctas - ctas / 8) * kAttnWarpsPerCta;
+    // CTAs per SM (FREEKV_ATTN_CTAS_PER_SM, default 1): one 4-warp CTA per SM keeps ~14 MB of
+    // TMA loads in flight (3 slabs x 8 KiB per warp), enough to cover HBM latency at full
+    // bandwidth, and leaves shared memory and warp slots for the select kernels that run
+    // concurrently in the pipelined step
+    const char* ce = getenv("FREEKV_ATTN_CTAS_PER_SM");
+    const int cps = std::max(1, std::min(per_sm, ce ? atoi(ce) : 1));
+    *warps = sms * cps * kAttnWarpsPerCta;
     return e;
 }
 
@@ -584,26 +667,28 @@ cudaError_t attn_resident_warps(int* warps) {
 }
 
 cudaError_t launch_attn_split(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                              int phase, const CUtensorMap& tmap, const uint16_t* arena, bool pdl, cudaStream_t s) {
+                              int phase, const CUtensorMap& tmap, const CUtensorMap& tmap_h, const uint16_t* arena,
+                              bool pdl, cudaStream_t s) {
     const int ctas = (D.attn_warps + kAttnWarpsPerCta - 1) / kAttnWarpsPerCta;
     const int nst = attn_stages();
     const int smem = kAttnWarpsPerCta * nst * kSlabBytes;
     switch (nst) {
         case 2:
             return launch_ex(fkv_attn_split_kernel<2>, dim3(ctas), dim3(kAttnWarpsPerCta * 32), smem, s, pdl, D, L, X, q,
-                             phase, tmap, arena);
+                             phase, tmap, tmap_h, arena);
         case 4:
             return launch_ex(fkv_attn_split_kernel<4>, dim3(ctas), dim3(kAttnWarpsPerCta * 32), smem, s, pdl, D, L, X, q,
-                             phase, tmap, arena);
+                             phase, tmap, tmap_h, arena);
         default:
             return launch_ex(fkv_attn_split_kernel<3>, dim3(ctas), dim3(kAttnWarpsPerCta * 32), smem, s, pdl, D, L, X, q,
-                             phase, tmap, arena);
+                             phase, tmap, tmap_h, arena);
     }
 }
 
 cudaError_t launch_attn_combine(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                                float* out, int split, bool pdl, cudaStream_t s) {
-    return launch_ex(fkv_attn_combine_kernel, dim3(D.U), dim3(D.G * kHeadDim), 0, s, pdl, D, L, X, q, out, split);
+                                float* out, int split, int commit, bool pdl, cudaStream_t s) {
+    return launch_ex(fkv_attn_combine_kernel, dim3(D.U), dim3(kCombThreads), 0, s, pdl, D, L, X, q, out, split,
+                     commit);
 }
 
 }  // namespace fkv

@@ -31,6 +31,9 @@ struct FkvDims {
     float attn_c;     // log2(e)/sqrt(d) for attention softmax (not CFR)
     int P_max;        // upper bound of attention pages per unit: n_sink + K + R_loc
     int attn_warps;   // T: warps of the balanced split-KV attention grid (<= resident warps)
+    int direct;       // 1: corrected units' fetched pages are read by the attention kernel straight
+                      // from the host pool (and written back to their slots); 0: synchronous recall
+                      // before a second attention phase
 };
 
 struct FkvLayer {
@@ -57,12 +60,15 @@ struct FkvLayer {
     int32_t* n_off;       // [U]     pages [0, n_off) are offloaded; candidates [n_sink, n_off)
     uint16_t* host;       // device-mapped host pool of this layer: [nb][n_page_host][n_kv][2][p][d]
     const uint16_t* arena;  // base of the device arena (row 0 of the attention TMA tensor)
+    int host_row0;        // first row of this layer's host pool in the host TMA tensor (256-byte rows)
 };
 
 struct FkvScratch {
     float* scores;        // [U][G][n_page_max]
     int32_t* page_rows;   // [U][P_max] attention page list of this step: arena row of the page's K block
-    uint8_t* page_valid;  // [U][P_max] valid tokens of each listed page
+    uint8_t* page_valid;  // [U][P_max] valid tokens of each listed page; bit 7: the row is a host
+                          // pool row (direct mode), to be written back to arena row page_dst
+    int32_t* page_dst;    // [U][P_max] arena row of the slot a host-read page is written back to
     unsigned long long* trace;  // diagnostics (FREEKV_TRACE=1): %globaltimer stamps, else NULL
     int32_t* page_cnt;    // [U]
     float* part_o;        // [2 phases][attn_warps][2 segments][G][d] per-warp, per-unit-segment partial outputs
@@ -93,7 +99,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-// trace slots: [kernel class 0..7][entity < 4096][stamp < 8]
+// trace slots: [kernel class 0..11][entity < 4096][stamp < 8]
+constexpr int kTraceClasses = 12;
 constexpr int kTraceEnt = 4096, kTraceStamps = 8;
 __device__ __forceinline__ void trace_stamp(unsigned long long* tr, int cls, int ent, int i) {
     if (tr && ent < kTraceEnt) tr[((size_t)cls * kTraceEnt + ent) * kTraceStamps + i] = gtimer();
@@ -156,19 +163,25 @@ cudaError_t launch_append(const FkvDims& D, const FkvLayer& L, const uint16_t* k
                           int n_new, cudaStream_t s);
 cudaError_t launch_summarize(const FkvDims& D, const FkvLayer& L, int page_begin, int page_end,
                              cudaStream_t s);
+// which (score / finalize): 0 every unit, 1 unflagged units only, 2 corrected units only
 cudaError_t launch_score(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                         int max_n_off, int pending, cudaStream_t s);
+                         int max_n_off, int pending, int which, cudaStream_t s);
+cudaError_t launch_prep(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
+                        const uint16_t* k_new, const uint16_t* v_new, uint8_t* corrected_out, cudaStream_t s);
 cudaError_t launch_select_fused(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                                 const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
                                 uint8_t* corrected_out, int cluster, int lptm, cudaStream_t s);
 cudaError_t launch_finalize(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                             const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
-                            uint8_t* corrected_out, int lpt, bool pdl, cudaStream_t s);
+                            uint8_t* corrected_out, int lpt, bool pdl, int which, cudaStream_t s);
 cudaError_t launch_recall(const FkvDims& D, const FkvLayer& L, int sync_mode, cudaStream_t s,
                           unsigned long long* trace = nullptr);
 cudaError_t attn_resident_warps(int* warps);  // SMs x resident warps/SM of the split kernel
 cudaError_t launch_attn_split(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                              int phase, const CUtensorMap& tmap, const uint16_t* arena, bool pdl, cudaStream_t s);
+                              int phase, const CUtensorMap& tmap, const CUtensorMap& tmap_host,
+                              const uint16_t* arena, bool pdl, cudaStream_t s);
+// commit: 0 = every unit (R := S_i, q_prev := q_i), 2 = corrected units only (pipelined step:
+// the background select kernel commits the others)
 cudaError_t launch_attn_combine(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                                float* out, int split, bool pdl, cudaStream_t s);
+                                float* out, int split, int commit, bool pdl, cudaStream_t s);
 }  // namespace fkv

@@ -29,9 +29,10 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
 
 // The grid strides over the flattened (unit, fetch) pairs with 16 KiB of PCIe
 // reads in flight per CTA.  Measured on B200: zero-copy read bandwidth scales
-// with the number of SMs issuing (8 CTAs reach ~4 GB/s, one CTA per pair over
-// all SMs reaches ~50 GB/s = 91% of the pinned-copy peak at full refresh), so by
-// default every pair gets its own CTA (FREEKV_RECALL_{SYNC,BG}_CTAS caps it).
+// with the number of SMs issuing (8 CTAs reach ~4 GB/s; one CTA per SM reaches
+// the host link), while a grid of thousands of CTAs (one per pair) crowds the
+// block scheduler and delays the attention kernels running concurrently -- so by
+// default one CTA per SM (FREEKV_RECALL_{SYNC,BG}_CTAS overrides).
 __global__ void __launch_bounds__(128) fkv_recall_kernel(FkvDims D, FkvLayer L, int sync_mode,
                                                          unsigned long long* __restrict__ trace) {
     if (threadIdx.x == 0) trace_stamp(trace, 2 + (sync_mode ? 0 : 1), blockIdx.x, 0);
@@ -69,7 +70,7 @@ static int recall_ctas(int sync_mode) {
     if (!c[sync_mode]) {
         const char* e = getenv(sync_mode ? "FREEKV_RECALL_SYNC_CTAS" : "FREEKV_RECALL_BG_CTAS");
         const int v = e ? atoi(e) : 0;
-        c[sync_mode] = v > 0 ? v : 1 << 20;  // default: one CTA per (unit, fetch) pair
+        c[sync_mode] = v > 0 ? v : 148;  // default: one CTA per SM (zero-copy bandwidth scales with SMs)
     }
     return c[sync_mode];
 }
@@ -82,7 +83,14 @@ cudaError_t launch_recall(const FkvDims& D, const FkvLayer& L, int sync_mode, cu
                              cudaSharedmemCarveoutMaxShared);
         configured = true;
     }
-    const int grid = std::min(recall_ctas(sync_mode ? 1 : 0), D.U * D.K);
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int want = recall_ctas(sync_mode ? 1 : 0);
+    const int grid = std::min(want == 148 ? sms : want, D.U * D.K);
     fkv_recall_kernel<<<grid, 128, 0, s>>>(D, L, sync_mode, trace);
     return cudaGetLastError();
 }

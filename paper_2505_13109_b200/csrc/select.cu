@@ -13,6 +13,7 @@
 // recipe with explicit round-to-nearest intrinsics, so the page
 // indices are bit-identical to the CPU oracle.
 #include <algorithm>
+#include <cstdlib>
 
 #include "append_unit.cuh"
 
@@ -95,75 +96,90 @@ template <int G>
 __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims D, FkvLayer L,
                                                                         float* __restrict__ scores,
                                                                         const uint16_t* __restrict__ q, int pending,
-                                                                        unsigned long long* __restrict__ trace) {
+                                                                        unsigned long long* __restrict__ trace,
+                                                                        int which, int gy) {
     constexpr int GP = (G + 3) / 4 * 4;
     extern __shared__ __align__(128) uint8_t s_raw[];
     __shared__ __align__(16) float qv[kHeadDim][GP];      // q_c per head
     __shared__ __align__(16) uint32_t qm[kHeadDim][GP];   // ~0 if q_c >= 0 (take max) else 0 (take min)
     __shared__ __align__(8) uint64_t bar[kScoreWarps][kRing];
     pdl_trigger();  // the select-finalize kernel may start its prologue now
-    const int u = blockIdx.x, b = u / D.n_kv, m = u % D.n_kv;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_off = max(L.n_off[u], frontier_for(D, L.ctx[u] + pending));
-    if ((int)blockIdx.y * kScoreWarps * 32 >= n_off) return;  // uniform: no candidate in this CTA
-    const int blk = blockIdx.y * kScoreWarps + warp;
-    const bool active = blk * 32 < n_off && blk * 32 + 31 >= D.n_sink;
-    const int tent = blockIdx.x * gridDim.y + blockIdx.y;
-    if (threadIdx.x == 0) trace_stamp(trace, 0, tent, 0);
+    const int tcls = which == 1 ? 9 : 0;  // trace class
     uint8_t* ring = s_raw + warp * (kRing * kChunkBytes);
-    const uint8_t* src = reinterpret_cast<const uint8_t*>(L.summ + summ_chunk_offset(D, u, blk * 32, 0, 0));
     if (lane == 0) {
 #pragma unroll
         for (int r = 0; r < kRing; ++r) mbar_init(&bar[warp][r], 1);
         fence_mbar_init();
-        if (active) {
+    }
+    uint32_t ph = 0u;  // per-slot parity of this warp's next completion (slots are reused across items)
+    // items (unit, 128-page block): one per CTA, or a grid-stride loop over all of them when the
+    // grid is smaller (the background score runs on a bounded number of CTAs)
+    for (int item = blockIdx.x; item < D.U * gy; item += gridDim.x) {
+        const int u = item / gy, yb = item - u * gy, b = u / D.n_kv, m = u % D.n_kv;
+        // which: 0 every unit; 1 unflagged units only (background); 2 corrected units only
+        const int flg = which ? L.flags[u] : 0;
+        const int n_off = max(L.n_off[u], frontier_for(D, L.ctx[u] + pending));
+        if (which && (flg != 0) != (which == 2)) continue;
+        if (yb * kScoreWarps * 32 >= n_off) continue;  // uniform: no candidate in this item
+        __syncthreads();  // the previous item's q staging is no longer read
+        const int blk = yb * kScoreWarps + warp;
+        const bool active = blk * 32 < n_off && blk * 32 + 31 >= D.n_sink;
+        const int tent = item;
+        if (threadIdx.x == 0) trace_stamp(trace, tcls, tent, 0);
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(L.summ + summ_chunk_offset(D, u, blk * 32, 0, 0));
+        if (lane == 0 && active) {
 #pragma unroll
             for (int k = 0; k < kRing; ++k) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_expect_tx(&bar[warp][k], kChunkBytes);
                 bulk_g2s(ring + k * kChunkBytes, src + k * kChunkBytes, kChunkBytes, &bar[warp][k]);
             }
         }
-    }
-    for (int i = threadIdx.x; i < GP * kHeadDim; i += blockDim.x) {
-        const int h = i / kHeadDim, c = i % kHeadDim;
-        float x = 0.0f;
-        if (h < G) x = bf16f(q[((size_t)b * D.n_qo + m * G + h) * kHeadDim + c]);
-        qv[c][h] = x;
-        qm[c][h] = x >= 0.0f ? 0xffffffffu : 0u;  // CFR-2: q_c >= 0 (incl. -0) uses the max
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) trace_stamp(trace, 0, tent, 1);
-    if (!active) return;
-    float acc[G];
+        for (int i = threadIdx.x; i < GP * kHeadDim; i += blockDim.x) {
+            const int h = i / kHeadDim, c = i % kHeadDim;
+            float x = 0.0f;
+            if (h < G) x = bf16f(q[((size_t)b * D.n_qo + m * G + h) * kHeadDim + c]);
+            qv[c][h] = x;
+            qm[c][h] = x >= 0.0f ? 0xffffffffu : 0u;  // CFR-2: q_c >= 0 (incl. -0) uses the max
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) trace_stamp(trace, tcls, tent, 1);
+        if (!active) continue;
+        float acc[G];
 #pragma unroll
-    for (int h = 0; h < G; ++h) acc[h] = 0.0f;
+        for (int h = 0; h < G; ++h) acc[h] = 0.0f;
 #pragma unroll 1
-    for (int k = 0; k < 4; ++k) {
-        const int slot = k % kRing;
-        mbar_wait(&bar[warp][slot], (uint32_t)(k / kRing) & 1u);
-        if (k == 0 && threadIdx.x == 0) trace_stamp(trace, 0, tent, 2);
-        score_channels<G>(reinterpret_cast<const uint4*>(ring + slot * kChunkBytes) - (k * 4) * 2 * 32, k * 4,
-                          lane, qv, qm, acc);
-        if (k + kRing < 4) {
-            __syncwarp();  // all lanes are done with this slot
-            if (lane == 0) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_expect_tx(&bar[warp][slot], kChunkBytes);
-                bulk_g2s(ring + slot * kChunkBytes, src + (k + kRing) * kChunkBytes, kChunkBytes, &bar[warp][slot]);
+        for (int k = 0; k < 4; ++k) {
+            const int slot = k % kRing;
+            mbar_wait(&bar[warp][slot], (ph >> slot) & 1u);
+            ph ^= 1u << slot;
+            if (k == 0 && threadIdx.x == 0) trace_stamp(trace, tcls, tent, 2);
+            score_channels<G>(reinterpret_cast<const uint4*>(ring + slot * kChunkBytes) - (k * 4) * 2 * 32, k * 4,
+                              lane, qv, qm, acc);
+            if (k + kRing < 4) {
+                __syncwarp();  // all lanes are done with this slot
+                if (lane == 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_expect_tx(&bar[warp][slot], kChunkBytes);
+                    bulk_g2s(ring + slot * kChunkBytes, src + (k + kRing) * kChunkBytes, kChunkBytes,
+                             &bar[warp][slot]);
+                }
             }
         }
-    }
-    const int j = blk * 32 + lane;
-    if (j >= D.n_sink && j < n_off) {
+        __syncwarp();  // every lane is done with the ring before the next item refills it
+        const int j = blk * 32 + lane;
+        if (j >= D.n_sink && j < n_off) {
 #pragma unroll
-        for (int h = 0; h < G; ++h)
-            scores[((size_t)u * G + h) * D.n_page_max + j] = __fmul_rn(acc[h], D.score_r);  // CFR-3
+            for (int h = 0; h < G; ++h)
+                scores[((size_t)u * G + h) * D.n_page_max + j] = __fmul_rn(acc[h], D.score_r);  // CFR-3
+        }
+        if (threadIdx.x == 0) trace_stamp(trace, tcls, tent, 3);
     }
-    if (threadIdx.x == 0) trace_stamp(trace, 0, tent, 3);
 }
 
 // ------------------------------------------------------ a9 + a1 + a3 + a4
-// One 1024-thread CTA per unit.  Leaf (page) j of the pairwise tree (CFR-6) is
+// One 512-thread CTA per unit.  Leaf (page) j of the pairwise tree (CFR-6) is
 // owned by thread j / LPT, so thread-local trees + an xor butterfly inside a warp
 // + the same butterfly over the 32 warp partials reproduce the balanced tree
 // over page ids exactly.  Cross-warp reductions are re-done redundantly by every
@@ -171,22 +187,19 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims 
 // its histogram (2 barriers per 8-bit pass) with warp-aggregated atomics; one
 // packed (gt, eq) block scan places the selected ids in ascending order.
 constexpr int kMaxK = 256;
-constexpr int kThreads = 1024;
+constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 
 template <int LPT, int GM>
-__global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D, FkvLayer L,
-                                                                       int32_t* __restrict__ page_rows,
-                                                                       uint8_t* __restrict__ page_valid,
-                                                                       int32_t* __restrict__ page_cnt,
-                                                                       unsigned long long* __restrict__ trace,
-                                                                       const float* __restrict__ scores,
-                                                                       const uint16_t* __restrict__ q,
-                                                                       const uint16_t* __restrict__ k_new,
-                                                                       const uint16_t* __restrict__ v_new,
-                                                                       int32_t* __restrict__ pages_out,
-                                                                       uint8_t* __restrict__ corrected_out) {
-    const int u = blockIdx.x, b = u / D.n_kv, m = u % D.n_kv, G = D.G;
+__device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, const FkvLayer& L,
+                                              int32_t* __restrict__ page_rows, uint8_t* __restrict__ page_valid,
+                                              int32_t* __restrict__ page_dst, int32_t* __restrict__ page_cnt,
+                                              unsigned long long* __restrict__ trace,
+                                              const float* __restrict__ scores, const uint16_t* __restrict__ q,
+                                              const uint16_t* __restrict__ k_new,
+                                              const uint16_t* __restrict__ v_new, int32_t* __restrict__ pages_out,
+                                              uint8_t* __restrict__ corrected_out, int which) {
+    const int b = u / D.n_kv, m = u % D.n_kv, G = D.G;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_sink = D.n_sink, K = D.K;
 
@@ -207,8 +220,14 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
     uint4* s_page = reinterpret_cast<uint4*>(s_dyn);                                   // append staging
     float* s_sc = reinterpret_cast<float*>(s_dyn + page_elems(D) * sizeof(uint16_t));  // [G][n_page_max]
 
-    if (tid == 0) trace_stamp(trace, 1, u, 0);
+    // which: 0 = every unit, flags computed here (primitive API / non-pipelined step);
+    // 1 = unflagged units only, flags from the prep kernel, commits R := S_i itself
+    // (background half of the pipelined step); 2 = corrected units only (critical half)
+    const int tcls = which == 1 ? 10 : 1;  // trace class
+    if (tid == 0) trace_stamp(trace, tcls, u, 0);
     pdl_trigger();  // attention may start its prologue
+    const int pre_flag = which ? (int)L.flags[u] : 0;
+    if (which && (pre_flag != 0) != (which == 2)) return;
     // ---- a9 (fused, decode path): append this step's token.  Runs while the score kernel
     // drains (PDL): it only touches the ring / the page completing now (not a candidate of
     // this step) / the host pool; ctx and n_off are published after pdl_wait().
@@ -222,7 +241,7 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
     }
     const int n_cand = n_off - n_sink;
     const bool rank_all = n_cand <= K;  // A-11: all candidates selected, no ranking
-    if (tid == 0) trace_stamp(trace, 1, u, 1);
+    if (tid == 0) trace_stamp(trace, tcls, u, 1);
 
     // ---- stage everything the CTA reads (one round trip): q_i, q_{i-1}, resident set, scores
     {
@@ -267,7 +286,7 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
     // ---- a1: correction (CFR-10): lanes 0..G-1 of the last warp run the sequential channel
     // sums in 4 chunks of 32 channels, interleaved with the radix passes below (where the
     // other warps wait on warp 0's digit scan) so they never lengthen the critical path
-    const bool cos_lane = warp == kWarps - 1 && lane < G;
+    const bool cos_lane = which == 0 && warp == kWarps - 1 && lane < G;
     float c_dot = 0.0f, c_n1 = 0.0f, c_n2 = 0.0f;
     auto cos_chunk = [&](int part) {
         const uint16_t* qa = reinterpret_cast<const uint16_t*>(s_qa) + lane * kHeadDim;
@@ -293,7 +312,7 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
         cnt = n_cand > 0 ? n_cand : 0;
         __syncthreads();
     } else {
-        if (tid == 0) trace_stamp(trace, 1, u, 2);
+        if (tid == 0) trace_stamp(trace, tcls, u, 2);
         const float* su = s_sc;
         const int jb = tid * LPT;
         // ---- CFR-4: max per head (exact, order-free); the G heads' shuffles interleave
@@ -358,7 +377,7 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
         for (int o = 1; o < 32; o <<= 1)
 #pragma unroll
             for (int g = 0; g < GM; ++g) Z[g] = __fadd_rn(Z[g], __shfl_xor_sync(0xffffffffu, Z[g], o));
-        if (tid == 0) trace_stamp(trace, 1, u, 3);
+        if (tid == 0) trace_stamp(trace, tcls, u, 3);
         // ---- CFR-7/8: p = e / Z; pooled = sequential sum over g; CFR-9 keys
         uint32_t key[LPT];
         bool cand[LPT];
@@ -423,7 +442,7 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
             prefix |= (uint32_t)s_dig[pass] << shift;
             mask |= 0xFFu << shift;
         }
-        if (tid == 0) trace_stamp(trace, 1, u, 4);
+        if (tid == 0) trace_stamp(trace, tcls, u, 4);
         const uint32_t T = prefix;  // K-th largest key; take k_rem of the keys equal to T (lowest ids)
         // ---- one packed block scan of (#gt, #eq) in page-id order
         unsigned n_gt = 0, n_eq = 0;
@@ -463,21 +482,25 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
     }
 
     // ---- flag (CFR-10 pooling, A-12, A-13)
-    if (tid == 0) trace_stamp(trace, 1, u, 5);
+    if (tid == 0) trace_stamp(trace, tcls, u, 5);
     if (tid == 0) {
-        float acc = s_cos[0];
-        for (int g = 1; g < G; ++g) acc = __fadd_rn(acc, s_cos[g]);
-        const float mean = __fdiv_rn(acc, (float)G);
-        int flag;
-        if (D.mode == 1 || D.tau >= 1.0f) flag = 1;
-        else if (D.mode == 2 || D.tau <= 0.0f) flag = 0;
-        else flag = mean < D.tau;
-        if (!res_valid) flag = 1;
-        s_flag = flag;
-        L.flags[u] = (uint8_t)flag;
-        L.cbar[u] = mean;
+        if (which) {
+            s_flag = pre_flag;  // decided by the prep kernel (same CFR-10 arithmetic)
+        } else {
+            float acc = s_cos[0];
+            for (int g = 1; g < G; ++g) acc = __fadd_rn(acc, s_cos[g]);
+            const float mean = __fdiv_rn(acc, (float)G);
+            int flag;
+            if (D.mode == 1 || D.tau >= 1.0f) flag = 1;
+            else if (D.mode == 2 || D.tau <= 0.0f) flag = 0;
+            else flag = mean < D.tau;
+            if (!res_valid) flag = 1;
+            s_flag = flag;
+            L.flags[u] = (uint8_t)flag;
+            L.cbar[u] = mean;
+            if (corrected_out) corrected_out[u] = (uint8_t)flag;
+        }
         L.pend_front[u] = n_off;
-        if (corrected_out) corrected_out[u] = (uint8_t)flag;
     }
     // ---- a4: delta vs resident (A-18) and slot assignment (slot double-buffering).  Membership
     // of S_i's pages in R via a page -> index table in the (now dead) score staging area;
@@ -535,6 +558,21 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
     }
     __syncthreads();
     for (int i = tid; i < K; i += kThreads) L.pend_slot[(size_t)u * K + i] = s_pslot[i];
+    if (which == 1) {
+        // background half: this unit's attention already ran on R (page list built by the prep
+        // kernel), so commit the speculative advance here: R := S_i
+        for (int i = tid; i < K; i += kThreads) {
+            L.res_pages[(size_t)u * K + i] = i < cnt ? s_sel[i] : -1;
+            L.res_slot[(size_t)u * K + i] = s_pslot[i];
+        }
+        if (tid == 0) {  // (q_prev := q_i was done by the prep kernel)
+            L.res_front[u] = n_off;
+            L.res_cnt[u] = cnt;
+            L.res_valid[u] = 1;
+            trace_stamp(trace, tcls, u, 6);
+        }
+        return;
+    }
     // ---- this step's attention page list (row a7), one entry per page: arena row of the
     // page's K block and its valid tokens -- sink pages, the pages in use (S_i if corrected,
     // the resident set otherwise), local pages [f*p, Lc) (reading A-9)
@@ -561,6 +599,16 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
                 const int slot = flag ? s_pslot[a] : s_res_slot[a];
                 base = L.slots + ((size_t)u * 2 * K + slot) * pe;
                 valid = p;
+                if (flag && D.direct && s_isfetch[a]) {
+                    // direct mode: the attention reads this page from the host pool and writes it
+                    // back into its slot (bit 7 of page_valid marks a host row)
+                    const int j = s_sel[a];
+                    page_rows[(size_t)u * D.P_max + i] =
+                        L.host_row0 + (int)((((size_t)b * D.n_page_host + j) * D.n_kv + m) * 2 * p);
+                    page_valid[(size_t)u * D.P_max + i] = (uint8_t)(p | 0x80);
+                    page_dst[(size_t)u * D.P_max + i] = (int)((base - L.arena) / kHeadDim);
+                    continue;
+                }
             } else {
                 const int j = f + (i - n_sp - n_sel);
                 base = L.ring + ((size_t)u * D.R_loc + (j % D.R_loc)) * pe;
@@ -572,12 +620,166 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
         }
         if (tid == 0) page_cnt[u] = total;
     }
-    if (tid == 0) trace_stamp(trace, 1, u, 6);
+    if (tid == 0) trace_stamp(trace, tcls, u, 6);
+}
+
+// One unit per CTA (grid = U), or, for the background select (which = 1), a bounded
+// grid (FREEKV_BG_SELECT_CTAS) striding over the units.
+template <int LPT, int GM>
+__global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D, FkvLayer L,
+                                                                       int32_t* __restrict__ page_rows,
+                                                                       uint8_t* __restrict__ page_valid,
+                                                                       int32_t* __restrict__ page_dst,
+                                                                       int32_t* __restrict__ page_cnt,
+                                                                       unsigned long long* __restrict__ trace,
+                                                                       const float* __restrict__ scores,
+                                                                       const uint16_t* __restrict__ q,
+                                                                       const uint16_t* __restrict__ k_new,
+                                                                       const uint16_t* __restrict__ v_new,
+                                                                       int32_t* __restrict__ pages_out,
+                                                                       uint8_t* __restrict__ corrected_out,
+                                                                       int which) {
+    for (int u = blockIdx.x; u < D.U; u += gridDim.x) {
+        finalize_unit<LPT, GM>(u, D, L, page_rows, page_valid, page_dst, page_cnt, trace, scores, q, k_new, v_new,
+                               pages_out, corrected_out, which);
+        __syncthreads();  // shared state of this unit is dead before the next unit reuses it
+    }
+}
+
+// ------------------------------------------------- pipelined step prologue
+// One CTA per unit, first kernel of a layer's decode step in the pipelined mode
+// (DESIGN.md §5): append this step's token (row a9), the correction check (row
+// a1, CFR-10 -- the same arithmetic as the select kernel's), and, for units that
+// are not corrected, this step's attention page list over the resident set R
+// (speculative units attend the pages selected at step i-1).  The
+// selection of step i then runs off the critical path for those units.
+constexpr int kPrepThreads = 256;
+
+__global__ void __launch_bounds__(kPrepThreads) fkv_prep_kernel(FkvDims D, FkvLayer L, FkvScratch X,
+                                                                const uint16_t* __restrict__ q,
+                                                                const uint16_t* __restrict__ k_new,
+                                                                const uint16_t* __restrict__ v_new,
+                                                                uint8_t* __restrict__ corrected_out) {
+    extern __shared__ __align__(16) uint8_t s_dyn[];  // append staging: one (2, p, d) page
+    __shared__ uint32_t s_qa[kMaxG * kHeadDim / 2], s_qb[kMaxG * kHeadDim / 2];
+    __shared__ float s_cos[kMaxG];
+    __shared__ int s_flag;
+    const int u = blockIdx.x, b = u / D.n_kv, m = u % D.n_kv, G = D.G, tid = threadIdx.x;
+    if (tid == 0) trace_stamp(X.trace, 8, u, 0);
+    // every load of the kernel is issued up front (one round trip)
+    const int L0 = L.ctx[u];
+    int n_off = L.n_off[u];
+    const int res_valid = D.full_refresh ? 0 : L.res_valid[u];
+    const int res_front = L.res_front[u], res_cnt = L.res_cnt[u];
+    const int my_slot = tid < D.K ? L.res_slot[(size_t)u * D.K + tid] : 0;
+    {
+        const uint32_t* qa32 = reinterpret_cast<const uint32_t*>(q + ((size_t)b * D.n_qo + m * G) * kHeadDim);
+        const uint32_t* qb32 = reinterpret_cast<const uint32_t*>(L.q_prev + ((size_t)b * D.n_qo + m * G) * kHeadDim);
+        for (int i = tid; i < G * kHeadDim / 2; i += kPrepThreads) {
+            s_qa[i] = qa32[i];
+            s_qb[i] = qb32[i];
+        }
+    }
+    if (k_new) append_unit(D, L, u, L0, k_new, v_new, 1, reinterpret_cast<uint4*>(s_dyn));
+    const int Lc = L0 + (k_new ? 1 : 0);
+    n_off = max(n_off, frontier_for(D, Lc));
+    __syncthreads();
+    // ---- a1 (CFR-10): head g's cosine, sequential channel sums by thread g
+    if (tid < G) {
+        const uint16_t* qa = reinterpret_cast<const uint16_t*>(s_qa) + tid * kHeadDim;
+        const uint16_t* qb = reinterpret_cast<const uint16_t*>(s_qb) + tid * kHeadDim;
+        float dot = 0.0f, n1 = 0.0f, n2 = 0.0f;
+#pragma unroll 8
+        for (int c = 0; c < kHeadDim; ++c) {
+            const float x = bf16f(qa[c]), y = bf16f(qb[c]);
+            dot = __fmaf_rn(x, y, dot);
+            n1 = __fmaf_rn(x, x, n1);
+            n2 = __fmaf_rn(y, y, n2);
+        }
+        s_cos[tid] = (n1 == 0.0f || n2 == 0.0f) ? 0.0f : __fdiv_rn(dot, __fmul_rn(__fsqrt_rn(n1), __fsqrt_rn(n2)));
+    }
+    __syncthreads();
+    // q_prev := q_i now (q_prev is read only by this check): the background select
+    // of this step reads q_i from here, so the caller's q buffer may be reused at once
+    {
+        uint32_t* qp = reinterpret_cast<uint32_t*>(L.q_prev + ((size_t)b * D.n_qo + m * G) * kHeadDim);
+        for (int i = tid; i < G * kHeadDim / 2; i += kPrepThreads) qp[i] = s_qa[i];
+    }
+    if (tid == 0) {
+        float acc = s_cos[0];
+        for (int g = 1; g < G; ++g) acc = __fadd_rn(acc, s_cos[g]);
+        const float mean = __fdiv_rn(acc, (float)G);
+        int flag;
+        if (D.mode == 1 || D.tau >= 1.0f) flag = 1;
+        else if (D.mode == 2 || D.tau <= 0.0f) flag = 0;
+        else flag = mean < D.tau;
+        if (!res_valid) flag = 1;
+        s_flag = flag;
+        L.flags[u] = (uint8_t)flag;
+        L.cbar[u] = mean;
+        if (corrected_out) corrected_out[u] = (uint8_t)flag;
+        L.ctx[u] = Lc;
+        L.n_off[u] = n_off;
+    }
+    __syncthreads();
+    if (s_flag) {  // corrected: the page list is built by the select kernel from S_i
+        if (tid == 0) trace_stamp(X.trace, 8, u, 1);
+        return;
+    }
+    // ---- page list over R: sink pages, R's slots, local pages [f_R * p, Lc) (reading A-9)
+    const int p = D.p;
+    const int sink_tok = min(D.S_tok, Lc);
+    const int n_sp = (sink_tok + p - 1) / p;
+    const int n_last = (Lc - 1) / p;
+    const int n_loc = (Lc > res_front * p) ? (n_last - res_front + 1) : 0;
+    const int total = n_sp + res_cnt + n_loc;
+    const size_t pe = page_elems(D);
+    if (tid < res_cnt) {  // R's slots (K <= 256 <= kPrepThreads)
+        const uint16_t* base = L.slots + ((size_t)u * 2 * D.K + my_slot) * pe;
+        X.page_rows[(size_t)u * D.P_max + n_sp + tid] = (int)((base - L.arena) / kHeadDim);
+        X.page_valid[(size_t)u * D.P_max + n_sp + tid] = (uint8_t)p;
+    }
+    for (int i = tid; i < total; i += kPrepThreads) {
+        const uint16_t* base;
+        int valid;
+        if (i < n_sp) {
+            base = L.sink + ((size_t)u * D.n_sink + i) * pe;
+            valid = min(p, sink_tok - i * p);
+        } else if (i < n_sp + res_cnt) {
+            continue;
+        } else {
+            const int j = res_front + (i - n_sp - res_cnt);
+            base = L.ring + ((size_t)u * D.R_loc + (j % D.R_loc)) * pe;
+            valid = min(p, Lc - j * p);
+        }
+        X.page_rows[(size_t)u * D.P_max + i] = (int)((base - L.arena) / kHeadDim);
+        X.page_valid[(size_t)u * D.P_max + i] = (uint8_t)valid;
+    }
+    if (tid == 0) {
+        X.page_cnt[u] = total;
+        trace_stamp(X.trace, 8, u, 1);
+    }
+}
+
+cudaError_t launch_prep(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
+                        const uint16_t* k_new, const uint16_t* v_new, uint8_t* corrected_out, cudaStream_t s) {
+    const size_t smem = page_elems(D) * sizeof(uint16_t);
+    static size_t configured = 0;
+    if (smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(fkv_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(fkv_prep_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    fkv_prep_kernel<<<D.U, kPrepThreads, smem, s>>>(D, L, X, q, k_new, v_new, corrected_out);
+    return cudaGetLastError();
 }
 
 template <int G>
 static void launch_score_g(const FkvDims& D, const FkvLayer& L, float* scores, const uint16_t* q, int max_n_off,
-                           int pending, unsigned long long* trace, cudaStream_t s) {
+                           int pending, unsigned long long* trace, int which, cudaStream_t s) {
     const int per_cta = kScoreWarps * 32;
     const int gy = (max_n_off + per_cta - 1) / per_cta;
     if (gy <= 0) return;
@@ -589,20 +791,29 @@ static void launch_score_g(const FkvDims& D, const FkvLayer& L, float* scores, c
                              cudaSharedmemCarveoutMaxShared);
         configured = true;
     }
-    fkv_score_kernel<G><<<dim3(D.U, gy), per_cta, smem, s>>>(D, L, scores, q, pending, trace);
+    // background (which = 1): a bounded grid-stride grid (FREEKV_BG_SCORE_CTAS, default 64) so the
+    // background score leaves most SMs to the attention running beside it
+    static int bg_ctas = 0;
+    if (!bg_ctas) {
+        const char* e = getenv("FREEKV_BG_SCORE_CTAS");
+        bg_ctas = std::max(1, e ? atoi(e) : 64);
+    }
+    const int items = D.U * gy;
+    const int grid = which == 1 ? std::min(items, bg_ctas) : items;
+    fkv_score_kernel<G><<<grid, per_cta, smem, s>>>(D, L, scores, q, pending, trace, which, gy);
 }
 
 cudaError_t launch_score(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                         int max_n_off, int pending, cudaStream_t s) {
+                         int max_n_off, int pending, int which, cudaStream_t s) {
     switch (D.G) {
-        case 1: launch_score_g<1>(D, L, X.scores, q, max_n_off, pending, X.trace, s); break;
-        case 2: launch_score_g<2>(D, L, X.scores, q, max_n_off, pending, X.trace, s); break;
-        case 3: launch_score_g<3>(D, L, X.scores, q, max_n_off, pending, X.trace, s); break;
-        case 4: launch_score_g<4>(D, L, X.scores, q, max_n_off, pending, X.trace, s); break;
-        case 5: launch_score_g<5>(D, L, X.scores, q, max_n_off, pending, X.trace, s); break;
-        case 6: launch_score_g<6>(D, L, X.scores, q, max_n_off, pending, X.trace, s); break;
-        case 7: launch_score_g<7>(D, L, X.scores, q, max_n_off, pending, X.trace, s); break;
-        case 8: launch_score_g<8>(D, L, X.scores, q, max_n_off, pending, X.trace, s); break;
+        case 1: launch_score_g<1>(D, L, X.scores, q, max_n_off, pending, X.trace, which, s); break;
+        case 2: launch_score_g<2>(D, L, X.scores, q, max_n_off, pending, X.trace, which, s); break;
+        case 3: launch_score_g<3>(D, L, X.scores, q, max_n_off, pending, X.trace, which, s); break;
+        case 4: launch_score_g<4>(D, L, X.scores, q, max_n_off, pending, X.trace, which, s); break;
+        case 5: launch_score_g<5>(D, L, X.scores, q, max_n_off, pending, X.trace, which, s); break;
+        case 6: launch_score_g<6>(D, L, X.scores, q, max_n_off, pending, X.trace, which, s); break;
+        case 7: launch_score_g<7>(D, L, X.scores, q, max_n_off, pending, X.trace, which, s); break;
+        case 8: launch_score_g<8>(D, L, X.scores, q, max_n_off, pending, X.trace, which, s); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -612,7 +823,7 @@ cudaError_t launch_score(const FkvDims& D, const FkvLayer& L, const FkvScratch& 
 template <int LPT, int GM>
 static cudaError_t launch_fin_g(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                                 const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
-                                uint8_t* corrected_out, size_t smem, bool pdl, cudaStream_t s) {
+                                uint8_t* corrected_out, size_t smem, bool pdl, int which, cudaStream_t s) {
     static size_t configured = 0;
     if (smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(fkv_select_finalize_kernel<LPT, GM>,
@@ -623,19 +834,25 @@ static cudaError_t launch_fin_g(const FkvDims& D, const FkvLayer& L, const FkvSc
         if (e != cudaSuccess) return e;
         configured = smem;
     }
-    return launch_ex(fkv_select_finalize_kernel<LPT, GM>, dim3(D.U), dim3(kThreads), smem, s, pdl, D, L, X.page_rows,
-                     X.page_valid, X.page_cnt, X.trace, (const float*)X.scores, q, k_new, v_new, pages_out,
-                     corrected_out);
+    static int bg_ctas = 0;
+    if (!bg_ctas) {
+        const char* e = getenv("FREEKV_BG_SELECT_CTAS");
+        bg_ctas = std::max(1, e ? atoi(e) : 32);
+    }
+    const int grid = which == 1 ? std::min(D.U, bg_ctas) : D.U;
+    return launch_ex(fkv_select_finalize_kernel<LPT, GM>, dim3(grid), dim3(kThreads), smem, s, pdl, D, L, X.page_rows,
+                     X.page_valid, X.page_dst, X.page_cnt, X.trace, (const float*)X.scores, q, k_new, v_new, pages_out,
+                     corrected_out, which);
 }
 
 template <int LPT>
 static cudaError_t launch_fin(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                               const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
-                              uint8_t* corrected_out, size_t smem, bool pdl, cudaStream_t s) {
-    if (D.G <= 1) return launch_fin_g<LPT, 1>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, s);
-    if (D.G <= 2) return launch_fin_g<LPT, 2>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, s);
-    if (D.G <= 4) return launch_fin_g<LPT, 4>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, s);
-    return launch_fin_g<LPT, 8>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, s);
+                              uint8_t* corrected_out, size_t smem, bool pdl, int which, cudaStream_t s) {
+    if (D.G <= 1) return launch_fin_g<LPT, 1>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
+    if (D.G <= 2) return launch_fin_g<LPT, 2>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
+    if (D.G <= 4) return launch_fin_g<LPT, 4>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
+    return launch_fin_g<LPT, 8>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
 }
 
 // lpt = leaves per thread of the kThreads-thread tree; kThreads * lpt >= next_pow2(n_off) for every n_off the
@@ -643,13 +860,14 @@ static cudaError_t launch_fin(const FkvDims& D, const FkvLayer& L, const FkvScra
 // this step's single-token append (row a9) into the kernel.
 cudaError_t launch_finalize(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                             const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
-                            uint8_t* corrected_out, int lpt, bool pdl, cudaStream_t s) {
+                            uint8_t* corrected_out, int lpt, bool pdl, int which, cudaStream_t s) {
     const size_t smem = page_elems(D) * sizeof(uint16_t) + (size_t)D.G * D.n_page_max * sizeof(float);
     switch (lpt) {
-        case 1: return launch_fin<1>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, s);
-        case 2: return launch_fin<2>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, s);
-        case 4: return launch_fin<4>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, s);
-        case 8: return launch_fin<8>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, s);
+        case 1: return launch_fin<1>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
+        case 2: return launch_fin<2>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
+        case 4: return launch_fin<4>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
+        case 8: return launch_fin<8>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
+        case 16: return launch_fin<16>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
         default: return cudaErrorInvalidValue;
     }
 }

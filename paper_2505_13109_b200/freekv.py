@@ -26,7 +26,8 @@ EXPORTED = [
     "freekv_last_error", "freekv_abi_version", "freekv_profile_begin", "freekv_profile_end",
     "freekv_step_graph_capture", "freekv_step_graph_launch", "freekv_step_graph_profile", "freekv_debug_trace",
 ]
-KERNEL_CLASSES = ["append", "score", "select_finalize", "recall_sync", "recall_bg", "attn_split", "attn_combine"]
+KERNEL_CLASSES = ["append", "score", "select_finalize", "recall_sync", "recall_bg", "attn_split", "attn_combine",
+                  "attn_split_phase2", "prep", "score_bg", "select_finalize_bg"]
 
 
 class FreeKVError(RuntimeError):
@@ -176,8 +177,9 @@ class FreeKV:
         if host_pool is None:
             host_pool = torch.empty(self.host_bytes, dtype=torch.uint8, pin_memory=True)
         self.host = host_pool
-        self.stream = compute_stream if compute_stream is not None else torch.cuda.Stream(self.device)
-        self.recall_stream = torch.cuda.Stream(self.device)
+        # the decode path outranks the background recall when SMs are contended
+        self.stream = compute_stream if compute_stream is not None else torch.cuda.Stream(self.device, priority=-1)
+        self.recall_stream = torch.cuda.Stream(self.device, priority=0)
         bufs = _Buffers(self.dev.data_ptr(), self.dev_bytes, self.host.data_ptr(), self.host_bytes)
         h = ctypes.c_void_p()
         c = cfg.to_c()
@@ -243,8 +245,8 @@ class FreeKV:
         return {c: (float(ms[i]), int(n[i])) for i, c in enumerate(KERNEL_CLASSES)}
 
     def debug_trace(self):
-        """[8][4096][8] uint64 %globaltimer stamps (ns) of the kernels since the last call."""
-        out = np.zeros((8, 4096, 8), np.uint64)
+        """[12][4096][8] uint64 %globaltimer stamps (ns) of the kernels since the last call."""
+        out = np.zeros((12, 4096, 8), np.uint64)
         _check(self.L.freekv_debug_trace(self.h, _np_ptr(out), out.size))
         return out
 

@@ -31,7 +31,7 @@ def rel_err(out, ref):
 
 def run_parity(G=4, n_kv=2, batch=2, page=32, sink=64, window=64, budget=256, L0=700, steps=6,
                n_layers=2, tau=0.8, mode=O.MODE_SPECULATIVE, event_rate=0.3, seed=11, tie_pages=False,
-               check_summaries=True, use_primitives=False):
+               check_summaries=True, use_primitives=False, check_fetch=True):
     _need_gpu()
     import paper_2505_13109_b200 as P
     d = 128
@@ -86,7 +86,7 @@ def run_parity(G=4, n_kv=2, batch=2, page=32, sink=64, window=64, budget=256, L0
                 assert np.array_equal(pages_out.cpu().numpy().reshape(-1, cfg.K), ref["sel"])
                 assert np.array_equal(corr_out.cpu().numpy().reshape(-1), ref["flags"])
             n_fetch, fetch_pages = fkv.get_fetch(layer)
-            for u in range(fkv.U):
+            for u in range(fkv.U if check_fetch else 0):
                 exp = ref["fetch_sync"][u] if ref["flags"][u] else ref["fetch_bg"][u]
                 assert list(fetch_pages[u, :n_fetch[u]]) == exp, (i, layer, u)
             e = rel_err(out.cpu().numpy().astype(np.float64), ref["out"])
@@ -209,3 +209,30 @@ def test_parity_fused_cluster_select(select_impl, monkeypatch):
 def test_parity_without_pdl(monkeypatch):
     monkeypatch.setenv("FREEKV_PDL", "0")
     run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=4)
+
+
+def test_parity_recall_mode(monkeypatch):
+    """FREEKV_CORR=recall: synchronous recall of the corrected units before a second
+    attention phase (instead of the attention reading their pages from the host pool)."""
+    monkeypatch.setenv("FREEKV_CORR", "recall")
+    run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=5)
+    run_parity(G=4, n_kv=2, batch=1, page=32, L0=900, steps=4, use_primitives=True)
+
+
+def test_parity_full_refresh_direct(monkeypatch):
+    """Every unit re-fetches all K pages every step (FREEKV_DEBUG_FULL_REFRESH): all pages of
+    every unit are read by the attention kernel from the host pool and written back."""
+    monkeypatch.setenv("FREEKV_DEBUG_FULL_REFRESH", "1")
+    run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=4, mode=O.MODE_ALWAYS, check_fetch=False)
+
+
+def test_parity_not_pipelined(monkeypatch):
+    """FREEKV_PIPELINE=0: selection of every unit before the attention (one select launch
+    per layer, corrected units' pages read from the host pool in the same attention)."""
+    monkeypatch.setenv("FREEKV_PIPELINE", "0")
+    run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=5)
+
+
+def test_parity_window_zero_pipelined():
+    """W = 0: the page completed by this step's token is a candidate at once (append first)."""
+    run_parity(G=4, n_kv=2, batch=1, page=32, sink=64, window=0, budget=256, L0=1000, steps=40, n_layers=1)

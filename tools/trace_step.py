@@ -17,7 +17,8 @@ for l in range(L):
     torch.cuda.synchronize()
     fkv.append_kv(l, k, v)
 fkv.synchronize()
-qps = [synth.QueryProcess(nb, nq, nk, d, seed, l, device=dev, event_rate=0.05) for l in range(L)]
+qps = [synth.QueryProcess(nb, nq, nk, d, seed, l, device=dev, event_rate=float(os.environ.get("FKV_EVENT_RATE", "0.05")))
+       for l in range(L)]
 out = torch.empty(nb, nq, d, dtype=torch.float32, device=dev)
 GRAPH = "--graph" in sys.argv
 if GRAPH:
@@ -25,7 +26,8 @@ if GRAPH:
     kb = torch.empty(L, nb, 1, nk, d, dtype=torch.bfloat16, device=dev)
     vb = torch.empty_like(kb)
     ob = torch.empty(L, nb, nq, d, dtype=torch.float32, device=dev)
-names = {0: "score", 1: "finalize", 2: "recall_sync", 3: "recall_bg", 5: "attn_phase1", 6: "attn_phase2", 7: "combine"}
+names = {0: "score", 1: "finalize", 2: "recall_sync", 3: "recall_bg", 4: "attn", 5: "attn_phase1", 6: "attn_phase2",
+         7: "combine", 8: "prep", 9: "score_bg", 10: "finalize_bg"}
 res = {}
 def steps():
     for i in range(12):
