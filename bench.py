@@ -58,60 +58,64 @@ def parse():
 
 # --------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock and clock-event (throttle) reasons sampled every ~2 ms through NVML during
+    the timed region (nvidia-smi as a fallback when NVML is unavailable)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    NAMES = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+             "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+             "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+             "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
+             "hw_power_brake_slowdown": "nvmlClocksEventReasonHwPowerBrakeSlowdown"}
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
-        self.proc = None
-        self.lines = []
+        self.samples = []  # (sm_mhz, reasons bitmask)
+        self.active = False
+        self.stop_flag = False
+        self.err = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(self.idx)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._loop, daemon=True)
             self.thread.start()
-        except Exception:
-            self.proc = None
+        except Exception as e:  # noqa: BLE001
+            self.err = f"nvml unavailable: {e}"
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _loop(self):
+        N = self.N
+        while not self.stop_flag:
+            if self.active:
+                try:
+                    sm = N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)
+                    rs = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                    self.samples.append((sm, rs))
+                except Exception as e:  # noqa: BLE001
+                    self.err = str(e)
+            time.sleep(0.002)
 
     def mark(self):
-        """Start of the timed region: later samples are the ones reported (if any arrive)."""
-        self.first = len(self.lines)
+        """Start of the timed region."""
+        self.active = True
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        lines = self.lines[getattr(self, "first", 0):] or self.lines
-        for ln in lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax.append(float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[4:8]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        self.active = False
+        self.stop_flag = True
+        if self.err and not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err]}
+        reasons = set()
+        for _, rs in self.samples:
+            for name, attr in self.NAMES.items():
+                bit = getattr(self.N, attr, 0)
+                if bit and (rs & bit):
+                    reasons.add(name)
+        sm = [x for x, _ in self.samples]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvml"}
 
 
 # ----------------------------------------------------------------- workload
@@ -161,7 +165,7 @@ def run_ours(args, c, rank, world, local_rank):
     b0, b1 = sh.batch_begin, sh.batch_end
     nb_loc = sh.batch
     n_layers = c["n_layers"]
-    total_steps = args.warmup + 1 + args.steps + args.profile_steps + args.steps  # warm, timed, profiled, e2e
+    total_steps = args.warmup + 1 + args.steps + 2 * args.profile_steps + args.steps  # warm, timed, profiled x2, e2e
     max_ctx = c["ctx"] + total_steps + 1
     stream = torch.cuda.Stream(dev, priority=-1)  # compute outranks the background recall stream
     t0 = time.time()
@@ -226,9 +230,6 @@ def run_ours(args, c, rank, world, local_rank):
 
     clocks = ClockSampler(local_rank)
     clocks.start()
-    t_wait = time.time()
-    while not clocks.lines and time.time() - t_wait < 3.0:  # let nvidia-smi start sampling
-        time.sleep(0.05)
     step = 0
     for _ in range(args.warmup):
         one_step(step)
@@ -259,22 +260,19 @@ def run_ours(args, c, rank, world, local_rank):
         t = torch.tensor([ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    # ---- profiled pass: per-kernel device time (CUDA events captured as graph nodes on the
-    # stream each kernel is launched on) + recall / correction statistics
+    # ---- profiled passes.  (a) roofline: the step graph re-captured with an event-record
+    # node pair around every attention-split kernel only (the dominant kernel; the other
+    # kernels keep their PDL edges), so each bracketed interval is that launch's device time
+    # on the stream it runs on; (b) per-kernel table: every kernel bracketed (event nodes
+    # then break every PDL overlap, so these are per-kernel durations, not the critical
+    # path -- that is the timed region above).  Eager mode: the library's event profiler.
     import paper_2505_13109_b200.freekv as FK
-    prof = {kc: [0.0, 0] for kc in FK.KERNEL_CLASSES}
-    if not args.eager:
-        fkv.step_graph_capture(q_buf, k_buf, v_buf, o_buf, profile=True)
-    else:
-        fkv.profile_begin(args.profile_steps * n_layers * 8 + 64)
+    cls = {k: i for i, k in enumerate(FK.KERNEL_CLASSES)}
     fetched = flagged = units = t_unit_tokens = j_pages = 0
     t_tok_p1 = t_tok_p2 = units_p1 = 0
-    for _ in range(args.profile_steps):
-        run(step)
-        if not args.eager:
-            for kc, (t, n) in fkv.step_graph_profile().items():
-                prof[kc][0] += t
-                prof[kc][1] += n
+
+    def sel_stats():
+        nonlocal fetched, flagged, units, t_unit_tokens, j_pages, t_tok_p1, t_tok_p2, units_p1
         for layer in range(n_layers):
             n_fetch, _ = fkv.get_fetch(layer)
             sel = fkv.get_selection(layer)
@@ -293,12 +291,36 @@ def run_ours(args, c, rank, world, local_rank):
             t_tok_p2 += int(tu[fl].sum())
             units_p1 += int((~fl).sum())
             j_pages += fkv.U * (n_off - c["sink"] // p)
-        step += 1
-    if args.eager:
-        prof = {k: list(v) for k, v in fkv.profile_end().items()}
-    else:
-        fkv.step_graph_capture(q_buf, k_buf, v_buf, o_buf, profile=False)
-    prof = {k: tuple(v) for k, v in prof.items()}
+
+    def profiled(mask):
+        nonlocal step
+        acc = {k: [0.0, 0] for k in FK.KERNEL_CLASSES}
+        if args.eager:
+            fkv.synchronize()
+            fkv.profile_begin(args.profile_steps * n_layers * 12 + 64)
+        else:
+            fkv.step_graph_capture(q_buf, k_buf, v_buf, o_buf, profile=mask)
+        for _ in range(args.profile_steps):
+            if args.eager:
+                with torch.cuda.stream(stream):
+                    torch.cuda._sleep(4_000_000)  # host runs ahead: events bracket kernels, not launch gaps
+            run(step)
+            fkv.synchronize()
+            if not args.eager:
+                for kc, (t, n) in fkv.step_graph_profile().items():
+                    acc[kc][0] += t
+                    acc[kc][1] += n
+            if mask != 1:
+                sel_stats()
+            step += 1
+        if args.eager:
+            acc = {k: list(v) for k, v in fkv.profile_end().items()}
+        return {k: tuple(v) for k, v in acc.items()}
+
+    roof_prof = profiled((1 << cls["attn_split"]) | (1 << cls["attn_split_phase2"]))
+    prof = profiled(1)
+    if not args.eager:  # plain graph again for the end-to-end pass
+        fkv.step_graph_capture(q_buf, k_buf, v_buf, o_buf)
     # ---- end-to-end pass: inputs from pinned host memory, outputs back to host, every step
     Qh = Qs[step:step + args.steps].cpu().pin_memory()
     Kh = Ks[step:step + args.steps].cpu().pin_memory()
@@ -332,7 +354,7 @@ def run_ours(args, c, rank, world, local_rank):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_e2e = float(t.item())
     link = host_link_peak(torch) if rank == 0 else None
-    res = dict(ms=ms, ms_e2e=ms_e2e, prof=prof, fetched=fetched, flagged=flagged, units=units,
+    res = dict(ms=ms, ms_e2e=ms_e2e, prof=prof, roof_prof=roof_prof, fetched=fetched, flagged=flagged, units=units,
                t_unit_tokens=t_unit_tokens, j_pages=j_pages, t_tok_p1=t_tok_p1, t_tok_p2=t_tok_p2, units_p1=units_p1, clocks=clk, link=link, t_alloc=t_alloc,
                t_prefill=t_prefill, h2d=h2d, d2h=d2h, K=K, G=G, kv_loc=kv_loc, nb_loc=nb_loc, seed=seed)
     fkv.close()
@@ -416,13 +438,17 @@ def main():
     d = 128
     G = r["G"]
     units_per_launch = r["nb_loc"] * r["kv_loc"]
-    # algorithmic bytes: attention reads |T|*2*d*2 B KV + G*d*2 B q per unit
-    # dominant kernel: attention phase 1 (units whose pages are resident, ~95% of the bytes);
-    # algorithmic bytes per launch = sum over its units of |T|*2*d*2 (KV) + G*d*2 (q)
-    attn_ms, attn_n = prof["attn_split"]
-    attn_bytes = r["t_tok_p1"] * 2 * d * 2 + r["units_p1"] * G * d * 2
+    # algorithmic bytes: attention reads |T|*2*d*2 B KV + G*d*2 B q per unit.
+    # Dominant kernel: the attention split kernel.  One launch attends every unit (corrected
+    # units read their fetched pages from the host pool in the same launch); in the two-phase
+    # modes its first launch covers the units with resident pages and phase 2 the others.
+    attn_ms, attn_n = r["roof_prof"]["attn_split"]
+    p2_ms, p2_n = r["roof_prof"]["attn_split_phase2"]
+    two_phase = p2_n > 0
+    tok1 = r["t_tok_p1"] if two_phase else r["t_unit_tokens"]
+    units1 = r["units_p1"] if two_phase else r["units"]
+    attn_bytes = tok1 * 2 * d * 2 + units1 * G * d * 2
     attn_gbs = attn_bytes / (attn_ms / 1e3) / 1e9 if attn_ms > 0 else 0.0
-    p2_ms, p2_n = prof["attn_split_phase2"]
     p2_bytes = r["t_tok_p2"] * 2 * d * 2
     sc_ms, sc_n = prof["score"]
     sc_bytes = r["j_pages"] * 2 * d * 2 + sc_n * units_per_launch * G * d * 2
@@ -432,17 +458,21 @@ def main():
     rec_gbs = rec_bytes / (rec_ms / 1e3) / 1e9 if rec_ms > 0 else 0.0
     kernels = {k: {"ms_total": round(v[0], 4), "launches": v[1],
                    "us_avg": round(v[0] / v[1] * 1e3, 3) if v[1] else None} for k, v in prof.items()}
-    dominant = "attn_split" if attn_ms >= sc_ms else "score"
-    if dominant == "attn_split":
-        roof = {"kernel": "fkv_attn_split_kernel phase 1 (units with resident pages)", "bound": "hbm",
-                "achieved": round(attn_gbs, 1), "peak": hbm_peak,
-                "unit": "GB/s", "frac": round(attn_gbs / hbm_peak, 4), "traffic": None,
-                "algorithmic_bytes_per_launch": int(attn_bytes / max(attn_n, 1)),
-                "us_per_launch": round(attn_ms / max(attn_n, 1) * 1e3, 2)}
-    else:
-        roof = {"kernel": "fkv_score_kernel", "bound": "hbm", "achieved": round(sc_gbs, 1), "peak": hbm_peak,
-                "unit": "GB/s", "frac": round(sc_gbs / hbm_peak, 4), "traffic": None,
-                "algorithmic_bytes_per_launch": int(sc_bytes / max(sc_n, 1))}
+    # DRAM bytes per launch of the attention kernel from the committed ncu --set full capture
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "attn_traffic.json")
+    if os.path.exists(tp):
+        try:
+            tj = _j.load(open(tp))
+            if tj.get("workload") == c["workload"]:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:  # noqa: BLE001
+            traffic = None
+    roof = {"kernel": "fkv_attn_split_kernel" + (" phase 1" if two_phase else " (all units)"), "bound": "hbm",
+            "achieved": round(attn_gbs, 1), "peak": hbm_peak, "unit": "GB/s", "frac": round(attn_gbs / hbm_peak, 4),
+            "traffic": traffic, "algorithmic_bytes_per_launch": int(attn_bytes / max(attn_n, 1)),
+            "us_per_launch": round(attn_ms / max(attn_n, 1) * 1e3, 2),
+            "timing": "event-record graph nodes around each attention launch on its stream (DESIGN.md §7)"}
     line = {
         "metric": METRIC, "value": round(tok_s, 2), "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(r["ms"] / args.steps, 4),
@@ -450,8 +480,8 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16 KV/q, fp32 scores+accumulate, fp32 out",
         "data": "synthetic (GEN-S keys with hot pages, GEN-Q AR(1) queries, seeded)", "config": cfg_out,
         "roofline": roof,
-        "attention_phase2": {"us_per_launch": round(p2_ms / max(p2_n, 1) * 1e3, 2),
-                             "algorithmic_bytes_per_launch": int(p2_bytes / max(p2_n, 1))},
+        "attention_phase2": ({"us_per_launch": round(p2_ms / max(p2_n, 1) * 1e3, 2),
+                              "algorithmic_bytes_per_launch": int(p2_bytes / max(p2_n, 1))} if two_phase else None),
         "scoring_hbm": {"achieved": round(sc_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
                         "frac": round(sc_gbs / hbm_peak, 4)},
         "recall": {"achieved_gbs": round(rec_gbs, 2), "host_link_peak_gbs": round(r["link"], 2) if r["link"] else None,
@@ -463,6 +493,7 @@ def main():
         "e2e": {"value": round(tok_s_e2e, 2), "unit": "tokens/s", "h2d_bytes_per_step": r["h2d"],
                 "d2h_bytes_per_step": r["d2h"]},
         "gpu_launches": int(sum(v[1] for v in prof.values()) / max(args.profile_steps, 1) * args.steps),
+        "gpu_launches_per_step": int(sum(v[1] for v in prof.values()) / max(args.profile_steps, 1)),
         "execution": "eager per-layer C-ABI calls" if args.eager else "whole-step CUDA graphs (compute + recall)",
         "clocks": r["clocks"],
         "setup_s": {"alloc_pin": round(r["t_alloc"], 1), "prefill": round(r["t_prefill"], 1)},

@@ -44,7 +44,7 @@ enum {
     FREEKV_ENCCL = -4,         /* reserved: collective failure */
     FREEKV_ESTATE = -5,        /* call out of order / handle in wrong state */
     FREEKV_ERANGE = -6,        /* context would exceed max_ctx_tokens */
-    FREEKV_EUNSUPPORTED = -7   /* head_dim != 128, page_size not in {16,32,64}, G > 8 */
+    FREEKV_EUNSUPPORTED = -7   /* head_dim != 128, page_size not in {16,32,64}, G > 8, batch*n_kv > 4096 */
 };
 
 /* Correction modes, P:661-665 (Table tab:abl-tau): tau = 0 "No Correction",
@@ -140,18 +140,22 @@ freekv_status freekv_decode_step(freekv_handle* h, int32_t layer, const void* q,
 /* Whole-step CUDA graphs: capture one decode step of every layer (the same
  * sequence as n_layers freekv_decode_step calls) with fixed device buffers
  * q_all [n_layers][nb][n_qo][d], k_all / v_all [n_layers][nb][1][n_kv][d]
- * (bf16) and out_all [n_layers][nb][n_qo][d] (fp32).  The compute-stream part
- * and the background-recall part are two graphs joined by external event
- * nodes (recall of layer l waits for its selection; step i+1's layer l waits
- * for step i's recall of layer l), so background recall keeps overlapping the
- * next layers and the next step exactly as in the eager path.  Kernel
- * arguments read all step-varying state from device memory, so one capture
- * replays for every later step.  step_graph_launch replays one step on the
- * handle's streams (ERANGE when the context would exceed max_ctx_tokens). */
+ * (bf16) and out_all [n_layers][nb][n_qo][d] (fp32).  In direct mode (default)
+ * each layer's background recall is a forked branch of the one step graph,
+ * joined at its end; in recall mode (FREEKV_CORR=recall) the compute-stream part
+ * and the background-recall part are two graphs joined by external event nodes
+ * (recall of layer l waits for its synchronous recall; step i+1's layer l waits
+ * for step i's recall of layer l).  Kernel arguments read all step-varying state
+ * from device memory, so one capture replays for every later step.
+ * step_graph_launch replays one step on the handle's streams (ERANGE when the
+ * context would exceed max_ctx_tokens).
+ * profile: 0 = none; 1 = an event-record node pair around every kernel node;
+ * otherwise a bit mask (bit c = kernel class c, see freekv_profile_end) of the
+ * classes to bracket -- fewer event nodes disturb the step less. */
 freekv_status freekv_step_graph_capture(freekv_handle* h, const void* q_all, const void* k_all,
                                         const void* v_all, float* out_all, int32_t profile);
 freekv_status freekv_step_graph_launch(freekv_handle* h);
-/* With profile != 0 at capture, every kernel node is bracketed by event-record
+/* With profile != 0 at capture, the selected kernel nodes are bracketed by event-record
  * nodes; after a replay has completed, this returns per kernel class the summed
  * device milliseconds and launch counts of that replay (classes as in
  * freekv_profile_end).  Blocking. */
@@ -186,7 +190,7 @@ freekv_status freekv_profile_begin(freekv_handle* h, int32_t max_launches);
 freekv_status freekv_profile_end(freekv_handle* h, float* ms /*[11]*/, int32_t* launches /*[11]*/);
 
 /* Diagnostics: with FREEKV_TRACE=1 in the environment at freekv_init, kernels write
- * %globaltimer stamps [class 8][entity 4096][stamp 8] (ns); this copies n <= 262144
+ * %globaltimer stamps [class 12][entity 4096][stamp 8] (ns); this copies n <= 393216
  * of them to host memory `out` and clears the buffer.  Blocking. */
 freekv_status freekv_debug_trace(freekv_handle* h, uint64_t* out, size_t n);
 

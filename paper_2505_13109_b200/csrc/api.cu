@@ -52,17 +52,18 @@ struct freekv_handle {
     cudaStream_t cs = nullptr, rs = nullptr;
     cudaStream_t ss = nullptr;  // library-owned high-priority stream for the synchronous recall
     std::vector<cudaEvent_t> ev_select, ev_recall, ev_sync, ev_sync_x, ev_pre, ev_fl;
-    FkvScratch Xb;               // scratch of the background select (own score buffer)
-    bool pipelined = true;       // pipelined step (FREEKV_PIPELINE=0 disables; needs direct mode)
+    bool pipelined = false;      // overlapped step (FREEKV_PIPELINE=1; needs direct mode)
+    bool one_graph = false;      // direct mode: recalls are forked branches of the one step graph
     std::vector<int> ctx_host;
     std::vector<int> recall_pending;
-    int lpt = 1;  // leaves per thread of the finalize tree (fixed per handle, CFR-6)
+    int lpt = 1, lpt1k = 1;  // leaves per thread of the 512 / 1024-thread select tree (fixed per handle, CFR-6)
     int sel_cluster = 8, sel_lptm = 1;  // fused select: CTAs per unit, max leaves per thread
     bool fused_select = false;          // FREEKV_SELECT=fused selects the one-launch cluster kernel
     bool pdl = true;                    // programmatic dependent launch (FREEKV_PDL=0 disables)
     bool serial_recall = false;  // diagnostics: FREEKV_SERIAL_RECALL=1 runs background recall on the compute stream
     // profiling (freekv_profile_begin/end)
     bool prof = false;
+    uint32_t prof_mask = ~0u;  // kernel classes bracketed by events while profiling
     std::vector<cudaEvent_t> prof_pool;
     size_t prof_used = 0;
     struct Rec { int cls; cudaEvent_t a, b; };
@@ -77,7 +78,6 @@ namespace {
 
 constexpr size_t kAlign = 256;
 constexpr int kMaxAttnWarps = 148 * 16;
-constexpr int kFinalizeThreads = 512;  // must match select.cu kThreads  // partial-record capacity; the grid uses min(resident warps, this)
 size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
 
 struct Sizes {
@@ -87,7 +87,7 @@ struct Sizes {
         o_pend_cnt,
         o_pend_pages, o_pend_slot, o_pend_front, o_flags, o_cbar, o_fetch_page, o_fetch_slot, o_n_fetch, o_ctx,
         o_n_off;
-    size_t o_scores, o_scores_bg, o_part_o, o_part_ml, o_page_rows, o_page_cnt, o_page_valid, o_page_dst;
+    size_t o_scores, o_part_o, o_part_ml, o_page_rows, o_page_cnt, o_page_valid, o_page_dst;
 };
 
 freekv_status validate(const freekv_config* c, FkvDims* D) {
@@ -118,6 +118,7 @@ freekv_status validate(const freekv_config* c, FkvDims* D) {
     if (!(c->mode == 0 || c->mode == 1 || c->mode == 2)) return fail(FREEKV_EINVAL, "mode must be 0, 1 or 2");
     if (!std::isfinite(c->tau)) return fail(FREEKV_EINVAL, "tau must be finite");
     if (c->first_layer_dense) return fail(FREEKV_EUNSUPPORTED, "first_layer_dense is not served by ABI v1");
+    if ((long long)c->batch * c->n_kv > 4096) return fail(FREEKV_EUNSUPPORTED, "batch * n_kv must be <= 4096");
     FkvDims d{};
     d.nb = c->batch;
     d.n_qo = c->n_qo;
@@ -177,7 +178,6 @@ Sizes compute_sizes(const freekv_config* c, const FkvDims& D) {
     s.layer_bytes = o;
     o = 0;
     s.o_scores = take(U * D.G * D.n_page_max * 4);
-    s.o_scores_bg = take(U * D.G * D.n_page_max * 4);
     s.o_part_o = take((size_t)4 * kMaxAttnWarps * D.G * D.d * 4);
     s.o_part_ml = take((size_t)4 * kMaxAttnWarps * D.G * 2 * 4);
     s.o_page_rows = take(U * D.P_max * 4);
@@ -206,7 +206,7 @@ enum { K_APPEND = 0, K_SCORE, K_FINALIZE, K_RECALL_SYNC, K_RECALL_BG, K_ATTN_SPL
 
 template <class F>
 cudaError_t timed(freekv_handle* h, int cls, cudaStream_t s, F&& launch) {
-    if (!h->prof || h->prof_used + 2 > h->prof_pool.size()) return launch();
+    if (!h->prof || !((h->prof_mask >> cls) & 1u) || h->prof_used + 2 > h->prof_pool.size()) return launch();
     cudaEvent_t a = h->prof_pool[h->prof_used++], b = h->prof_pool[h->prof_used++];
     // under stream capture only "external" records become real event-record graph nodes
     const unsigned fl = h->capturing ? cudaEventRecordExternal : 0u;
@@ -238,8 +238,10 @@ freekv_status do_select(freekv_handle* h, int layer, const void* q, int32_t* pag
     if (!q) return fail(FREEKV_EINVAL, "q is NULL");
     const int pending = k_new ? 1 : 0;
     if (h->ctx_host[layer] + pending <= 0) return fail(FREEKV_ESTATE, "select before any token was appended");
-    // the background recall of the previous step reads this layer's fetch list
-    if (h->capturing)
+    // the background recall of the previous step reads this layer's fetch list (one-graph
+    // capture: the previous graph launch, which joins its recalls, has completed)
+    if (h->capturing && h->one_graph) {
+    } else if (h->capturing)
         FKV_CUDA(cudaStreamWaitEvent(s, h->ev_recall[layer], cudaEventWaitExternal));
     else if (h->recall_pending[layer])
         FKV_CUDA(cudaStreamWaitEvent(s, h->ev_recall[layer], 0));
@@ -253,11 +255,11 @@ freekv_status do_select(freekv_handle* h, int layer, const void* q, int32_t* pag
             h->capturing ? max_n_off(h->D, h->D.max_ctx) : max_n_off(h->D, h->ctx_host[layer] + pending);
         if (h->capturing || mno - h->D.n_sink > h->D.K)
             FKV_CUDA(timed(h, K_SCORE, s, [&] {
-                return launch_score(h->D, h->layers[layer], h->X, (const uint16_t*)q, mno, pending, 0, s);
+                return launch_score(h->D, h->layers[layer], h->X, (const uint16_t*)q, mno, pending, 0, h->pdl, s);
             }));
         FKV_CUDA(timed(h, K_FINALIZE, s, [&] {
             return launch_finalize(h->D, h->layers[layer], h->X, (const uint16_t*)q, (const uint16_t*)k_new,
-                                   (const uint16_t*)v_new, pages_out, corr_out, h->lpt, h->pdl, 0, s);
+                                   (const uint16_t*)v_new, pages_out, corr_out, h->lpt1k, 1024, h->pdl, 0, s);
         }));
     }
     if (k_new && !h->capturing) h->ctx_host[layer] += 1;
@@ -320,7 +322,16 @@ freekv_status do_step_tail(freekv_handle* h, int layer, const void* q, float* ou
         // the background recall of this layer starts after its attention (an event node between
         // select and attention would break their PDL edge, and the host link is then free for
         // the attention's own host reads); it overlaps the next layers
-        if (h->capturing) {
+        if (h->serial_recall) {  // diagnostics: no overlap at all
+            FKV_CUDA(timed(h, K_RECALL_BG, cs, [&] { return launch_recall(D, L, 0, cs, h->X.trace); }));
+            FKV_CUDA(cudaEventRecord(h->ev_recall[layer], cs));
+            if (!h->capturing) h->recall_pending[layer] = 1;
+        } else if (h->capturing && h->one_graph) {  // forked branch of the step graph, joined at its end
+            FKV_CUDA(cudaEventRecord(h->ev_select[layer], cs));
+            FKV_CUDA(cudaStreamWaitEvent(h->rs, h->ev_select[layer], 0));
+            FKV_CUDA(timed(h, K_RECALL_BG, h->rs, [&] { return launch_recall(D, L, 0, h->rs, h->X.trace); }));
+            FKV_CUDA(cudaEventRecord(h->ev_recall[layer], h->rs));
+        } else if (h->capturing) {
             FKV_CUDA(cudaEventRecordWithFlags(h->ev_select[layer], cs, cudaEventRecordExternal));
         } else if (h->serial_recall) {
             FKV_CUDA(timed(h, K_RECALL_BG, cs, [&] { return launch_recall(D, L, 0, cs, h->X.trace); }));
@@ -363,84 +374,57 @@ freekv_status do_step_tail(freekv_handle* h, int layer, const void* q, float* ou
     return FREEKV_OK;
 }
 
-// Background half of the pipelined step of one layer (rs): select S_i for the units
-// that attended their resident set (score + select, which = 1; the select kernel
-// commits R := S_i, q_prev := q_i for them), then recall S_i \ R into free slots
-// for step i+1.  Nothing of the current step waits on it.
-cudaError_t bg_chain(freekv_handle* h, int layer, cudaStream_t s) {
-    const FkvDims& D = h->D;
-    FkvLayer& L = h->layers[layer];
-    const uint16_t* q = L.q_prev;  // q_i, stored there by this step's prep kernel
-    const int mno = h->capturing ? max_n_off(D, D.max_ctx) : max_n_off(D, h->ctx_host[layer]);
-    cudaError_t e = cudaSuccess;
-    if (h->capturing || mno - D.n_sink > D.K)
-        e = timed(h, K_SCORE_BG, s, [&] { return launch_score(D, L, h->Xb, (const uint16_t*)q, mno, 0, 1, s); });
-    if (e == cudaSuccess)
-        e = timed(h, K_FINALIZE_BG, s, [&] {
-            return launch_finalize(D, L, h->Xb, (const uint16_t*)q, nullptr, nullptr, nullptr, nullptr, h->lpt, h->pdl,
-                                   1, s);
-        });
-    if (e == cudaSuccess) e = timed(h, K_RECALL_BG, s, [&] { return launch_recall(D, L, 0, s, h->X.trace); });
-    return e;
-}
-
-// Pipelined decode step of one layer (default), PAPER.md P:223-226,
-// speculative retrieval takes selection and recall off the critical
-// path:
+// Overlapped decode step of one layer (FREEKV_PIPELINE=1), PAPER.md
+// the units whose correction check passes attend their
+// resident set R (selected at step i-1) while the selection of step i runs:
 //   cs: prep (append, correction flags, page lists over R) -> attention of the
-//       speculative units -> [join] -> combine (+ commit of corrected units)
-//   ss: score + select of the corrected units (which = 2) -> their attention, which
-//       reads the pages they lack straight from the host pool and caches them
-//   rs: bg_chain, right after the prep (the next step's prep of this layer waits
-//       for it); its HBM-bound score overlaps the HBM-bound attention
+//       speculative units -> [join] -> attention of the corrected units (their
+//       missing pages read from the host pool) -> combine + commit
+//   ss: score + select of every unit (flags from the prep; page lists of the corrected
+//       units only) -> [fork] rs: background recall of S_i \ R for step i+1
 freekv_status do_step_pipelined(freekv_handle* h, int layer, const void* q, const void* k_new, const void* v_new,
                                 float* out) {
     cudaStream_t cs = h->cs, ss = h->ss;
     const FkvDims& D = h->D;
     FkvLayer& L = h->layers[layer];
     if (!q || !out) return fail(FREEKV_EINVAL, "q/out is NULL");
-    // the previous step's background half of this layer (R, q_prev, slots)
-    if (h->capturing)
-        FKV_CUDA(cudaStreamWaitEvent(cs, h->ev_recall[layer], cudaEventWaitExternal));
-    else if (h->recall_pending[layer])
-        FKV_CUDA(cudaStreamWaitEvent(cs, h->ev_recall[layer], 0));
+    // the previous step's recall of this layer (its slots); one-graph capture: the previous
+    // graph launch joined it
+    if (!h->capturing && h->recall_pending[layer]) FKV_CUDA(cudaStreamWaitEvent(cs, h->ev_recall[layer], 0));
     FKV_CUDA(timed(h, K_PREP, cs, [&] {
         return launch_prep(D, L, h->X, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new, nullptr,
                            cs);
     }));
     if (!h->capturing) h->ctx_host[layer] += 1;
-    // background half right after the prep: its HBM-bound score runs beside this layer's
-    // HBM-bound attention instead of beside the next layer's latency-bound prologue
-    if (h->capturing) {  // the recall graph runs bg_chain after this node
-        FKV_CUDA(cudaEventRecordWithFlags(h->ev_select[layer], cs, cudaEventRecordExternal));
-    } else if (!h->serial_recall) {
-        FKV_CUDA(cudaEventRecord(h->ev_select[layer], cs));
-        FKV_CUDA(cudaStreamWaitEvent(h->rs, h->ev_select[layer], 0));
-        FKV_CUDA(bg_chain(h, layer, h->rs));
-        FKV_CUDA(cudaEventRecord(h->ev_recall[layer], h->rs));
-        h->recall_pending[layer] = 1;
-    }
     FKV_CUDA(cudaEventRecord(h->ev_pre[layer], cs));
     FKV_CUDA(cudaStreamWaitEvent(ss, h->ev_pre[layer], 0));
     const int mno = h->capturing ? max_n_off(D, D.max_ctx) : max_n_off(D, h->ctx_host[layer]);
     if (h->capturing || mno - D.n_sink > D.K)
-        FKV_CUDA(timed(h, K_SCORE, ss, [&] { return launch_score(D, L, h->X, (const uint16_t*)q, mno, 0, 2, ss); }));
+        FKV_CUDA(timed(h, K_SCORE, ss, [&] { return launch_score(D, L, h->X, (const uint16_t*)q, mno, 0, 0, false, ss); }));
     FKV_CUDA(timed(h, K_FINALIZE, ss, [&] {
-        return launch_finalize(D, L, h->X, (const uint16_t*)q, nullptr, nullptr, nullptr, nullptr, h->lpt, h->pdl, 2,
+        return launch_finalize(D, L, h->X, (const uint16_t*)q, nullptr, nullptr, nullptr, nullptr, h->lpt, 512, h->pdl, 3,
                                ss);
     }));
-    FKV_CUDA(timed(h, K_ATTN_P2, ss, [&] {
-        return launch_attn_split(D, L, h->X, (const uint16_t*)q, 2, h->tmap_kv, h->tmap_host, h->arena, h->pdl, ss);
-    }));
     FKV_CUDA(cudaEventRecord(h->ev_fl[layer], ss));
+    if (h->serial_recall) {
+        FKV_CUDA(timed(h, K_RECALL_BG, ss, [&] { return launch_recall(D, L, 0, ss, h->X.trace); }));
+        FKV_CUDA(cudaEventRecord(h->ev_recall[layer], ss));
+    } else {
+        FKV_CUDA(cudaStreamWaitEvent(h->rs, h->ev_fl[layer], 0));
+        FKV_CUDA(timed(h, K_RECALL_BG, h->rs, [&] { return launch_recall(D, L, 0, h->rs, h->X.trace); }));
+        FKV_CUDA(cudaEventRecord(h->ev_recall[layer], h->rs));
+    }
+    if (!h->capturing) h->recall_pending[layer] = 1;
     FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] {
         return launch_attn_split(D, L, h->X, (const uint16_t*)q, 1, h->tmap_kv, h->tmap_host, h->arena, h->pdl, cs);
     }));
     FKV_CUDA(cudaStreamWaitEvent(cs, h->ev_fl[layer], 0));
-    FKV_CUDA(timed(h, K_ATTN_COMBINE, cs, [&] {
-        return launch_attn_combine(D, L, h->X, (const uint16_t*)q, out, 1, 2, false, cs);
+    FKV_CUDA(timed(h, K_ATTN_P2, cs, [&] {
+        return launch_attn_split(D, L, h->X, (const uint16_t*)q, 2, h->tmap_kv, h->tmap_host, h->arena, false, cs);
     }));
-    if (!h->capturing && h->serial_recall) FKV_CUDA(bg_chain(h, layer, cs));
+    FKV_CUDA(timed(h, K_ATTN_COMBINE, cs, [&] {
+        return launch_attn_combine(D, L, h->X, (const uint16_t*)q, out, 1, 0, h->pdl, cs);
+    }));
     return FREEKV_OK;
 }
 
@@ -571,12 +555,12 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
     h->X.page_cnt = (int32_t*)(sb + s.o_page_cnt);
     h->X.page_valid = (uint8_t*)(sb + s.o_page_valid);
     h->X.page_dst = (int32_t*)(sb + s.o_page_dst);
-    h->Xb = h->X;
-    h->Xb.scores = (float*)(sb + s.o_scores_bg);
+
     {
         int P2 = 1;
         while (P2 < D.n_page_host) P2 <<= 1;
-        h->lpt = P2 <= kFinalizeThreads ? 1 : P2 / kFinalizeThreads;
+        h->lpt = P2 <= 512 ? 1 : P2 / 512;      // 512-thread select (overlapped step)
+        h->lpt1k = P2 <= 1024 ? 1 : P2 / 1024;  // 1024-thread select (every unit at once)
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
         h->sel_cluster = (P2 >= 2048 && D.U * 8 < 2 * sms) ? 16 : 8;  // few units: wider clusters
@@ -585,7 +569,8 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         h->fused_select = fs && fs[0] == 'f';
         if (h->fused_select) h->D.direct = 0;  // the cluster select writes slot rows only
         const char* pp = getenv("FREEKV_PIPELINE");
-        h->pipelined = h->D.direct && !(pp && pp[0] == '0');
+        h->pipelined = h->D.direct && pp && pp[0] == '1';
+        h->one_graph = h->D.direct;  // recalls are forked branches of the one step graph
         const char* pd = getenv("FREEKV_PDL");
         h->pdl = !(pd && pd[0] == '0');
         if (h->lpt > 16) {
@@ -595,7 +580,7 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
     }
     {
         int warps = 0;
-        cudaError_t oe = attn_resident_warps(&warps);
+        cudaError_t oe = attn_resident_warps(h->pipelined ? 1 : 2, &warps);
         if (oe != cudaSuccess) {
             freekv_destroy(h);
             return fail(FREEKV_ECUDA, std::string("occupancy query: ") + cudaGetErrorString(oe));
@@ -620,7 +605,6 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
             }
         }
     }
-    h->Xb.trace = h->X.trace;
     {
         const char* fr = getenv("FREEKV_DEBUG_FULL_REFRESH");
         h->D.full_refresh = (fr && fr[0] == '1') ? 1 : 0;
@@ -865,6 +849,7 @@ freekv_status freekv_step_graph_capture(freekv_handle* h, const void* q_all, con
     if (profile) {  // event pool: <= 8 kernels per layer, 2 events each
         freekv_status ps = freekv_profile_begin(h, h->cfg.n_layers * 8 + 8);
         if (ps != FREEKV_OK) return ps;
+        h->prof_mask = profile == 1 ? ~0u : (uint32_t)profile;
     }
     for (int l = 0; l < h->cfg.n_layers; ++l)
         if (h->ctx_host[l] <= 0) return fail(FREEKV_ESTATE, "capture before the first append of every layer");
@@ -893,16 +878,17 @@ freekv_status freekv_step_graph_capture(freekv_handle* h, const void* q_all, con
         }
         if (st == FREEKV_OK) st = do_step_tail(h, l, q, out_all + o_stride * l);
     }
+    if (h->one_graph)  // join every layer's recall branch
+        for (int l = 0; l < h->cfg.n_layers && e == cudaSuccess && st == FREEKV_OK; ++l)
+            e = cudaStreamWaitEvent(h->cs, h->ev_recall[l], 0);
     cudaError_t e2 = cudaStreamEndCapture(h->cs, &gc);
     if (e == cudaSuccess) e = e2;
-    if (e == cudaSuccess && st == FREEKV_OK) {
+    if (e == cudaSuccess && st == FREEKV_OK && !h->one_graph) {
         e = cudaStreamBeginCapture(h->rs, cudaStreamCaptureModeThreadLocal);
         for (int l = 0; l < h->cfg.n_layers && e == cudaSuccess; ++l) {
-            // direct / pipelined mode: after this layer's attention; recall mode: after its synchronous recall
-            e = cudaStreamWaitEvent(h->rs, D.direct ? h->ev_select[l] : h->ev_sync_x[l], cudaEventWaitExternal);
-            if (e == cudaSuccess && h->pipelined)
-                e = bg_chain(h, l, h->rs);
-            else if (e == cudaSuccess)
+            // recall mode: after this layer's synchronous recall
+            e = cudaStreamWaitEvent(h->rs, h->ev_sync_x[l], cudaEventWaitExternal);
+            if (e == cudaSuccess)
                 e = timed(h, K_RECALL_BG, h->rs, [&] { return launch_recall(D, h->layers[l], 0, h->rs, h->X.trace); });
             if (e == cudaSuccess) e = cudaEventRecordWithFlags(h->ev_recall[l], h->rs, cudaEventRecordExternal);
         }
@@ -912,11 +898,12 @@ freekv_status freekv_step_graph_capture(freekv_handle* h, const void* q_all, con
     h->capturing = false;
     if (profile) {
         h->prof = false;
+        h->prof_mask = ~0u;
         h->graph_recs = h->prof_recs;
         h->prof_recs.clear();
     }
     if (e == cudaSuccess && st == FREEKV_OK) e = cudaGraphInstantiate(&h->g_compute, gc, 0);
-    if (e == cudaSuccess && st == FREEKV_OK) e = cudaGraphInstantiate(&h->g_recall, gr, 0);
+    if (e == cudaSuccess && st == FREEKV_OK && gr) e = cudaGraphInstantiate(&h->g_recall, gr, 0);
     if (gc) cudaGraphDestroy(gc);
     if (gr) cudaGraphDestroy(gr);
     if (st != FREEKV_OK) {
@@ -952,13 +939,16 @@ freekv_status freekv_step_graph_profile(freekv_handle* h, float* ms, int32_t* la
 
 freekv_status freekv_step_graph_launch(freekv_handle* h) {
     if (!h) return fail(FREEKV_EINVAL, "handle is NULL");
-    if (!h->g_compute || !h->g_recall) return fail(FREEKV_ESTATE, "no captured step graph");
+    if (!h->g_compute || (!h->g_recall && !h->one_graph)) return fail(FREEKV_ESTATE, "no captured step graph");
     for (int l = 0; l < h->cfg.n_layers; ++l)
         if (h->ctx_host[l] + 1 > h->D.max_ctx) return fail(FREEKV_ERANGE, "context would exceed max_ctx_tokens");
     FKV_CUDA(cudaGraphLaunch(h->g_compute, h->cs));
-    FKV_CUDA(cudaGraphLaunch(h->g_recall, h->rs));
+    if (h->g_recall) FKV_CUDA(cudaGraphLaunch(h->g_recall, h->rs));
     for (int l = 0; l < h->cfg.n_layers; ++l) {
         h->ctx_host[l] += 1;
+        // one graph: its recall branches are joined into its end, so the graph's completion
+        // on cs stands for them (for callers that later use other streams)
+        if (h->one_graph) FKV_CUDA(cudaEventRecord(h->ev_recall[l], h->cs));
         h->recall_pending[l] = 1;
     }
     return FREEKV_OK;

@@ -481,18 +481,47 @@ __global__ void __launch_bounds__(kCombThreads, 2) fkv_attn_combine_kernel(FkvDi
     // select kernel (two launches back) is still running, so nothing is read before this
     pdl_wait();  // the attention's partial records (and the select kernel's lists) are complete
     const int u = blockIdx.x, b = u / D.n_kv, m = u % D.n_kv, G = D.G;
-    // rank of u among the units of its attention phase (split: by correction flag)
+    const int E = G * (kHeadDim / 4);  // float4 per record
+    const int RG = kCombThreads / E;   // record groups
+    const int e = threadIdx.x % E, rg = threadIdx.x / E, h = e / (kHeadDim / 4);
+    // independent loads first (one round trip): this thread's q (for q_prev), commit lists
+    const size_t row = (size_t)b * D.n_qo + m * G + h;
+    const int c4 = e % (kHeadDim / 4);
+    uint2 qv = make_uint2(0u, 0u);
+    if (rg == 0) qv = reinterpret_cast<const uint2*>(q + row * kHeadDim)[c4];
+    int rp = 0, rs = 0;
+    if (threadIdx.x < D.K) {
+        rp = L.pend_pages[(size_t)u * D.K + threadIdx.x];
+        rs = L.pend_slot[(size_t)u * D.K + threadIdx.x];
+    }
+    int pf = 0, pc = 0;
+    if (threadIdx.x == 0) {
+        pf = L.pend_front[u];
+        pc = L.pend_cnt[u];
+    }
+    // rank of u among the units of its attention phase (split: by correction flag); the
+    // flags are loaded in one batch (<= 8 per lane), not one dependent load per 32 units
     __shared__ int s_rank, s_n;
+    const int my_flag = L.flags[u];
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
-        const int my_phase = split ? (L.flags[u] ? 2 : 1) : 0;
+        const int my_phase = split ? (my_flag ? 2 : 1) : 0;
         int cnt = 0, rank = 0;
-        for (int base = 0; base < D.U; base += 32) {
-            const int v = base + lane;
-            const bool f = v < D.U && (my_phase == 0 || ((L.flags[v] != 0) == (my_phase == 2)));
-            const unsigned bal = __ballot_sync(0xffffffffu, f);
-            if (base <= u && u < base + 32) rank = cnt + __popc(bal & ((1u << (u - base)) - 1u));
-            cnt += __popc(bal);
+        for (int base0 = 0; base0 < D.U; base0 += 256) {
+            uint8_t fv[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int v = base0 + 32 * i + lane;
+                fv[i] = (split && v < D.U) ? L.flags[v] : 0;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int base = base0 + 32 * i, v = base + lane;
+                const bool f = v < D.U && (my_phase == 0 || ((fv[i] != 0) == (my_phase == 2)));
+                const unsigned bal = __ballot_sync(0xffffffffu, f);
+                if (base <= u && u < base + 32) rank = cnt + __popc(bal & ((1u << (u - base)) - 1u));
+                cnt += __popc(bal);
+            }
         }
         if (lane == 0) {
             s_rank = rank;
@@ -500,7 +529,7 @@ __global__ void __launch_bounds__(kCombThreads, 2) fkv_attn_combine_kernel(FkvDi
         }
     }
     __syncthreads();
-    const int rec_base = (split && L.flags[u]) ? D.attn_warps : 0;
+    const int rec_base = (split && my_flag) ? D.attn_warps : 0;
     const unsigned V = (unsigned)(s_n * D.P_max);
     const unsigned T = min((unsigned)D.attn_warps, V);  // the phase's warp count (see the split kernel)
     const unsigned x0 = (unsigned)s_rank * D.P_max, x1 = x0 + D.P_max;
@@ -513,14 +542,6 @@ __global__ void __launch_bounds__(kCombThreads, 2) fkv_attn_combine_kernel(FkvDi
         const unsigned w = (unsigned)(w_first + r);
         const unsigned a = w * V / T;
         s_rec[r] = (int)((rec_base + w) * 2 + ((a / D.P_max == (unsigned)s_rank) ? 0 : 1));
-    }
-    const int E = G * (kHeadDim / 4);  // float4 per record
-    const int RG = kCombThreads / E;   // record groups
-    const int e = threadIdx.x % E, rg = threadIdx.x / E, h = e / (kHeadDim / 4);
-    int rp = 0, rs = 0;
-    if (threadIdx.x < D.K) {
-        rp = L.pend_pages[(size_t)u * D.K + threadIdx.x];
-        rs = L.pend_slot[(size_t)u * D.K + threadIdx.x];
     }
     __syncthreads();
     float M = -INFINITY, Ls = 0.0f;
@@ -575,7 +596,7 @@ __global__ void __launch_bounds__(kCombThreads, 2) fkv_attn_combine_kernel(FkvDi
         s_l[threadIdx.x] = Ls;
     }
     __syncthreads();
-    const bool do_commit = commit == 0 || L.flags[u] != 0;
+    const bool do_commit = commit == 0 || my_flag != 0;
     if (rg == 0) {
         float Mb = M;
         for (int g2 = 1; g2 < RG; ++g2) Mb = fmaxf(Mb, s_m[g2 * E + e]);
@@ -592,13 +613,9 @@ __global__ void __launch_bounds__(kCombThreads, 2) fkv_attn_combine_kernel(FkvDi
             Ot.z += wg * og.z;
             Ot.w += wg * og.w;
         }
-        const size_t row = (size_t)b * D.n_qo + m * G + h;
-        const int c4 = e % (kHeadDim / 4);
         reinterpret_cast<float4*>(out + row * kHeadDim)[c4] = make_float4(Ot.x / Lt, Ot.y / Lt, Ot.z / Lt, Ot.w / Lt);
         // q_prev := q_i (4 bf16 = 8 bytes per thread)
-        if (do_commit)
-            reinterpret_cast<uint2*>(L.q_prev + row * kHeadDim)[c4] =
-                reinterpret_cast<const uint2*>(q + row * kHeadDim)[c4];
+        if (do_commit) reinterpret_cast<uint2*>(L.q_prev + row * kHeadDim)[c4] = qv;
     }
     if (!do_commit) return;
     if (threadIdx.x < D.K) {
@@ -610,8 +627,8 @@ __global__ void __launch_bounds__(kCombThreads, 2) fkv_attn_combine_kernel(FkvDi
         L.res_slot[(size_t)u * D.K + i] = L.pend_slot[(size_t)u * D.K + i];
     }
     if (threadIdx.x == 0) {
-        L.res_front[u] = L.pend_front[u];
-        L.res_cnt[u] = L.pend_cnt[u];
+        L.res_front[u] = pf;
+        L.res_cnt[u] = pc;
         L.res_valid[u] = 1;
         trace_stamp(X.trace, 7, blockIdx.x, 1);
     }
@@ -629,7 +646,7 @@ static int attn_stages() {
 }
 
 template <int NST>
-static cudaError_t attn_setup(int* warps) {
+static cudaError_t attn_setup(int cps_want, int* warps) {
     const int smem = kAttnWarpsPerCta * NST * kSlabBytes;
     int dev = 0, sms = 0, per_sm = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -647,22 +664,21 @@ static cudaError_t attn_setup(int* warps) {
     if (e == cudaSuccess)
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fkv_attn_split_kernel<NST>,
                                                           kAttnWarpsPerCta * 32, smem);
-    // CTAs per SM (FREEKV_ATTN_CTAS_PER_SM, default 1): one 4-warp CTA per SM keeps ~14 MB of
-    // TMA loads in flight (3 slabs x 8 KiB per warp), enough to cover HBM latency at full
-    // bandwidth, and leaves shared memory and warp slots for the select kernels that run
-    // concurrently in the pipelined step
+    // CTAs per SM (FREEKV_ATTN_CTAS_PER_SM overrides the caller's choice): 2 when the attention
+    // runs alone (8 warps per SM hide the per-slab MMA/softmax latency); 1 in the pipelined
+    // step, where it leaves shared memory and registers to the select kernels running beside it
     const char* ce = getenv("FREEKV_ATTN_CTAS_PER_SM");
-    const int cps = std::max(1, std::min(per_sm, ce ? atoi(ce) : 1));
+    const int cps = std::max(1, std::min(per_sm, ce ? atoi(ce) : cps_want));
     *warps = sms * cps * kAttnWarpsPerCta;
     return e;
 }
 
 // Resident warps of the split kernel (stage count from FREEKV_ATTN_STAGES: 2, 3 or 4).
-cudaError_t attn_resident_warps(int* warps) {
+cudaError_t attn_resident_warps(int cps, int* warps) {
     switch (attn_stages()) {
-        case 2: return attn_setup<2>(warps);
-        case 4: return attn_setup<4>(warps);
-        default: return attn_setup<3>(warps);
+        case 2: return attn_setup<2>(cps, warps);
+        case 4: return attn_setup<4>(cps, warps);
+        default: return attn_setup<3>(cps, warps);
     }
 }
 

@@ -139,6 +139,37 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// CFR-10 for one head: sequential fp32 channel sums of x*y, x*x and y*y over d = 128
+// bf16 channels (fma = exact product + one rounding), then dot / (sqrt(n1) * sqrt(n2)),
+// 0 when either norm is 0.  All 2 x 256 bytes are loaded first (16-byte vectors), so the
+// chain runs from registers.
+__device__ __forceinline__ float cos_cfr10(const uint16_t* qa, const uint16_t* qb) {
+    uint4 va[16], vb[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        va[i] = reinterpret_cast<const uint4*>(qa)[i];
+        vb[i] = reinterpret_cast<const uint4*>(qb)[i];
+    }
+    float dot = 0.0f, n1 = 0.0f, n2 = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const uint32_t wa[4] = {va[i].x, va[i].y, va[i].z, va[i].w};
+        const uint32_t wb[4] = {vb[i].x, vb[i].y, vb[i].z, vb[i].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {  // channel 8i + 2k + h: low half first
+                const float x = h ? bf16_hi(wa[k]) : bf16_lo(wa[k]);
+                const float y = h ? bf16_hi(wb[k]) : bf16_lo(wb[k]);
+                dot = __fmaf_rn(x, y, dot);
+                n1 = __fmaf_rn(x, x, n1);
+                n2 = __fmaf_rn(y, y, n2);
+            }
+        }
+    }
+    return (n1 == 0.0f || n2 == 0.0f) ? 0.0f : __fdiv_rn(dot, __fmul_rn(__fsqrt_rn(n1), __fsqrt_rn(n2)));
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
                              Args... args) {
@@ -165,7 +196,7 @@ cudaError_t launch_summarize(const FkvDims& D, const FkvLayer& L, int page_begin
                              cudaStream_t s);
 // which (score / finalize): 0 every unit, 1 unflagged units only, 2 corrected units only
 cudaError_t launch_score(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                         int max_n_off, int pending, int which, cudaStream_t s);
+                         int max_n_off, int pending, int which, bool pdl, cudaStream_t s);
 cudaError_t launch_prep(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                         const uint16_t* k_new, const uint16_t* v_new, uint8_t* corrected_out, cudaStream_t s);
 cudaError_t launch_select_fused(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
@@ -173,10 +204,10 @@ cudaError_t launch_select_fused(const FkvDims& D, const FkvLayer& L, const FkvSc
                                 uint8_t* corrected_out, int cluster, int lptm, cudaStream_t s);
 cudaError_t launch_finalize(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                             const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
-                            uint8_t* corrected_out, int lpt, bool pdl, int which, cudaStream_t s);
+                            uint8_t* corrected_out, int lpt, int nt, bool pdl, int which, cudaStream_t s);
 cudaError_t launch_recall(const FkvDims& D, const FkvLayer& L, int sync_mode, cudaStream_t s,
                           unsigned long long* trace = nullptr);
-cudaError_t attn_resident_warps(int* warps);  // SMs x resident warps/SM of the split kernel
+cudaError_t attn_resident_warps(int cps, int* warps);  // warps of the split kernel's grid (cps CTAs per SM)
 cudaError_t launch_attn_split(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                               int phase, const CUtensorMap& tmap, const CUtensorMap& tmap_host,
                               const uint16_t* arena, bool pdl, cudaStream_t s);

@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims 
     __shared__ __align__(8) uint64_t bar[kScoreWarps][kRing];
     pdl_trigger();  // the select-finalize kernel may start its prologue now
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tcls = which == 1 ? 9 : 0;  // trace class
+    const int tcls = 0;  // trace class
     uint8_t* ring = s_raw + warp * (kRing * kChunkBytes);
     if (lane == 0) {
 #pragma unroll
@@ -117,10 +117,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims 
     // grid is smaller (the background score runs on a bounded number of CTAs)
     for (int item = blockIdx.x; item < D.U * gy; item += gridDim.x) {
         const int u = item / gy, yb = item - u * gy, b = u / D.n_kv, m = u % D.n_kv;
-        // which: 0 every unit; 1 unflagged units only (background); 2 corrected units only
-        const int flg = which ? L.flags[u] : 0;
         const int n_off = max(L.n_off[u], frontier_for(D, L.ctx[u] + pending));
-        if (which && (flg != 0) != (which == 2)) continue;
         if (yb * kScoreWarps * 32 >= n_off) continue;  // uniform: no candidate in this item
         __syncthreads();  // the previous item's q staging is no longer read
         const int blk = yb * kScoreWarps + warp;
@@ -136,6 +133,9 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims 
                 bulk_g2s(ring + k * kChunkBytes, src + k * kChunkBytes, kChunkBytes, &bar[warp][k]);
             }
         }
+        // q_i is this layer's input: with PDL the kernel may start while the previous layer's
+        // last kernel drains; everything above (state and summaries of this layer) is independent
+        pdl_wait();
         for (int i = threadIdx.x; i < GP * kHeadDim; i += blockDim.x) {
             const int h = i / kHeadDim, c = i % kHeadDim;
             float x = 0.0f;
@@ -187,10 +187,9 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims 
 // its histogram (2 barriers per 8-bit pass) with warp-aggregated atomics; one
 // packed (gt, eq) block scan places the selected ids in ascending order.
 constexpr int kMaxK = 256;
-constexpr int kThreads = 512;
-constexpr int kWarps = kThreads / 32;
+constexpr int kHistBins = 4096;
 
-template <int LPT, int GM>
+template <int LPT, int GM, int NT>
 __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, const FkvLayer& L,
                                               int32_t* __restrict__ page_rows, uint8_t* __restrict__ page_valid,
                                               int32_t* __restrict__ page_dst, int32_t* __restrict__ page_cnt,
@@ -199,14 +198,17 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
                                               const uint16_t* __restrict__ k_new,
                                               const uint16_t* __restrict__ v_new, int32_t* __restrict__ pages_out,
                                               uint8_t* __restrict__ corrected_out, int which) {
+    constexpr int kThreads = NT, kWarps = NT / 32;
     const int b = u / D.n_kv, m = u % D.n_kv, G = D.G;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_sink = D.n_sink, K = D.K;
 
     __shared__ float s_redm[kWarps][kMaxG], s_redz[kWarps][kMaxG];
     __shared__ float s_cos[kMaxG];
-    __shared__ int s_hist[2][256];
+    __shared__ __align__(16) int s_h[kHistBins];  // radix histogram
     __shared__ int s_dig[4], s_abv[4];
+    __shared__ uint32_t s_bk[32];  // boundary-bin keys and ids
+    __shared__ int s_bid[32], s_bn;
     __shared__ unsigned s_wsum[kWarps];
     __shared__ int s_sel[kMaxK];
     __shared__ int s_res[kMaxK], s_res_slot[kMaxK];
@@ -215,19 +217,19 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
     __shared__ int s_flag;
     __shared__ int s_free[2 * kMaxK];
     __shared__ unsigned char s_used[2 * kMaxK];
-    __shared__ uint32_t s_qa[kMaxG * kHeadDim / 2], s_qb[kMaxG * kHeadDim / 2];
+    __shared__ __align__(16) uint32_t s_qa[kMaxG * kHeadDim / 2], s_qb[kMaxG * kHeadDim / 2];
     extern __shared__ __align__(16) uint8_t s_dyn[];
     uint4* s_page = reinterpret_cast<uint4*>(s_dyn);                                   // append staging
-    float* s_sc = reinterpret_cast<float*>(s_dyn + page_elems(D) * sizeof(uint16_t));  // [G][n_page_max]
+    uint16_t* s_idx = reinterpret_cast<uint16_t*>(s_dyn + page_elems(D) * sizeof(uint16_t));  // [n_page_max]
 
-    // which: 0 = every unit, flags computed here (primitive API / non-pipelined step);
-    // 1 = unflagged units only, flags from the prep kernel, commits R := S_i itself
-    // (background half of the pipelined step); 2 = corrected units only (critical half)
-    const int tcls = which == 1 ? 10 : 1;  // trace class
+    // which: 0 = flags computed here (primitive API / sequential step); 3 = flags from the prep
+    // kernel (overlapped step: the page lists of the units that attend their resident set were
+    // built by the prep kernel and are being read while this kernel runs -- only the corrected
+    // units' lists are written here)
+    const int tcls = 1;  // trace class
     if (tid == 0) trace_stamp(trace, tcls, u, 0);
     pdl_trigger();  // attention may start its prologue
     const int pre_flag = which ? (int)L.flags[u] : 0;
-    if (which && (pre_flag != 0) != (which == 2)) return;
     // ---- a9 (fused, decode path): append this step's token.  Runs while the score kernel
     // drains (PDL): it only touches the ring / the page completing now (not a candidate of
     // this step) / the host pool; ctx and n_off are published after pdl_wait().
@@ -243,8 +245,16 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
     const bool rank_all = n_cand <= K;  // A-11: all candidates selected, no ranking
     if (tid == 0) trace_stamp(trace, tcls, u, 1);
 
-    // ---- stage everything the CTA reads (one round trip): q_i, q_{i-1}, resident set, scores
-    {
+    // ---- a1: correction (CFR-10), which == 0 only: lanes 0..G-1 of the last warp run the
+    // sequential channel sums before the scores arrive
+    const bool cos_lane = which == 0 && warp == kWarps - 1 && lane < G;
+    auto cos_all = [&]() {
+        s_cos[lane] = cos_cfr10(reinterpret_cast<const uint16_t*>(s_qa) + lane * kHeadDim,
+                                reinterpret_cast<const uint16_t*>(s_qb) + lane * kHeadDim);
+    };
+
+    // ---- stage everything the CTA reads (one round trip): q_i, q_{i-1}, resident set
+    if (which == 0) {
         const uint32_t* qa32 = reinterpret_cast<const uint32_t*>(q + ((size_t)b * D.n_qo + m * G) * kHeadDim);
         const uint32_t* qb32 = reinterpret_cast<const uint32_t*>(L.q_prev + ((size_t)b * D.n_qo + m * G) * kHeadDim);
         for (int i = tid; i < G * kHeadDim / 2; i += kThreads) {
@@ -262,71 +272,47 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
         s_res_slot[i] = res_valid ? L.res_slot[(size_t)u * K + i] : -1;
     }
     for (int i = tid; i < 2 * K; i += kThreads) s_used[i] = 0;
-    for (int i = tid; i < 256; i += kThreads) s_hist[0][i] = 0;
+    for (int i = tid; i < kHistBins; i += kThreads) s_h[i] = 0;
+    if (tid == 0) s_bn = 0;
     const size_t srow = (size_t)D.n_page_max;
+    __syncthreads();  // staging visible
+    // work that needs no scores runs while the score kernel drains (PDL): the resident set's
+    // page -> index table and used-slot map, and (which == 0) the correction check
+    if (tid < K && s_res[tid] >= 0) {
+        s_idx[s_res[tid]] = (uint16_t)tid;
+        s_used[s_res_slot[tid]] = 1;
+    }
+    if (cos_lane) cos_all();
     pdl_wait();  // the score kernel has completed: its scores are visible, ctx may be published
     if (k_new && tid == 0) {
         L.ctx[u] = Lc_now;
         L.n_off[u] = n_off;
     }
-    if (!rank_all) {
-        const float* sg = scores + (size_t)u * G * srow;
-        for (int j = n_sink + tid; j < n_off; j += kThreads) {
-            float v[GM];  // all heads' loads in flight together
-#pragma unroll
-            for (int g = 0; g < GM; ++g)
-                if (g < G) v[g] = sg[g * srow + j];
-#pragma unroll
-            for (int g = 0; g < GM; ++g)
-                if (g < G) s_sc[g * srow + j] = v[g];
-        }
-    }
-    __syncthreads();
-
-    // ---- a1: correction (CFR-10): lanes 0..G-1 of the last warp run the sequential channel
-    // sums in 4 chunks of 32 channels, interleaved with the radix passes below (where the
-    // other warps wait on warp 0's digit scan) so they never lengthen the critical path
-    const bool cos_lane = which == 0 && warp == kWarps - 1 && lane < G;
-    float c_dot = 0.0f, c_n1 = 0.0f, c_n2 = 0.0f;
-    auto cos_chunk = [&](int part) {
-        const uint16_t* qa = reinterpret_cast<const uint16_t*>(s_qa) + lane * kHeadDim;
-        const uint16_t* qb = reinterpret_cast<const uint16_t*>(s_qb) + lane * kHeadDim;
-#pragma unroll 8
-        for (int c = part * 32; c < part * 32 + 32; ++c) {
-            const float x = bf16f(qa[c]), y = bf16f(qb[c]);
-            c_dot = __fmaf_rn(x, y, c_dot);  // exact product, one rounding = fl(dot + x*y)
-            c_n1 = __fmaf_rn(x, x, c_n1);
-            c_n2 = __fmaf_rn(y, y, c_n2);
-        }
-        if (part == 3)
-            s_cos[lane] = (c_n1 == 0.0f || c_n2 == 0.0f)
-                              ? 0.0f
-                              : __fdiv_rn(c_dot, __fmul_rn(__fsqrt_rn(c_n1), __fsqrt_rn(c_n2)));
-    };
-
     int cnt;
     if (rank_all) {
         for (int i = tid; i < K; i += kThreads) s_sel[i] = i < n_cand ? n_sink + i : -1;
-        if (cos_lane)
-            for (int part = 0; part < 4; ++part) cos_chunk(part);
         cnt = n_cand > 0 ? n_cand : 0;
         __syncthreads();
     } else {
         if (tid == 0) trace_stamp(trace, tcls, u, 2);
-        const float* su = s_sc;
         const int jb = tid * LPT;
+        // this thread's leaves, straight from global memory into registers (no staging pass)
+        const float* sg = scores + (size_t)u * G * srow;
+        bool cand[LPT];
+        float sv[GM][LPT];
+#pragma unroll
+        for (int l = 0; l < LPT; ++l) cand[l] = jb + l >= n_sink && jb + l < n_off;
+#pragma unroll
+        for (int g = 0; g < GM; ++g)
+#pragma unroll
+            for (int l = 0; l < LPT; ++l) sv[g][l] = (g < G && cand[l]) ? sg[g * srow + jb + l] : -INFINITY;
         // ---- CFR-4: max per head (exact, order-free); the G heads' shuffles interleave
         float M[GM];
 #pragma unroll
         for (int g = 0; g < GM; ++g) {
-            M[g] = -INFINITY;
-            if (g < G) {
+            M[g] = sv[g][0];
 #pragma unroll
-                for (int l = 0; l < LPT; ++l) {
-                    const int j = jb + l;
-                    if (j >= n_sink && j < n_off) M[g] = fmaxf(M[g], su[g * srow + j]);
-                }
-            }
+            for (int l = 1; l < LPT; ++l) M[g] = fmaxf(M[g], sv[g][l]);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1)
@@ -348,20 +334,17 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
         float Z[GM];
 #pragma unroll
         for (int g = 0; g < GM; ++g) {
-            Z[g] = 0.0f;
-            if (g < G) {
-                float e[LPT];
 #pragma unroll
-                for (int l = 0; l < LPT; ++l) {
-                    const int j = jb + l;
-                    e[l] = (j >= n_sink && j < n_off) ? cexp2_cfr(__fsub_rn(su[g * srow + j], M[g])) : 0.0f;
-                }
+            for (int l = 0; l < LPT; ++l)
+                sv[g][l] = (g < G && cand[l]) ? cexp2_cfr(__fsub_rn(sv[g][l], M[g])) : 0.0f;  // sv := e
+            float t[LPT];
 #pragma unroll
-                for (int w = 1; w < LPT; w <<= 1)
+            for (int l = 0; l < LPT; ++l) t[l] = sv[g][l];
 #pragma unroll
-                    for (int l = 0; l < LPT; l += 2 * w) e[l] = __fadd_rn(e[l], e[l + w]);
-                Z[g] = e[0];
-            }
+            for (int w = 1; w < LPT; w <<= 1)
+#pragma unroll
+                for (int l = 0; l < LPT; l += 2 * w) t[l] = __fadd_rn(t[l], t[l + w]);
+            Z[g] = t[0];
         }
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1)
@@ -380,17 +363,14 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
         if (tid == 0) trace_stamp(trace, tcls, u, 3);
         // ---- CFR-7/8: p = e / Z; pooled = sequential sum over g; CFR-9 keys
         uint32_t key[LPT];
-        bool cand[LPT];
 #pragma unroll
         for (int l = 0; l < LPT; ++l) {
-            const int j = jb + l;
-            cand[l] = j >= n_sink && j < n_off;
             float pi = 0.0f;
             if (cand[l]) {
 #pragma unroll
                 for (int g = 0; g < GM; ++g) {
                     if (g < G) {
-                        const float pg = __fdiv_rn(cexp2_cfr(__fsub_rn(su[g * srow + j], M[g])), Z[g]);
+                        const float pg = __fdiv_rn(sv[g][l], Z[g]);
                         pi = g == 0 ? pg : __fadd_rn(pi, pg);
                     }
                 }
@@ -398,52 +378,121 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
             const uint32_t kk = __float_as_uint(pi);
             key[l] = kk == 0x80000000u ? 0u : kk;
         }
-        // ---- radix select of the K-th largest key (4 x 8-bit passes)
+        // ---- exact K-th largest key: radix passes of 12, 12 and 8 bits; as soon as the boundary
+        // bin holds <= 32 keys, one warp ranks them directly (usually after the first pass)
         uint32_t prefix = 0u, mask = 0u;
         int k_rem = K;
+        uint32_t T = 0u;
+        bool resolved = false;
 #pragma unroll 1
-        for (int pass = 0; pass < 4; ++pass) {
-            const int shift = 24 - 8 * pass;
-            int* H = s_hist[pass & 1];
+        for (int pass = 0; pass < 3; ++pass) {
+            const int shift = pass == 0 ? 20 : (pass == 1 ? 8 : 0);
+            const int nbits = pass == 2 ? 8 : 12;
+            const uint32_t dmask = (1u << nbits) - 1u;
+            if (pass > 0) {  // fallback passes (rare): clear the histogram first
+                __syncthreads();
+                for (int i = tid; i < kHistBins; i += kThreads) s_h[i] = 0;
+                __syncthreads();
+            }
 #pragma unroll
             for (int l = 0; l < LPT; ++l) {
-                const int dg = (cand[l] && (key[l] & mask) == prefix) ? (int)((key[l] >> shift) & 255u) : -1;
+                const int dg = (cand[l] && (key[l] & mask) == prefix) ? (int)((key[l] >> shift) & dmask) : -1;
                 const unsigned grp = __match_any_sync(0xffffffffu, dg);
-                if (dg >= 0 && lane == __ffs(grp) - 1) atomicAdd(&H[dg], __popc(grp));
+                if (dg >= 0 && lane == __ffs(grp) - 1) atomicAdd(&s_h[dg], __popc(grp));
             }
-            for (int i = tid; i < 256; i += kThreads) s_hist[(pass + 1) & 1][i] = 0;
             __syncthreads();
-            if (cos_lane) cos_chunk(pass);
             if (warp == 0) {
-                int bins[8], lsum = 0;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    bins[i] = H[lane * 8 + i];
-                    lsum += bins[i];
+                // lane owns bins [lane * per, (lane + 1) * per); suffix scan over lanes (descending bins)
+                const int per = (int)(dmask + 1u) >> 5;
+                int lsum = 0;
+                for (int i = 0; i < per; i += 4) {
+                    const int4 h4 = *reinterpret_cast<const int4*>(&s_h[lane * per + i]);
+                    lsum += h4.x + h4.y + h4.z + h4.w;
                 }
-                int suf = lsum;  // inclusive suffix scan over lanes
+                int suf = lsum;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const int y = __shfl_down_sync(0xffffffffu, suf, o);
                     if (lane + o < 32) suf += y;
                 }
-                int above = suf - lsum;
+                const int above = suf - lsum;  // keys in bins of higher lanes
+                const unsigned hit = __ballot_sync(0xffffffffu, above < k_rem && above + lsum >= k_rem);
+                const int lb = __ffs(hit) - 1;  // the lane whose bins hold the boundary
+                const int above_lb = __shfl_sync(0xffffffffu, above, lb);
+                // refine inside lane lb's bins, 4 per lane, again by a suffix scan
+                const int nl = per >> 2;
+                int4 c4 = make_int4(0, 0, 0, 0);
+                if (lane < nl) c4 = *reinterpret_cast<const int4*>(&s_h[lb * per + 4 * lane]);
+                const int s4 = c4.x + c4.y + c4.z + c4.w;
+                int suf2 = s4;
 #pragma unroll
-                for (int i = 7; i >= 0; --i) {
-                    if (above < k_rem && above + bins[i] >= k_rem) {
-                        s_dig[pass] = lane * 8 + i;
-                        s_abv[pass] = above;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_down_sync(0xffffffffu, suf2, o);
+                    if (lane + o < 32) suf2 += y;
+                }
+                int a = above_lb + suf2 - s4;
+                if (lane < nl && a < k_rem && a + s4 >= k_rem) {
+                    int bin, c;
+                    if (a + c4.w >= k_rem) {
+                        bin = 3, c = c4.w;
+                    } else if ((a += c4.w) + c4.z >= k_rem) {
+                        bin = 2, c = c4.z;
+                    } else if ((a += c4.z) + c4.y >= k_rem) {
+                        bin = 1, c = c4.y;
+                    } else {
+                        a += c4.y;
+                        bin = 0, c = c4.x;
                     }
-                    above += bins[i];
+                    s_dig[0] = lb * per + 4 * lane + bin;
+                    s_abv[0] = a;
+                    s_dig[1] = c;
                 }
             }
             __syncthreads();
-            k_rem -= s_abv[pass];
-            prefix |= (uint32_t)s_dig[pass] << shift;
-            mask |= 0xFFu << shift;
+            k_rem -= s_abv[0];
+            prefix |= (uint32_t)s_dig[0] << shift;
+            mask |= dmask << shift;
+            if (pass == 2) {  // every bit fixed: T = prefix, take k_rem of the keys equal to it
+                T = prefix;
+                resolved = true;
+                break;
+            }
+            if (s_dig[1] <= 32) break;
         }
         if (tid == 0) trace_stamp(trace, tcls, u, 4);
-        const uint32_t T = prefix;  // K-th largest key; take k_rem of the keys equal to T (lowest ids)
+        if (!resolved) {
+            // the boundary bin's (key, id) pairs (<= 32) -> one warp ranks them exactly (ties -> lower id)
+#pragma unroll
+            for (int l = 0; l < LPT; ++l) {
+                if (cand[l] && (key[l] & mask) == prefix) {
+                    const int at = atomicAdd(&s_bn, 1);
+                    s_bk[at] = key[l];
+                    s_bid[at] = jb + l;
+                }
+            }
+            __syncthreads();
+            if (warp == 0) {
+                const int n = s_bn;
+                const uint32_t mk = lane < n ? s_bk[lane] : 0u;
+                const int mi = lane < n ? s_bid[lane] : 0x7fffffff;
+                int rank = 0;
+                for (int i = 0; i < n; ++i) {
+                    const uint32_t ok = __shfl_sync(0xffffffffu, mk, i);
+                    const int oi = __shfl_sync(0xffffffffu, mi, i);
+                    rank += (ok > mk || (ok == mk && oi < mi)) ? 1 : 0;
+                }
+                // the k_rem-th largest of the bin is the threshold; keys above it in the bin are taken
+                if (lane < n && rank == k_rem - 1) {
+                    int gt = 0;
+                    for (int i = 0; i < n; ++i) gt += s_bk[i] > mk ? 1 : 0;
+                    s_dig[2] = (int)mk;
+                    s_abv[2] = k_rem - gt;
+                }
+            }
+            __syncthreads();
+            T = (uint32_t)s_dig[2];
+            k_rem = s_abv[2];
+        }
         // ---- one packed block scan of (#gt, #eq) in page-id order
         unsigned n_gt = 0, n_eq = 0;
 #pragma unroll
@@ -481,53 +530,31 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
         __syncthreads();
     }
 
-    // ---- flag (CFR-10 pooling, A-12, A-13)
+    // ---- flag (CFR-10 pooling, A-12, A-13) and a4: delta vs resident (A-18) + slot assignment
+    // (slot double-buffering), warp-synchronous in warp 0: membership of S_i's pages in R via
+    // the page -> index table built before the scores arrived (entries validated against s_res)
     if (tid == 0) trace_stamp(trace, tcls, u, 5);
-    if (tid == 0) {
-        if (which) {
-            s_flag = pre_flag;  // decided by the prep kernel (same CFR-10 arithmetic)
-        } else {
-            float acc = s_cos[0];
-            for (int g = 1; g < G; ++g) acc = __fadd_rn(acc, s_cos[g]);
-            const float mean = __fdiv_rn(acc, (float)G);
-            int flag;
-            if (D.mode == 1 || D.tau >= 1.0f) flag = 1;
-            else if (D.mode == 2 || D.tau <= 0.0f) flag = 0;
-            else flag = mean < D.tau;
-            if (!res_valid) flag = 1;
-            s_flag = flag;
-            L.flags[u] = (uint8_t)flag;
-            L.cbar[u] = mean;
-            if (corrected_out) corrected_out[u] = (uint8_t)flag;
-        }
-        L.pend_front[u] = n_off;
-    }
-    // ---- a4: delta vs resident (A-18) and slot assignment (slot double-buffering).  Membership
-    // of S_i's pages in R via a page -> index table in the (now dead) score staging area;
-    // entries are validated against s_res, so stale table contents are harmless.
-    uint16_t* s_idx = reinterpret_cast<uint16_t*>(s_sc);
-    for (int i = tid; i < K; i += kThreads)
-        if (s_res[i] >= 0) s_idx[s_res[i]] = (uint16_t)i;
-    __syncthreads();
-    if (tid < K) {
-        int f = 0;
-        const int Sa = tid < cnt ? s_sel[tid] : -1;
-        if (Sa >= 0) {
-            f = 1;
-            const int i = s_idx[Sa];
-            if (i < K && s_res[i] == Sa) {
-                f = 0;
-                s_pslot[tid] = s_res_slot[i];
-            }
-        }
-        s_isfetch[tid] = f;
-        if (s_res[tid] >= 0) s_used[s_res_slot[tid]] = 1;
-        L.pend_pages[(size_t)u * K + tid] = Sa;
-        if (pages_out) pages_out[(size_t)u * K + tid] = Sa;
-        if (Sa < 0) s_pslot[tid] = -1;
-    }
-    __syncthreads();
     if (warp == 0) {
+        if (lane == 0) {
+            if (which) {
+                s_flag = pre_flag;  // decided by the prep kernel (same CFR-10 arithmetic)
+            } else {
+                float acc = s_cos[0];
+                for (int g = 1; g < G; ++g) acc = __fadd_rn(acc, s_cos[g]);
+                const float mean = __fdiv_rn(acc, (float)G);
+                int flag;
+                if (D.mode == 1 || D.tau >= 1.0f) flag = 1;
+                else if (D.mode == 2 || D.tau <= 0.0f) flag = 0;
+                else flag = mean < D.tau;
+                if (!res_valid) flag = 1;
+                s_flag = flag;
+                L.flags[u] = (uint8_t)flag;
+                L.cbar[u] = mean;
+                if (corrected_out) corrected_out[u] = (uint8_t)flag;
+            }
+            L.pend_front[u] = n_off;
+            L.pend_cnt[u] = cnt;
+        }
         int nfree = 0;
         for (int base = 0; base < 2 * K; base += 32) {
             const int sl = base + lane;
@@ -540,43 +567,40 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
         int nf = 0;
         for (int base = 0; base < K; base += 32) {
             const int a = base + lane;
-            const bool fe = a < K && s_isfetch[a];
+            int fe = 0, slot = -1;
+            const int Sa = (a < K && a < cnt) ? s_sel[a] : -1;
+            if (Sa >= 0) {
+                fe = 1;
+                const int i = s_idx[Sa];
+                if (i < K && s_res[i] == Sa) {
+                    fe = 0;
+                    slot = s_res_slot[i];
+                }
+            }
             const unsigned bal = __ballot_sync(0xffffffffu, fe);
             if (fe) {
                 const int r = nf + __popc(bal & ((1u << lane) - 1u));
-                const int slot = s_free[r];
-                s_pslot[a] = slot;
-                L.fetch_page[(size_t)u * K + r] = s_sel[a];
+                slot = s_free[r];
+                L.fetch_page[(size_t)u * K + r] = Sa;
                 L.fetch_slot[(size_t)u * K + r] = slot;
             }
             nf += __popc(bal);
+            if (a < K) {
+                s_isfetch[a] = fe;
+                s_pslot[a] = slot;
+                L.pend_pages[(size_t)u * K + a] = Sa;
+                L.pend_slot[(size_t)u * K + a] = slot;
+                if (pages_out) pages_out[(size_t)u * K + a] = Sa;
+            }
         }
-        if (lane == 0) {
-            L.n_fetch[u] = nf;
-            L.pend_cnt[u] = cnt;
-        }
+        if (lane == 0) L.n_fetch[u] = nf;
     }
     __syncthreads();
-    for (int i = tid; i < K; i += kThreads) L.pend_slot[(size_t)u * K + i] = s_pslot[i];
-    if (which == 1) {
-        // background half: this unit's attention already ran on R (page list built by the prep
-        // kernel), so commit the speculative advance here: R := S_i
-        for (int i = tid; i < K; i += kThreads) {
-            L.res_pages[(size_t)u * K + i] = i < cnt ? s_sel[i] : -1;
-            L.res_slot[(size_t)u * K + i] = s_pslot[i];
-        }
-        if (tid == 0) {  // (q_prev := q_i was done by the prep kernel)
-            L.res_front[u] = n_off;
-            L.res_cnt[u] = cnt;
-            L.res_valid[u] = 1;
-            trace_stamp(trace, tcls, u, 6);
-        }
-        return;
-    }
+    if (tid == 0) trace_stamp(trace, tcls, u, 7);
     // ---- this step's attention page list (row a7), one entry per page: arena row of the
     // page's K block and its valid tokens -- sink pages, the pages in use (S_i if corrected,
     // the resident set otherwise), local pages [f*p, Lc) (reading A-9)
-    {
+    if (which == 0 || s_flag) {
         const int flag = s_flag;
         const int Lc = Lc_now;
         const int p = D.p;
@@ -623,10 +647,9 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
     if (tid == 0) trace_stamp(trace, tcls, u, 6);
 }
 
-// One unit per CTA (grid = U), or, for the background select (which = 1), a bounded
-// grid (FREEKV_BG_SELECT_CTAS) striding over the units.
-template <int LPT, int GM>
-__global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D, FkvLayer L,
+// One unit per CTA (the loop also serves smaller grids).
+template <int LPT, int GM, int NT>
+__global__ void __launch_bounds__(NT) fkv_select_finalize_kernel(FkvDims D, FkvLayer L,
                                                                        int32_t* __restrict__ page_rows,
                                                                        uint8_t* __restrict__ page_valid,
                                                                        int32_t* __restrict__ page_dst,
@@ -640,7 +663,7 @@ __global__ void __launch_bounds__(kThreads) fkv_select_finalize_kernel(FkvDims D
                                                                        uint8_t* __restrict__ corrected_out,
                                                                        int which) {
     for (int u = blockIdx.x; u < D.U; u += gridDim.x) {
-        finalize_unit<LPT, GM>(u, D, L, page_rows, page_valid, page_dst, page_cnt, trace, scores, q, k_new, v_new,
+        finalize_unit<LPT, GM, NT>(u, D, L, page_rows, page_valid, page_dst, page_cnt, trace, scores, q, k_new, v_new,
                                pages_out, corrected_out, which);
         __syncthreads();  // shared state of this unit is dead before the next unit reuses it
     }
@@ -661,7 +684,7 @@ __global__ void __launch_bounds__(kPrepThreads) fkv_prep_kernel(FkvDims D, FkvLa
                                                                 const uint16_t* __restrict__ v_new,
                                                                 uint8_t* __restrict__ corrected_out) {
     extern __shared__ __align__(16) uint8_t s_dyn[];  // append staging: one (2, p, d) page
-    __shared__ uint32_t s_qa[kMaxG * kHeadDim / 2], s_qb[kMaxG * kHeadDim / 2];
+    __shared__ __align__(16) uint32_t s_qa[kMaxG * kHeadDim / 2], s_qb[kMaxG * kHeadDim / 2];
     __shared__ float s_cos[kMaxG];
     __shared__ int s_flag;
     const int u = blockIdx.x, b = u / D.n_kv, m = u % D.n_kv, G = D.G, tid = threadIdx.x;
@@ -685,19 +708,9 @@ __global__ void __launch_bounds__(kPrepThreads) fkv_prep_kernel(FkvDims D, FkvLa
     n_off = max(n_off, frontier_for(D, Lc));
     __syncthreads();
     // ---- a1 (CFR-10): head g's cosine, sequential channel sums by thread g
-    if (tid < G) {
-        const uint16_t* qa = reinterpret_cast<const uint16_t*>(s_qa) + tid * kHeadDim;
-        const uint16_t* qb = reinterpret_cast<const uint16_t*>(s_qb) + tid * kHeadDim;
-        float dot = 0.0f, n1 = 0.0f, n2 = 0.0f;
-#pragma unroll 8
-        for (int c = 0; c < kHeadDim; ++c) {
-            const float x = bf16f(qa[c]), y = bf16f(qb[c]);
-            dot = __fmaf_rn(x, y, dot);
-            n1 = __fmaf_rn(x, x, n1);
-            n2 = __fmaf_rn(y, y, n2);
-        }
-        s_cos[tid] = (n1 == 0.0f || n2 == 0.0f) ? 0.0f : __fdiv_rn(dot, __fmul_rn(__fsqrt_rn(n1), __fsqrt_rn(n2)));
-    }
+    if (tid < G)
+        s_cos[tid] = cos_cfr10(reinterpret_cast<const uint16_t*>(s_qa) + tid * kHeadDim,
+                               reinterpret_cast<const uint16_t*>(s_qb) + tid * kHeadDim);
     __syncthreads();
     // q_prev := q_i now (q_prev is read only by this check): the background select
     // of this step reads q_i from here, so the caller's q buffer may be reused at once
@@ -779,7 +792,7 @@ cudaError_t launch_prep(const FkvDims& D, const FkvLayer& L, const FkvScratch& X
 
 template <int G>
 static void launch_score_g(const FkvDims& D, const FkvLayer& L, float* scores, const uint16_t* q, int max_n_off,
-                           int pending, unsigned long long* trace, int which, cudaStream_t s) {
+                           int pending, unsigned long long* trace, int which, bool pdl, cudaStream_t s) {
     const int per_cta = kScoreWarps * 32;
     const int gy = (max_n_off + per_cta - 1) / per_cta;
     if (gy <= 0) return;
@@ -791,85 +804,83 @@ static void launch_score_g(const FkvDims& D, const FkvLayer& L, float* scores, c
                              cudaSharedmemCarveoutMaxShared);
         configured = true;
     }
-    // background (which = 1): a bounded grid-stride grid (FREEKV_BG_SCORE_CTAS, default 64) so the
-    // background score leaves most SMs to the attention running beside it
-    static int bg_ctas = 0;
-    if (!bg_ctas) {
-        const char* e = getenv("FREEKV_BG_SCORE_CTAS");
-        bg_ctas = std::max(1, e ? atoi(e) : 64);
-    }
-    const int items = D.U * gy;
-    const int grid = which == 1 ? std::min(items, bg_ctas) : items;
-    fkv_score_kernel<G><<<grid, per_cta, smem, s>>>(D, L, scores, q, pending, trace, which, gy);
+    const int grid = D.U * gy;  // one (unit, 128-page block) item per CTA
+    launch_ex(fkv_score_kernel<G>, dim3(grid), dim3(per_cta), smem, s, pdl, D, L, scores, q, pending, trace, which, gy);
 }
 
 cudaError_t launch_score(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                         int max_n_off, int pending, int which, cudaStream_t s) {
+                         int max_n_off, int pending, int which, bool pdl, cudaStream_t s) {
     switch (D.G) {
-        case 1: launch_score_g<1>(D, L, X.scores, q, max_n_off, pending, X.trace, which, s); break;
-        case 2: launch_score_g<2>(D, L, X.scores, q, max_n_off, pending, X.trace, which, s); break;
-        case 3: launch_score_g<3>(D, L, X.scores, q, max_n_off, pending, X.trace, which, s); break;
-        case 4: launch_score_g<4>(D, L, X.scores, q, max_n_off, pending, X.trace, which, s); break;
-        case 5: launch_score_g<5>(D, L, X.scores, q, max_n_off, pending, X.trace, which, s); break;
-        case 6: launch_score_g<6>(D, L, X.scores, q, max_n_off, pending, X.trace, which, s); break;
-        case 7: launch_score_g<7>(D, L, X.scores, q, max_n_off, pending, X.trace, which, s); break;
-        case 8: launch_score_g<8>(D, L, X.scores, q, max_n_off, pending, X.trace, which, s); break;
+        case 1: launch_score_g<1>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s); break;
+        case 2: launch_score_g<2>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s); break;
+        case 3: launch_score_g<3>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s); break;
+        case 4: launch_score_g<4>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s); break;
+        case 5: launch_score_g<5>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s); break;
+        case 6: launch_score_g<6>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s); break;
+        case 7: launch_score_g<7>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s); break;
+        case 8: launch_score_g<8>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
 }
 
 // GM = group-size bucket (1, 2, 4, 8) >= G: the per-head loops and shuffles run GM wide
-template <int LPT, int GM>
+template <int LPT, int GM, int NT>
 static cudaError_t launch_fin_g(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                                 const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
                                 uint8_t* corrected_out, size_t smem, bool pdl, int which, cudaStream_t s) {
     static size_t configured = 0;
     if (smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(fkv_select_finalize_kernel<LPT, GM>,
+        cudaError_t e = cudaFuncSetAttribute(fkv_select_finalize_kernel<LPT, GM, NT>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(fkv_select_finalize_kernel<LPT, GM>,
+            e = cudaFuncSetAttribute(fkv_select_finalize_kernel<LPT, GM, NT>,
                                      cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return e;
         configured = smem;
     }
-    static int bg_ctas = 0;
-    if (!bg_ctas) {
-        const char* e = getenv("FREEKV_BG_SELECT_CTAS");
-        bg_ctas = std::max(1, e ? atoi(e) : 32);
-    }
-    const int grid = which == 1 ? std::min(D.U, bg_ctas) : D.U;
-    return launch_ex(fkv_select_finalize_kernel<LPT, GM>, dim3(grid), dim3(kThreads), smem, s, pdl, D, L, X.page_rows,
+    const int grid = D.U;
+    return launch_ex(fkv_select_finalize_kernel<LPT, GM, NT>, dim3(grid), dim3(NT), smem, s, pdl, D, L, X.page_rows,
                      X.page_valid, X.page_dst, X.page_cnt, X.trace, (const float*)X.scores, q, k_new, v_new, pages_out,
                      corrected_out, which);
 }
 
-template <int LPT>
+template <int LPT, int NT>
 static cudaError_t launch_fin(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                               const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
                               uint8_t* corrected_out, size_t smem, bool pdl, int which, cudaStream_t s) {
-    if (D.G <= 1) return launch_fin_g<LPT, 1>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
-    if (D.G <= 2) return launch_fin_g<LPT, 2>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
-    if (D.G <= 4) return launch_fin_g<LPT, 4>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
-    return launch_fin_g<LPT, 8>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
+    if (D.G <= 1) return launch_fin_g<LPT, 1, NT>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
+    if (D.G <= 2) return launch_fin_g<LPT, 2, NT>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
+    if (D.G <= 4) return launch_fin_g<LPT, 4, NT>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
+    return launch_fin_g<LPT, 8, NT>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
 }
 
-// lpt = leaves per thread of the kThreads-thread tree; kThreads * lpt >= next_pow2(n_off) for every n_off the
-// handle can reach (a larger zero-padded tree gives the same Z, CFR-6).  k_new/v_new non-NULL fuses
-// this step's single-token append (row a9) into the kernel.
+// nt = threads per CTA (512 or 1024); lpt = leaves per thread: nt * lpt >= next_pow2(n_off) for every
+// n_off the handle can reach (a larger zero-padded tree gives the same Z, CFR-6).  k_new/v_new non-NULL
+// fuses this step's single-token append (row a9) into the kernel.
 cudaError_t launch_finalize(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                             const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
-                            uint8_t* corrected_out, int lpt, bool pdl, int which, cudaStream_t s) {
-    const size_t smem = page_elems(D) * sizeof(uint16_t) + (size_t)D.G * D.n_page_max * sizeof(float);
+                            uint8_t* corrected_out, int lpt, int nt, bool pdl, int which, cudaStream_t s) {
+    const size_t smem = page_elems(D) * sizeof(uint16_t) + (size_t)D.n_page_max * sizeof(uint16_t);
+#define FKV_FIN(LP, N) return launch_fin<LP, N>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s)
+    if (nt == 1024) {
+        switch (lpt) {
+            case 1: FKV_FIN(1, 1024);
+            case 2: FKV_FIN(2, 1024);
+            case 4: FKV_FIN(4, 1024);
+            case 8: FKV_FIN(8, 1024);
+            default: return cudaErrorInvalidValue;
+        }
+    }
     switch (lpt) {
-        case 1: return launch_fin<1>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
-        case 2: return launch_fin<2>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
-        case 4: return launch_fin<4>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
-        case 8: return launch_fin<8>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
-        case 16: return launch_fin<16>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
+        case 1: FKV_FIN(1, 512);
+        case 2: FKV_FIN(2, 512);
+        case 4: FKV_FIN(4, 512);
+        case 8: FKV_FIN(8, 512);
+        case 16: FKV_FIN(16, 512);
         default: return cudaErrorInvalidValue;
     }
+#undef FKV_FIN
 }
 
 }  // namespace fkv

@@ -149,10 +149,13 @@ def test_parity_long_context_many_tiles():
     run_parity(G=4, n_kv=1, batch=1, page=16, sink=64, window=64, budget=640, L0=20000, steps=3, n_layers=1)
 
 
-def test_step_graph_matches_eager():
-    """Whole-step CUDA graphs (two graphs joined by external event nodes) give the
-    same selections and bit-identical outputs as the eager per-layer calls."""
+@pytest.mark.parametrize("pipeline", ["0", "1"])
+def test_step_graph_matches_eager(pipeline, monkeypatch):
+    """Whole-step CUDA graphs (one graph with forked recall branches; pipelined: two graphs
+    joined by external event nodes) give the same selections and bit-identical outputs as
+    the eager per-layer calls."""
     _need_gpu()
+    monkeypatch.setenv("FREEKV_PIPELINE", pipeline)
     import paper_2505_13109_b200 as P
     nb, n_kv, G, d, p, L0, steps, n_layers = 2, 2, 4, 128, 32, 1200, 6, 3
     n_qo = G * n_kv
@@ -226,13 +229,15 @@ def test_parity_full_refresh_direct(monkeypatch):
     run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=4, mode=O.MODE_ALWAYS, check_fetch=False)
 
 
-def test_parity_not_pipelined(monkeypatch):
-    """FREEKV_PIPELINE=0: selection of every unit before the attention (one select launch
-    per layer, corrected units' pages read from the host pool in the same attention)."""
-    monkeypatch.setenv("FREEKV_PIPELINE", "0")
+def test_parity_pipelined(monkeypatch):
+    """FREEKV_PIPELINE=1: speculative units attend R while the selection of step i runs in the
+    background; corrected units run score + select + attention on a second stream."""
+    monkeypatch.setenv("FREEKV_PIPELINE", "1")
     run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=5)
+    run_parity(G=7, n_kv=1, batch=2, page=16, sink=64, window=64, budget=640, L0=3000, steps=4, n_layers=1)
+    run_parity(G=4, n_kv=2, batch=1, page=32, sink=64, window=0, budget=256, L0=1000, steps=40, n_layers=1)
 
 
-def test_parity_window_zero_pipelined():
+def test_parity_window_zero():
     """W = 0: the page completed by this step's token is a candidate at once (append first)."""
     run_parity(G=4, n_kv=2, batch=1, page=32, sink=64, window=0, budget=256, L0=1000, steps=40, n_layers=1)

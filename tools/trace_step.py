@@ -68,7 +68,7 @@ for i, l in steps():
             step[nm] = {"n": int(len(ents)), "first_start_us": round(float(rel[:, 0].min()), 2),
                         "last_start_us": round(float(rel[:, 0].max()), 2),
                         "end_us": round(float((last.max() - t0) / 1000.0), 2),
-                        "median_stamps_rel_start_us": [round(float(np.median(np.where(ents[:, j] > 0, ents[:, j] - ents[:, 0], np.nan)[~np.isnan(np.where(ents[:, j] > 0, ents[:, j] - ents[:, 0], np.nan))]) / 1000.0), 2) if (ents[:, j] > 0).any() else None for j in range(1, 7)],
+                        "median_stamps_rel_start_us": [round(float(np.median(np.where(ents[:, j] > 0, ents[:, j] - ents[:, 0], np.nan)[~np.isnan(np.where(ents[:, j] > 0, ents[:, j] - ents[:, 0], np.nan))]) / 1000.0), 2) if (ents[:, j] > 0).any() else None for j in range(1, 8)],
                         "max_span_us": round(float((last - ents[:, 0]).max() / 1000.0), 2)}
         res[f"step{i}_layer{l}"] = step
 print(json.dumps(res, indent=1))
