@@ -59,6 +59,9 @@ struct freekv_handle {
     int lpt = 1, lpt1k = 1;  // leaves per thread of the 512 / 1024-thread select tree (fixed per handle, CFR-6)
     int sel_cluster = 8, sel_lptm = 1;  // fused select: CTAs per unit, max leaves per thread
     bool fused_select = false;          // FREEKV_SELECT=fused selects the one-launch cluster kernel
+    int c2_nt = 512, c2_lpt = 2;        // threads per CTA / leaves per thread of the fused select
+    bool c2_select = false;             // score + select fused in 2-CTA clusters (default when it fits;
+                                        // FREEKV_SELECT=split keeps two launches)
     bool pdl = true;                    // programmatic dependent launch (FREEKV_PDL=0 disables)
     bool serial_recall = false;  // diagnostics: FREEKV_SERIAL_RECALL=1 runs background recall on the compute stream
     // profiling (freekv_profile_begin/end)
@@ -245,7 +248,12 @@ freekv_status do_select(freekv_handle* h, int layer, const void* q, int32_t* pag
         FKV_CUDA(cudaStreamWaitEvent(s, h->ev_recall[layer], cudaEventWaitExternal));
     else if (h->recall_pending[layer])
         FKV_CUDA(cudaStreamWaitEvent(s, h->ev_recall[layer], 0));
-    if (h->fused_select) {
+    if (h->c2_select) {  // score + select in one launch (2-CTA clusters)
+        FKV_CUDA(timed(h, K_FINALIZE, s, [&] {
+            return launch_select_c2(h->D, h->layers[layer], h->X, (const uint16_t*)q, (const uint16_t*)k_new,
+                                    (const uint16_t*)v_new, pages_out, corr_out, h->c2_lpt, h->c2_nt, 2, h->pdl, 0, s);
+        }));
+    } else if (h->fused_select) {
         FKV_CUDA(timed(h, K_FINALIZE, s, [&] {
             return launch_select_fused(h->D, h->layers[layer], h->X, (const uint16_t*)q, (const uint16_t*)k_new,
                                        (const uint16_t*)v_new, pages_out, corr_out, h->sel_cluster, h->sel_lptm, s);
@@ -378,10 +386,13 @@ freekv_status do_step_tail(freekv_handle* h, int layer, const void* q, float* ou
 // the units whose correction check passes attend their
 // resident set R (selected at step i-1) while the selection of step i runs:
 //   cs: prep (append, correction flags, page lists over R) -> attention of the
-//       speculative units -> [join] -> attention of the corrected units (their
-//       missing pages read from the host pool) -> combine + commit
-//   ss: score + select of every unit (flags from the prep; page lists of the corrected
-//       units only) -> [fork] rs: background recall of S_i \ R for step i+1
+//       speculative units on the SMs the select leaves free (one 8-warp CTA per SM)
+//       -> [join] -> attention of the corrected units (their missing pages read from
+//       the host pool) -> combine + commit
+//   ss: fused score + select of every unit, one CTA per unit (flags from the prep; page
+//       lists of the corrected units only) -> [fork] rs: background recall of S_i \ R
+// The select CTA (~200 KB of shared memory) and the 8-warp attention CTA (192 KB)
+// cannot share an SM, so the two kernels partition the GPU whichever starts first.
 freekv_status do_step_pipelined(freekv_handle* h, int layer, const void* q, const void* k_new, const void* v_new,
                                 float* out) {
     cudaStream_t cs = h->cs, ss = h->ss;
@@ -393,17 +404,14 @@ freekv_status do_step_pipelined(freekv_handle* h, int layer, const void* q, cons
     if (!h->capturing && h->recall_pending[layer]) FKV_CUDA(cudaStreamWaitEvent(cs, h->ev_recall[layer], 0));
     FKV_CUDA(timed(h, K_PREP, cs, [&] {
         return launch_prep(D, L, h->X, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new, nullptr,
-                           cs);
+                           h->pdl, cs);
     }));
     if (!h->capturing) h->ctx_host[layer] += 1;
     FKV_CUDA(cudaEventRecord(h->ev_pre[layer], cs));
     FKV_CUDA(cudaStreamWaitEvent(ss, h->ev_pre[layer], 0));
-    const int mno = h->capturing ? max_n_off(D, D.max_ctx) : max_n_off(D, h->ctx_host[layer]);
-    if (h->capturing || mno - D.n_sink > D.K)
-        FKV_CUDA(timed(h, K_SCORE, ss, [&] { return launch_score(D, L, h->X, (const uint16_t*)q, mno, 0, 0, false, ss); }));
     FKV_CUDA(timed(h, K_FINALIZE, ss, [&] {
-        return launch_finalize(D, L, h->X, (const uint16_t*)q, nullptr, nullptr, nullptr, nullptr, h->lpt, 512, h->pdl, 3,
-                               ss);
+        return launch_select_c2(D, L, h->X, (const uint16_t*)q, nullptr, nullptr, nullptr, nullptr, h->lpt, 512, 1,
+                                false, 3, ss);
     }));
     FKV_CUDA(cudaEventRecord(h->ev_fl[layer], ss));
     if (h->serial_recall) {
@@ -416,7 +424,8 @@ freekv_status do_step_pipelined(freekv_handle* h, int layer, const void* q, cons
     }
     if (!h->capturing) h->recall_pending[layer] = 1;
     FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] {
-        return launch_attn_split(D, L, h->X, (const uint16_t*)q, 1, h->tmap_kv, h->tmap_host, h->arena, h->pdl, cs);
+        return launch_attn_split(D, L, h->X, (const uint16_t*)q, 1, h->tmap_kv, h->tmap_host, h->arena, h->pdl, cs,
+                                 8);
     }));
     FKV_CUDA(cudaStreamWaitEvent(cs, h->ev_fl[layer], 0));
     FKV_CUDA(timed(h, K_ATTN_P2, cs, [&] {
@@ -557,8 +566,11 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
     h->X.page_dst = (int32_t*)(sb + s.o_page_dst);
 
     {
+        // leaves of the select tree: page ids [0, n_off); n_off never exceeds
+        // max(S/p, max_ctx/p - W/p), so the tree (zero-padded, CFR-6) needs next_pow2 of that
+        const int n_off_max = std::max(D.n_sink, D.max_ctx / D.p - D.n_win);
         int P2 = 1;
-        while (P2 < D.n_page_host) P2 <<= 1;
+        while (P2 < n_off_max) P2 <<= 1;
         h->lpt = P2 <= 512 ? 1 : P2 / 512;      // 512-thread select (overlapped step)
         h->lpt1k = P2 <= 1024 ? 1 : P2 / 1024;  // 1024-thread select (every unit at once)
         int sms = 148;
@@ -568,6 +580,14 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         const char* fs = getenv("FREEKV_SELECT");
         h->fused_select = fs && fs[0] == 'f';
         if (h->fused_select) h->D.direct = 0;  // the cluster select writes slot rows only
+        {
+            const char* ne = getenv("FREEKV_SELECT_THREADS");  // 256, 512 (default) or 1024
+            h->c2_nt = ne ? atoi(ne) : 512;
+            if (h->c2_nt != 256 && h->c2_nt != 1024) h->c2_nt = 512;
+            h->c2_lpt = P2 <= h->c2_nt ? 1 : P2 / h->c2_nt;
+            if (h->c2_nt == 256 && h->c2_lpt < 2) h->c2_lpt = 2;  // (instantiated: 2..8)
+        }
+        h->c2_select = !h->fused_select && !(fs && fs[0] == 's') && select_c2_fits(h->D, h->c2_lpt, h->c2_nt);
         const char* pp = getenv("FREEKV_PIPELINE");
         h->pipelined = h->D.direct && pp && pp[0] == '1';
         h->one_graph = h->D.direct;  // recalls are forked branches of the one step graph
@@ -580,7 +600,7 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
     }
     {
         int warps = 0;
-        cudaError_t oe = attn_resident_warps(h->pipelined ? 1 : 2, &warps);
+        cudaError_t oe = attn_resident_warps(2, &warps);
         if (oe != cudaSuccess) {
             freekv_destroy(h);
             return fail(FREEKV_ECUDA, std::string("occupancy query: ") + cudaGetErrorString(oe));
@@ -593,6 +613,20 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         long long T = std::min<long long>({(long long)warps, (long long)kMaxAttnWarps, V / minp, 254LL * D.U});
         while (T > 1 && T * V >= (1LL << 31)) T /= 2;
         h->D.attn_warps = (int)std::max(1LL, T);
+        h->D.attn_warps_p1 = h->D.attn_warps;
+        if (h->pipelined) {
+            // phase 1 runs on the SMs the one-CTA-per-unit select leaves free
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+            const int free_sms = sms - D.U;
+            if (free_sms < 16 || !select_c2_fits(h->D, h->lpt, 512)) {
+                h->pipelined = false;  // not enough room beside the select: sequential step
+            } else {
+                const long long T1 = std::min<long long>({(long long)free_sms * 8, (long long)kMaxAttnWarps, V,
+                                                          254LL * D.U});
+                h->D.attn_warps_p1 = (int)std::max(1LL, T1);
+            }
+        }
     }
     h->X.trace = nullptr;
     {
@@ -608,6 +642,8 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
     {
         const char* fr = getenv("FREEKV_DEBUG_FULL_REFRESH");
         h->D.full_refresh = (fr && fr[0] == '1') ? 1 : 0;
+        const char* dx = getenv("FREEKV_DEBUG_EXP");
+        h->D.dbg = dx ? atoi(dx) : 0;
     }
     {
         const char* sr = getenv("FREEKV_SERIAL_RECALL");

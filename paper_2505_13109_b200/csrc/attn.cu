@@ -292,8 +292,8 @@ __device__ __forceinline__ int phase_units(const FkvDims& D, const FkvLayer& L, 
 // half runs while the synchronous recall of the corrected units is in flight);
 // 2 = corrected units only (after that recall).  Each unit is attended in exactly
 // one phase, so every partial record is written once per step.
-template <int NST>
-__global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2) fkv_attn_split_kernel(FkvDims D, FkvLayer L, FkvScratch X,
+template <int NST, int WPC>
+__global__ void __launch_bounds__(WPC * 32, WPC == 8 ? 1 : (NST == 2 ? 3 : 2)) fkv_attn_split_kernel(FkvDims D, FkvLayer L, FkvScratch X,
                                                                                const uint16_t* __restrict__ q,
                                                                                int phase,
                                                                                const __grid_constant__ CUtensorMap tmap,
@@ -301,11 +301,11 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2) fkv_a
                                                                                const uint16_t* arena) {
     constexpr int kStages = NST;
     extern __shared__ __align__(1024) uint8_t s_stage[];  // [warps][kStages][8 KiB]
-    __shared__ __align__(8) uint64_t bar[kAttnWarpsPerCta][kStages];
+    __shared__ __align__(8) uint64_t bar[WPC][kStages];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
-    const int w = blockIdx.x * kAttnWarpsPerCta + warp;
-    const int T = D.attn_warps;
+    const int w = blockIdx.x * WPC + warp;
+    const int T = phase == 1 ? D.attn_warps_p1 : D.attn_warps;  // this launch's warps
     pdl_trigger();  // the next kernel (attention phase 2 / combine) may start its prologue
     if (w >= T) return;
     const int tcls = 4 + phase;  // trace class 4/5/6 = attention phase 0/1/2
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2) fkv_a
     const long long s0 = range_start(w, V, Tp), s1 = range_start(w + 1, V, Tp);
     int ua = -1, ub = -1;  // units of ranks s0 / P_max and s0 / P_max + 1
     if (s0 < s1) phase_units(D, L, phase, (int)(s0 / D.P_max), lane, ua, ub);
-    const int rec_base = phase == 2 ? T : 0;  // records of phase 2 live after phase 1's
+    const int rec_base = phase == 2 ? D.attn_warps_p1 : 0;  // records of phase 2 live after phase 1's
     int k_rec = 0;
     for (long long seg = s0; seg < s1; ++k_rec) {
         const int r = (int)(seg / D.P_max);
@@ -529,9 +529,10 @@ __global__ void __launch_bounds__(kCombThreads, 2) fkv_attn_combine_kernel(FkvDi
         }
     }
     __syncthreads();
-    const int rec_base = (split && my_flag) ? D.attn_warps : 0;
+    const int rec_base = (split && my_flag) ? D.attn_warps_p1 : 0;
     const unsigned V = (unsigned)(s_n * D.P_max);
-    const unsigned T = min((unsigned)D.attn_warps, V);  // the phase's warp count (see the split kernel)
+    const unsigned Tl = (split && !my_flag) ? (unsigned)D.attn_warps_p1 : (unsigned)D.attn_warps;  // the launch's warps
+    const unsigned T = min(Tl, V);  // the phase's warp count (see the split kernel)
     const unsigned x0 = (unsigned)s_rank * D.P_max, x1 = x0 + D.P_max;
     const int w_first = (int)(((x0 + 1) * T + V - 1) / V) - 1;
     const int w_last = (int)((x1 * T + V - 1) / V) - 1;
@@ -645,24 +646,32 @@ static int attn_stages() {
     return st;
 }
 
+template <int NST, int WPC>
+static cudaError_t attn_config() {
+    const int smem = WPC * NST * kSlabBytes;
+    cudaError_t e = cudaFuncSetAttribute(fkv_attn_split_kernel<NST, WPC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         smem);
+    // every kernel of the path prefers the max-shared carveout, so consecutive kernels never
+    // force an L1/shared-memory reconfiguration of the SMs
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(fkv_attn_split_kernel<NST, WPC>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared);
+    return e;
+}
+
 template <int NST>
 static cudaError_t attn_setup(int cps_want, int* warps) {
     const int smem = kAttnWarpsPerCta * NST * kSlabBytes;
     int dev = 0, sms = 0, per_sm = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(fkv_attn_split_kernel<NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    // every kernel of the path prefers the max-shared carveout, so consecutive kernels never
-    // force an L1/shared-memory reconfiguration of the SMs
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(fkv_attn_split_kernel<NST>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 cudaSharedmemCarveoutMaxShared);
+    if (e == cudaSuccess) e = attn_config<NST, 4>();
+    if (e == cudaSuccess) e = NST == 2 ? attn_config<2, 8>() : attn_config<3, 8>();
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(fkv_attn_combine_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared);
     if (e == cudaSuccess)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fkv_attn_split_kernel<NST>,
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fkv_attn_split_kernel<NST, 4>,
                                                           kAttnWarpsPerCta * 32, smem);
     // CTAs per SM (FREEKV_ATTN_CTAS_PER_SM overrides the caller's choice): 2 when the attention
     // runs alone (8 warps per SM hide the per-slab MMA/softmax latency); 1 in the pipelined
@@ -682,23 +691,24 @@ cudaError_t attn_resident_warps(int cps, int* warps) {
     }
 }
 
+// wpc = 8 (phase 1 of the overlapped step): one 8-warp CTA per SM, which cannot share an SM
+// with a select CTA, so the two kernels split the SMs between them
 cudaError_t launch_attn_split(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                               int phase, const CUtensorMap& tmap, const CUtensorMap& tmap_h, const uint16_t* arena,
-                              bool pdl, cudaStream_t s) {
-    const int ctas = (D.attn_warps + kAttnWarpsPerCta - 1) / kAttnWarpsPerCta;
+                              bool pdl, cudaStream_t s, int wpc) {
+    const int T = phase == 1 ? D.attn_warps_p1 : D.attn_warps;
     const int nst = attn_stages();
-    const int smem = kAttnWarpsPerCta * nst * kSlabBytes;
-    switch (nst) {
-        case 2:
-            return launch_ex(fkv_attn_split_kernel<2>, dim3(ctas), dim3(kAttnWarpsPerCta * 32), smem, s, pdl, D, L, X, q,
-                             phase, tmap, tmap_h, arena);
-        case 4:
-            return launch_ex(fkv_attn_split_kernel<4>, dim3(ctas), dim3(kAttnWarpsPerCta * 32), smem, s, pdl, D, L, X, q,
-                             phase, tmap, tmap_h, arena);
-        default:
-            return launch_ex(fkv_attn_split_kernel<3>, dim3(ctas), dim3(kAttnWarpsPerCta * 32), smem, s, pdl, D, L, X, q,
-                             phase, tmap, tmap_h, arena);
+#define FKV_ATTN(NS, W)                                                                                         \
+    return launch_ex(fkv_attn_split_kernel<NS, W>, dim3((T + W - 1) / W), dim3(W * 32), W * NS * kSlabBytes, s, \
+                     pdl, D, L, X, q, phase, tmap, tmap_h, arena)
+    if (wpc == 8) {
+        if (nst == 2) FKV_ATTN(2, 8);
+        FKV_ATTN(3, 8);
     }
+    if (nst == 2) FKV_ATTN(2, 4);
+    if (nst == 4) FKV_ATTN(4, 4);
+    FKV_ATTN(3, 4);
+#undef FKV_ATTN
 }
 
 cudaError_t launch_attn_combine(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,

@@ -26,11 +26,14 @@ struct FkvDims {
     int U;            // nb * n_kv
     int mode;
     int full_refresh; // diagnostics (env FREEKV_DEBUG_FULL_REFRESH=1): no slot reuse, all pages re-fetched
+    int dbg;          // timing experiments only (env FREEKV_DEBUG_EXP, bit flags; results not valid)
     float tau;
     float score_r;    // CFR-3: fl32(log2(e)/sqrt(d))
     float attn_c;     // log2(e)/sqrt(d) for attention softmax (not CFR)
     int P_max;        // upper bound of attention pages per unit: n_sink + K + R_loc
     int attn_warps;   // T: warps of the balanced split-KV attention grid (<= resident warps)
+    int attn_warps_p1;  // T of attention phase 1 (units attending R) -- smaller in the overlapped
+                        // step, where it runs beside the select on the SMs the select leaves free
     int direct;       // 1: corrected units' fetched pages are read by the attention kernel straight
                       // from the host pool (and written back to their slots); 0: synchronous recall
                       // before a second attention phase
@@ -139,6 +142,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// Warp-wide max of a float (exact, order-free): one redux.sync (sm_100a)
+__device__ __forceinline__ float warp_max_f32(float v) {
+    float r;
+    asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+    return r;
+}
+
 // CFR-10 for one head: sequential fp32 channel sums of x*y, x*x and y*y over d = 128
 // bf16 channels (fma = exact product + one rounding), then dot / (sqrt(n1) * sqrt(n2)),
 // 0 when either norm is 0.  All 2 x 256 bytes are loaded first (16-byte vectors), so the
@@ -198,19 +208,24 @@ cudaError_t launch_summarize(const FkvDims& D, const FkvLayer& L, int page_begin
 cudaError_t launch_score(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                          int max_n_off, int pending, int which, bool pdl, cudaStream_t s);
 cudaError_t launch_prep(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                        const uint16_t* k_new, const uint16_t* v_new, uint8_t* corrected_out, cudaStream_t s);
+                        const uint16_t* k_new, const uint16_t* v_new, uint8_t* corrected_out, bool pdl,
+                        cudaStream_t s);
 cudaError_t launch_select_fused(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                                 const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
                                 uint8_t* corrected_out, int cluster, int lptm, cudaStream_t s);
 cudaError_t launch_finalize(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                             const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
                             uint8_t* corrected_out, int lpt, int nt, bool pdl, int which, cudaStream_t s);
+bool select_c2_fits(const FkvDims& D, int lpt, int nt);
+cudaError_t launch_select_c2(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
+                             const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
+                             uint8_t* corrected_out, int lpt, int nt, int cl, bool pdl, int which, cudaStream_t s);
 cudaError_t launch_recall(const FkvDims& D, const FkvLayer& L, int sync_mode, cudaStream_t s,
                           unsigned long long* trace = nullptr);
 cudaError_t attn_resident_warps(int cps, int* warps);  // warps of the split kernel's grid (cps CTAs per SM)
 cudaError_t launch_attn_split(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                               int phase, const CUtensorMap& tmap, const CUtensorMap& tmap_host,
-                              const uint16_t* arena, bool pdl, cudaStream_t s);
+                              const uint16_t* arena, bool pdl, cudaStream_t s, int wpc = 4);
 // commit: 0 = every unit (R := S_i, q_prev := q_i), 2 = corrected units only (pipelined step:
 // the background select kernel commits the others)
 cudaError_t launch_attn_combine(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,

@@ -12,10 +12,14 @@
 // Every floating-point step that decides an index follows the canonical fp32
 // recipe with explicit round-to-nearest intrinsics, so the page
 // indices are bit-identical to the CPU oracle.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cstdlib>
 
 #include "append_unit.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace fkv {
 
@@ -197,7 +201,11 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
                                               const float* __restrict__ scores, const uint16_t* __restrict__ q,
                                               const uint16_t* __restrict__ k_new,
                                               const uint16_t* __restrict__ v_new, int32_t* __restrict__ pages_out,
-                                              uint8_t* __restrict__ corrected_out, int which) {
+                                              uint8_t* __restrict__ corrected_out, int which,
+                                              const float* ssc = nullptr, const float* cos_in = nullptr) {
+    // ssc != NULL: the scores are already in shared memory ([G][n_page_max], fused select);
+    // cos_in != NULL (fused select, which == 0): the helper CTA has done the correction check
+    // (cos_in = per-head cosines in this CTA's shared memory) and the append of this step's token
     constexpr int kThreads = NT, kWarps = NT / 32;
     const int b = u / D.n_kv, m = u % D.n_kv, G = D.G;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -230,38 +238,25 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
     if (tid == 0) trace_stamp(trace, tcls, u, 0);
     pdl_trigger();  // attention may start its prologue
     const int pre_flag = which ? (int)L.flags[u] : 0;
-    // ---- a9 (fused, decode path): append this step's token.  Runs while the score kernel
-    // drains (PDL): it only touches the ring / the page completing now (not a candidate of
-    // this step) / the host pool; ctx and n_off are published after pdl_wait().
     int n_off = L.n_off[u];
-    int Lc_now = L.ctx[u];
-    if (k_new) {
-        const int ctx0 = Lc_now;
-        Lc_now = ctx0 + 1;
-        append_unit(D, L, u, ctx0, k_new, v_new, 1, s_page);
-        n_off = max(n_off, frontier_for(D, ctx0 + 1));
-    }
+    const int ctx0 = L.ctx[u];
+    const int Lc_now = ctx0 + (k_new ? 1 : 0);
+    if (k_new) n_off = max(n_off, frontier_for(D, Lc_now));
     const int n_cand = n_off - n_sink;
     const bool rank_all = n_cand <= K;  // A-11: all candidates selected, no ranking
     if (tid == 0) trace_stamp(trace, tcls, u, 1);
 
     // ---- a1: correction (CFR-10), which == 0 only: lanes 0..G-1 of the last warp run the
     // sequential channel sums before the scores arrive
-    const bool cos_lane = which == 0 && warp == kWarps - 1 && lane < G;
+    const bool cos_lane = which == 0 && warp == kWarps - 1 && lane < G && !(D.dbg & 1);
     auto cos_all = [&]() {
         s_cos[lane] = cos_cfr10(reinterpret_cast<const uint16_t*>(s_qa) + lane * kHeadDim,
                                 reinterpret_cast<const uint16_t*>(s_qb) + lane * kHeadDim);
     };
 
-    // ---- stage everything the CTA reads (one round trip): q_i, q_{i-1}, resident set
-    if (which == 0) {
-        const uint32_t* qa32 = reinterpret_cast<const uint32_t*>(q + ((size_t)b * D.n_qo + m * G) * kHeadDim);
-        const uint32_t* qb32 = reinterpret_cast<const uint32_t*>(L.q_prev + ((size_t)b * D.n_qo + m * G) * kHeadDim);
-        for (int i = tid; i < G * kHeadDim / 2; i += kThreads) {
-            s_qa[i] = qa32[i];
-            s_qb[i] = qb32[i];
-        }
-    }
+    // ---- stage the state this CTA reads (one round trip): resident set.  Step inputs (q_i,
+    // the new token) are read only after pdl_wait(): with PDL this kernel may start before
+    // the previous layer's last kernel has completed (its prologue overlaps it)
     // debug mode 3 (FREEKV_DEBUG_FULL_REFRESH): forget the resident set every step, so every
     // unit re-fetches all K pages synchronously -- the GEN-X recall-bandwidth stress case
     const int res_valid = D.full_refresh ? 0 : L.res_valid[u];
@@ -276,17 +271,38 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
     if (tid == 0) s_bn = 0;
     const size_t srow = (size_t)D.n_page_max;
     __syncthreads();  // staging visible
-    // work that needs no scores runs while the score kernel drains (PDL): the resident set's
-    // page -> index table and used-slot map, and (which == 0) the correction check
+    // the resident set's page -> index table and used-slot map (no scores needed)
     if (tid < K && s_res[tid] >= 0) {
         s_idx[s_res[tid]] = (uint16_t)tid;
         s_used[s_res_slot[tid]] = 1;
     }
-    if (cos_lane) cos_all();
-    pdl_wait();  // the score kernel has completed: its scores are visible, ctx may be published
-    if (k_new && tid == 0) {
-        L.ctx[u] = Lc_now;
-        L.n_off[u] = n_off;
+    pdl_wait();  // the previous kernel (score) has completed: scores and step inputs are ready
+    // ---- step inputs: q_i, q_{i-1} (correction check), and the fused append (row a9) of this
+    // step's token -- it only touches the ring / the page completing now (not a candidate of
+    // this step) / the host pool
+    if (cos_in) {
+        if (tid < G) s_cos[tid] = cos_in[tid];  // visible to warp 0 after the barriers below
+    } else {
+        if (which == 0) {
+            const uint32_t* qa32 = reinterpret_cast<const uint32_t*>(q + ((size_t)b * D.n_qo + m * G) * kHeadDim);
+            const uint32_t* qb32 =
+                reinterpret_cast<const uint32_t*>(L.q_prev + ((size_t)b * D.n_qo + m * G) * kHeadDim);
+            for (int i = tid; i < G * kHeadDim / 2; i += kThreads) {
+                s_qa[i] = qa32[i];
+                s_qb[i] = qb32[i];
+            }
+        }
+        if (k_new) {
+            append_unit(D, L, u, ctx0, k_new, v_new, 1, s_page);
+            if (tid == 0) {
+                L.ctx[u] = Lc_now;
+                L.n_off[u] = n_off;
+            }
+        }
+        if (which == 0) {
+            __syncthreads();  // s_qa / s_qb staged
+            if (cos_lane) cos_all();
+        }
     }
     int cnt;
     if (rank_all) {
@@ -305,29 +321,23 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
 #pragma unroll
         for (int g = 0; g < GM; ++g)
 #pragma unroll
-            for (int l = 0; l < LPT; ++l) sv[g][l] = (g < G && cand[l]) ? sg[g * srow + jb + l] : -INFINITY;
-        // ---- CFR-4: max per head (exact, order-free); the G heads' shuffles interleave
+            for (int l = 0; l < LPT; ++l)
+                sv[g][l] = (g < G && cand[l]) ? (ssc ? ssc[g * srow + jb + l] : sg[g * srow + jb + l]) : -INFINITY;
+        // ---- CFR-4: max per head (exact, order-free): one warp-wide redux per head, twice
         float M[GM];
 #pragma unroll
         for (int g = 0; g < GM; ++g) {
             M[g] = sv[g][0];
 #pragma unroll
             for (int l = 1; l < LPT; ++l) M[g] = fmaxf(M[g], sv[g][l]);
+            M[g] = warp_max_f32(M[g]);
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-            for (int g = 0; g < GM; ++g) M[g] = fmaxf(M[g], __shfl_xor_sync(0xffffffffu, M[g], o));
         if (lane == 0)
 #pragma unroll
             for (int g = 0; g < GM; ++g) s_redm[warp][g] = M[g];
         __syncthreads();
 #pragma unroll
-        for (int g = 0; g < GM; ++g) M[g] = lane < kWarps ? s_redm[lane][g] : -INFINITY;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-            for (int g = 0; g < GM; ++g) M[g] = fmaxf(M[g], __shfl_xor_sync(0xffffffffu, M[g], o));
+        for (int g = 0; g < GM; ++g) M[g] = warp_max_f32(lane < kWarps ? s_redm[lane][g] : -INFINITY);
         // ---- CFR-5/6: e = cexp2(s - m); Z = pairwise tree in page-id order: thread-local tree over
         // its LPT contiguous leaves, xor butterfly over the 32 lanes, butterfly over the warp
         // partials (lanes >= kWarps hold +0 leaves, which leave a pairwise tree's value unchanged)
@@ -356,10 +366,15 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
         __syncthreads();
 #pragma unroll
         for (int g = 0; g < GM; ++g) Z[g] = lane < kWarps ? s_redz[lane][g] : 0.0f;
+        // the warp partials occupy lanes [0, kWarps): log2(kWarps) butterfly levels build their
+        // pairwise tree (the padded lanes would only add +0)
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1)
+        for (int o = 1; o < kWarps; o <<= 1)
 #pragma unroll
             for (int g = 0; g < GM; ++g) Z[g] = __fadd_rn(Z[g], __shfl_xor_sync(0xffffffffu, Z[g], o));
+        if (kWarps < 32)
+#pragma unroll
+            for (int g = 0; g < GM; ++g) Z[g] = __shfl_sync(0xffffffffu, Z[g], 0);
         if (tid == 0) trace_stamp(trace, tcls, u, 3);
         // ---- CFR-7/8: p = e / Z; pooled = sequential sum over g; CFR-9 keys
         uint32_t key[LPT];
@@ -689,12 +704,14 @@ __global__ void __launch_bounds__(kPrepThreads) fkv_prep_kernel(FkvDims D, FkvLa
     __shared__ int s_flag;
     const int u = blockIdx.x, b = u / D.n_kv, m = u % D.n_kv, G = D.G, tid = threadIdx.x;
     if (tid == 0) trace_stamp(X.trace, 8, u, 0);
-    // every load of the kernel is issued up front (one round trip)
+    pdl_trigger();
+    // state loads first (with PDL they overlap the previous layer's last kernel) ...
     const int L0 = L.ctx[u];
     int n_off = L.n_off[u];
     const int res_valid = D.full_refresh ? 0 : L.res_valid[u];
     const int res_front = L.res_front[u], res_cnt = L.res_cnt[u];
     const int my_slot = tid < D.K ? L.res_slot[(size_t)u * D.K + tid] : 0;
+    pdl_wait();  // ... step inputs (q_i, the new token) only after the previous layer has completed
     {
         const uint32_t* qa32 = reinterpret_cast<const uint32_t*>(q + ((size_t)b * D.n_qo + m * G) * kHeadDim);
         const uint32_t* qb32 = reinterpret_cast<const uint32_t*>(L.q_prev + ((size_t)b * D.n_qo + m * G) * kHeadDim);
@@ -775,7 +792,8 @@ __global__ void __launch_bounds__(kPrepThreads) fkv_prep_kernel(FkvDims D, FkvLa
 }
 
 cudaError_t launch_prep(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                        const uint16_t* k_new, const uint16_t* v_new, uint8_t* corrected_out, cudaStream_t s) {
+                        const uint16_t* k_new, const uint16_t* v_new, uint8_t* corrected_out, bool pdl,
+                        cudaStream_t s) {
     const size_t smem = page_elems(D) * sizeof(uint16_t);
     static size_t configured = 0;
     if (smem > configured) {
@@ -786,8 +804,8 @@ cudaError_t launch_prep(const FkvDims& D, const FkvLayer& L, const FkvScratch& X
         if (e != cudaSuccess) return e;
         configured = smem;
     }
-    fkv_prep_kernel<<<D.U, kPrepThreads, smem, s>>>(D, L, X, q, k_new, v_new, corrected_out);
-    return cudaGetLastError();
+    return launch_ex(fkv_prep_kernel, dim3(D.U), dim3(kPrepThreads), smem, s, pdl, D, L, X, q, k_new, v_new,
+                     corrected_out);
 }
 
 template <int G>
@@ -822,6 +840,227 @@ cudaError_t launch_score(const FkvDims& D, const FkvLayer& L, const FkvScratch& 
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
+}
+
+// ------------------------------------------- fused select: score + select, 2-CTA cluster
+// One cluster of two 1024-thread CTAs per unit.  Both CTAs stream half of the unit's
+// candidate summary blocks through a 2-deep ring of 4 KiB chunks (16 scoring warps, chunks
+// of this step in flight before the previous kernel has finished -- summaries are state,
+// not step input) and score them (CFR-2/3, the same arithmetic as fkv_score_kernel) into
+// the leader CTA's shared memory (DSMEM stores); after one cluster barrier the helper
+// exits and the leader runs the select on the scores in shared memory.  Removes the
+// score kernel's launch, its global score round trip and the score -> select boundary.
+constexpr int kFusedScoreWarps = 16;
+constexpr int kFusedRing = 2;
+
+__host__ __device__ inline size_t fused_off_sc(const FkvDims& D) {
+    return (page_elems(D) * 2 + (size_t)D.n_page_max * 2 + 15) / 16 * 16;
+}
+__host__ __device__ inline size_t fused_off_ring(const FkvDims& D) {
+    return (fused_off_sc(D) + (size_t)D.G * D.n_page_max * 4 + 127) / 128 * 128;
+}
+__host__ __device__ inline size_t fused_smem_bytes(const FkvDims& D) {  // + kMaxG floats (helper cosines)
+    return fused_off_ring(D) + (size_t)kFusedScoreWarps * kFusedRing * kChunkBytes;
+}
+
+template <int LPT, int GM, int NT, int CL>
+__global__ void __launch_bounds__(NT)
+    fkv_select_c2_kernel(FkvDims D, FkvLayer L, int32_t* __restrict__ page_rows, uint8_t* __restrict__ page_valid,
+                         int32_t* __restrict__ page_dst, int32_t* __restrict__ page_cnt,
+                         unsigned long long* __restrict__ trace, const uint16_t* __restrict__ q,
+                         const uint16_t* __restrict__ k_new, const uint16_t* __restrict__ v_new,
+                         int32_t* __restrict__ pages_out, uint8_t* __restrict__ corrected_out, int which) {
+    constexpr int GP = (GM + 3) / 4 * 4;
+    extern __shared__ __align__(16) uint8_t s_dyn[];
+    __shared__ __align__(16) float qv[kHeadDim][GP];
+    __shared__ __align__(16) uint32_t qm[kHeadDim][GP];
+    __shared__ __align__(8) uint64_t bar[kFusedScoreWarps][kFusedRing];
+    const int rank = CL == 2 ? (int)cg::this_cluster().block_rank() : 0;
+    const int u = CL == 2 ? (blockIdx.x >> 1) : blockIdx.x, b = u / D.n_kv, m = u % D.n_kv, G = D.G;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    float* s_sc = reinterpret_cast<float*>(s_dyn + fused_off_sc(D));
+    uint8_t* ring = s_dyn + fused_off_ring(D) + (size_t)warp * kFusedRing * kChunkBytes;
+    pdl_trigger();
+    // ---- this CTA's summary blocks (state: readable before pdl_wait)
+    const int ctx0 = L.ctx[u];
+    const int n_off = max(L.n_off[u], frontier_for(D, ctx0 + (k_new ? 1 : 0)));
+    const int blk_lo = D.n_sink >> 5;
+    const int nblk = n_off > D.n_sink ? ((n_off - 1) >> 5) - blk_lo + 1 : 0;
+    const int half = CL == 2 ? (nblk + 1) >> 1 : nblk;
+    const int my0 = rank ? half : 0, my1 = rank ? nblk : half;
+    const int nmine = my1 - my0;
+    // chunk c (0..) of warp w: block my0 + w + 16 * (c >> 2), channel group c & 3
+    constexpr int kSW = NT / 32 < kFusedScoreWarps ? NT / 32 : kFusedScoreWarps;  // scoring warps
+    const bool scorer = warp < kSW && warp < nmine;
+    const int nchunks = scorer ? ((nmine - warp + kSW - 1) / kSW) * 4 : 0;
+    auto chunk_src = [&](int c) {
+        const int blk = blk_lo + my0 + warp + kSW * (c >> 2);
+        return reinterpret_cast<const uint8_t*>(L.summ + summ_chunk_offset(D, u, blk * 32, 0, 0)) +
+               (size_t)(c & 3) * kChunkBytes;
+    };
+    if (scorer && lane == 0) {
+#pragma unroll
+        for (int r = 0; r < kFusedRing; ++r) mbar_init(&bar[warp][r], 1);
+        fence_mbar_init();
+        for (int c = 0; c < kFusedRing && c < nchunks; ++c) {
+            mbar_expect_tx(&bar[warp][c], kChunkBytes);
+            bulk_g2s(ring + c * kChunkBytes, chunk_src(c), kChunkBytes, &bar[warp][c]);
+        }
+    }
+    pdl_wait();  // step inputs (q_i) are ready
+    float* s_cosx = reinterpret_cast<float*>(s_dyn + fused_smem_bytes(D));  // [kMaxG] helper -> leader
+    const bool helped = CL == 2 && which == 0 && !(D.dbg & 2);  // FREEKV_DEBUG_EXP bit 1: off (A/B)
+    if (CL == 2 && rank == 1 && helped) {
+        // the helper CTA takes the leader's prologue: the correction check (CFR-10) on lanes
+        // 0..G-1 of its last warp, and the append of this step's token (row a9), while its
+        // first summary chunks are in flight
+        if (warp == NT / 32 - 1 && lane < G) {
+            const size_t row = ((size_t)b * D.n_qo + m * G + lane) * kHeadDim;
+            *cg::this_cluster().map_shared_rank(&s_cosx[lane], 0) = cos_cfr10(q + row, L.q_prev + row);
+        }
+        if (k_new) {
+            append_unit(D, L, u, ctx0, k_new, v_new, 1, reinterpret_cast<uint4*>(s_dyn));
+            if (tid == 0) {
+                L.ctx[u] = ctx0 + 1;
+                L.n_off[u] = n_off;
+            }
+        }
+    }
+    for (int i = tid; i < GP * kHeadDim; i += blockDim.x) {
+        const int h = i / kHeadDim, c = i % kHeadDim;
+        float x = 0.0f;
+        if (h < G) x = bf16f(q[((size_t)b * D.n_qo + m * G + h) * kHeadDim + c]);
+        qv[c][h] = x;
+        qm[c][h] = x >= 0.0f ? 0xffffffffu : 0u;  // CFR-2: q_c >= 0 (incl. -0) uses the max
+    }
+    __syncthreads();
+    float* dst_sc = s_sc;  // scores land in the leader
+    if (CL == 2 && rank) dst_sc = cg::this_cluster().map_shared_rank(s_sc, 0);
+    if (scorer) {
+        float acc[GM];
+        int cur_blk = -1;
+        for (int c = 0; c < nchunks; ++c) {
+            const int slot = c % kFusedRing;
+            if ((c & 3) == 0) {
+#pragma unroll
+                for (int h = 0; h < GM; ++h) acc[h] = 0.0f;
+                cur_blk = blk_lo + my0 + warp + kSW * (c >> 2);
+            }
+            mbar_wait(&bar[warp][slot], (uint32_t)(c / kFusedRing) & 1u);
+            score_channels<GM>(reinterpret_cast<const uint4*>(ring + slot * kChunkBytes) - ((c & 3) * 4) * 2 * 32,
+                               (c & 3) * 4, lane, qv, qm, acc);
+            __syncwarp();  // every lane is done with this slot
+            if (c + kFusedRing < nchunks && lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(&bar[warp][slot], kChunkBytes);
+                bulk_g2s(ring + slot * kChunkBytes, chunk_src(c + kFusedRing), kChunkBytes, &bar[warp][slot]);
+            }
+            if ((c & 3) == 3) {
+                const int j = cur_blk * 32 + lane;
+                if (j >= D.n_sink && j < n_off) {
+#pragma unroll
+                    for (int h = 0; h < GM; ++h)
+                        if (h < G) dst_sc[(size_t)h * D.n_page_max + j] = __fmul_rn(acc[h], D.score_r);  // CFR-3
+                }
+            }
+        }
+    }
+    if (CL == 2) {
+        cg::this_cluster().sync();  // every score is in the leader's shared memory
+        if (rank) return;
+    } else {
+        __syncthreads();
+    }
+    // helped: the append (ctx / n_off already published, visible after the cluster barrier)
+    // and the correction check were done by the helper CTA
+    finalize_unit<LPT, GM, NT>(u, D, L, page_rows, page_valid, page_dst, page_cnt, trace, nullptr, q,
+                               helped ? nullptr : k_new, helped ? nullptr : v_new, pages_out, corrected_out, which,
+                               s_sc, helped ? s_cosx : nullptr);
+}
+
+template <int LPT, int GM, int NT, int CL>
+static cudaError_t launch_c2_g(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
+                               const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
+                               uint8_t* corrected_out, bool pdl, int which, cudaStream_t s) {
+    auto kern = fkv_select_c2_kernel<LPT, GM, NT, CL>;
+    const size_t smem = fused_smem_bytes(D) + kMaxG * sizeof(float);
+    static size_t configured = 0;
+    if (smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL * D.U);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (CL > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = CL;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    if (pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = na ? attr : nullptr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, kern, D, L, X.page_rows, X.page_valid, X.page_dst, X.page_cnt, X.trace, q, k_new,
+                              v_new, pages_out, corrected_out, which);
+}
+
+// Fused score + select (2-CTA clusters).  Returns cudaErrorNotSupported when the handle's
+// shapes do not fit (caller falls back to score + select).
+bool select_c2_fits(const FkvDims& D, int lpt, int nt) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const size_t static_est = 40 * 1024;  // finalize_unit + scoring statics (upper bound)
+    const bool lpt_ok = nt == 1024 ? lpt <= 2 : (nt == 512 ? lpt <= 4 : (nt == 256 && lpt >= 2 && lpt <= 8));
+    return lpt_ok && fused_smem_bytes(D) + static_est <= (size_t)optin;
+}
+
+// lpt = leaves per thread for nt threads (nt * lpt >= the tree size); nt in {256, 512, 1024}
+cudaError_t launch_select_c2(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
+                             const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
+                             uint8_t* corrected_out, int lpt, int nt, int cl, bool pdl, int which, cudaStream_t s) {
+#define FKV_C2C(LP, GMV, N)                                                                                       \
+    do {                                                                                                         \
+        if (cl == 1)                                                                                             \
+            return launch_c2_g<LP, GMV, N, 1>(D, L, X, q, k_new, v_new, pages_out, corrected_out, pdl, which, s); \
+        return launch_c2_g<LP, GMV, N, 2>(D, L, X, q, k_new, v_new, pages_out, corrected_out, pdl, which, s);     \
+    } while (0)
+#define FKV_C2G(LP, N)                       \
+    do {                                     \
+        if (D.G <= 1) FKV_C2C(LP, 1, N);     \
+        if (D.G <= 2) FKV_C2C(LP, 2, N);     \
+        if (D.G <= 4) FKV_C2C(LP, 4, N);     \
+        FKV_C2C(LP, 8, N);                   \
+    } while (0)
+    if (nt == 1024) {
+        if (lpt == 1) FKV_C2G(1, 1024);
+        if (lpt == 2) FKV_C2G(2, 1024);
+    } else if (nt == 512) {
+        if (lpt == 1) FKV_C2G(1, 512);
+        if (lpt == 2) FKV_C2G(2, 512);
+        if (lpt == 4) FKV_C2G(4, 512);
+    } else if (nt == 256) {
+        if (lpt == 2) FKV_C2G(2, 256);
+        if (lpt == 4) FKV_C2G(4, 256);
+        if (lpt == 8) FKV_C2G(8, 256);
+    }
+#undef FKV_C2G
+#undef FKV_C2C
+    return cudaErrorNotSupported;
 }
 
 // GM = group-size bucket (1, 2, 4, 8) >= G: the per-head loops and shuffles run GM wide

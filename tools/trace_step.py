@@ -71,4 +71,7 @@ for i, l in steps():
                         "median_stamps_rel_start_us": [round(float(np.median(np.where(ents[:, j] > 0, ents[:, j] - ents[:, 0], np.nan)[~np.isnan(np.where(ents[:, j] > 0, ents[:, j] - ents[:, 0], np.nan))]) / 1000.0), 2) if (ents[:, j] > 0).any() else None for j in range(1, 8)],
                         "max_span_us": round(float((last - ents[:, 0]).max() / 1000.0), 2)}
         res[f"step{i}_layer{l}"] = step
+        if i == 9 and "--dump" in sys.argv:  # raw stamps of this step for offline analysis
+            sel = fkv.get_selection(l)
+            np.savez(os.path.join(ROOT, "gpurun_out", "trace_raw.npz"), tr=tr, t0=t0, flags=sel["flags"])
 print(json.dumps(res, indent=1))
