@@ -54,6 +54,7 @@ struct freekv_handle {
     std::vector<cudaEvent_t> ev_select, ev_recall, ev_sync, ev_sync_x, ev_pre, ev_fl;
     bool pipelined = false;      // overlapped step (FREEKV_PIPELINE=1; needs direct mode)
     bool one_graph = false;      // direct mode: recalls are forked branches of the one step graph
+    int attn_cluster = 0;        // CTAs per unit of the clustered attention (0: split + combine kernels)
     std::vector<int> ctx_host;
     std::vector<int> recall_pending;
     int lpt = 1, lpt1k = 1;  // leaves per thread of the 512 / 1024-thread select tree (fixed per handle, CFR-6)
@@ -294,6 +295,13 @@ freekv_status do_recall(freekv_handle* h, int layer, cudaStream_t s) {
 
 freekv_status do_attn(freekv_handle* h, int layer, const void* q, float* out, cudaStream_t s) {
     if (!q || !out) return fail(FREEKV_EINVAL, "q/out is NULL");
+    if (h->attn_cluster) {
+        FKV_CUDA(timed(h, K_ATTN_SPLIT, s, [&] {
+            return launch_attn_cluster(h->D, h->layers[layer], h->X, (const uint16_t*)q, out, 0, h->tmap_kv,
+                                       h->tmap_host, 0, h->attn_cluster, false, s);
+        }));
+        return FREEKV_OK;
+    }
     FKV_CUDA(timed(h, K_ATTN_SPLIT, s, [&] {
         return launch_attn_split(h->D, h->layers[layer], h->X, (const uint16_t*)q, 0, h->tmap_kv, h->tmap_host,
                                  h->arena, false, s);
@@ -320,13 +328,20 @@ freekv_status do_step_tail(freekv_handle* h, int layer, const void* q, float* ou
     const FkvDims& D = h->D;
     FkvLayer& L = h->layers[layer];
     if (D.direct) {
-        FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] {
-            return launch_attn_split(D, L, h->X, (const uint16_t*)q, 0, h->tmap_kv, h->tmap_host, h->arena, h->pdl,
-                                     cs);
-        }));
-        FKV_CUDA(timed(h, K_ATTN_COMBINE, cs, [&] {
-            return launch_attn_combine(D, L, h->X, (const uint16_t*)q, out, 0, 0, h->pdl, cs);
-        }));
+        if (h->attn_cluster) {  // attention + merge + commit in one launch (clusters per unit)
+            FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] {
+                return launch_attn_cluster(D, L, h->X, (const uint16_t*)q, out, 0, h->tmap_kv, h->tmap_host, 0,
+                                           h->attn_cluster, h->pdl, cs);
+            }));
+        } else {
+            FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] {
+                return launch_attn_split(D, L, h->X, (const uint16_t*)q, 0, h->tmap_kv, h->tmap_host, h->arena,
+                                         h->pdl, cs);
+            }));
+            FKV_CUDA(timed(h, K_ATTN_COMBINE, cs, [&] {
+                return launch_attn_combine(D, L, h->X, (const uint16_t*)q, out, 0, 0, h->pdl, cs);
+            }));
+        }
         // the background recall of this layer starts after its attention (an event node between
         // select and attention would break their PDL edge, and the host link is then free for
         // the attention's own host reads); it overlaps the next layers
@@ -614,6 +629,16 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         while (T > 1 && T * V >= (1LL << 31)) T /= 2;
         h->D.attn_warps = (int)std::max(1LL, T);
         h->D.attn_warps_p1 = h->D.attn_warps;
+        {
+            // clustered attention (direct mode): C CTAs per unit, the largest power of two <= 8
+            // with U * C within one wave of 2 CTAs per SM (FREEKV_ATTN=split: two kernels)
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+            const char* ae = getenv("FREEKV_ATTN");
+            int c = 8;
+            while (c > 1 && D.U * c > 2 * sms) c >>= 1;
+            h->attn_cluster = (h->D.direct && !(ae && ae[0] == 's')) ? c : 0;
+        }
         if (h->pipelined) {
             // phase 1 runs on the SMs the one-CTA-per-unit select leaves free
             int sms = 148;

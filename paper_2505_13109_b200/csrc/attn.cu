@@ -25,10 +25,14 @@
 // each warp always has 8 KiB in flight.  P is split into bf16 hi + lo parts
 // (two PV MMAs) so its rounding stays ~2^-17, far inside the 2e-3 output
 // tolerance (readings A-19/A-21).
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cstdlib>
 
 #include "fkv_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace fkv {
 
@@ -254,6 +258,97 @@ __device__ __forceinline__ void compute_slab(const uint8_t* st, int valid, const
     }
 }
 
+// Attend pages [pa, pb) of unit u's page list (sink, selected/resident, local; written by
+// the select or prep kernel): online softmax over every token of those pages into
+// (m_run, l_run, oacc) -- lane (g, t) holds heads 2t, 2t+1.  One warp; ring/bar are the
+// warp's NST slab stages, phase_bits their parities (carried across calls).
+template <int NST>
+__device__ __forceinline__ void attend_pages(const FkvDims& D, const FkvScratch& X, const uint16_t* __restrict__ q,
+                                             const CUtensorMap* tmap_p, const CUtensorMap* tmap_hp, int u, int pa,
+                                             int pb_cap, uint8_t* ring, uint64_t* bars, uint32_t& phase_bits,
+                                             float (&m_run)[2], float (&l_run)[2], float (&oacc)[8][4], int tcls,
+                                             int w) {
+    constexpr int kStages = NST;
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int G = D.G, spp = D.p >> 4, lspp = spp == 1 ? 0 : (spp == 2 ? 1 : 2);
+    const float sc = D.attn_c;
+    const CUtensorMap& tmap = *tmap_p;
+    const CUtensorMap& tmap_h = *tmap_hp;
+    const int32_t* prow = X.page_rows + (size_t)u * D.P_max;  // written by the select kernel
+    const int pb = min(pb_cap, X.page_cnt[u]);
+    const int b = u / D.n_kv, m = u % D.n_kv;
+    // Q fragments: lane (g, t) holds Q[head g][64b + 16t + 8e .. +8] (heads >= G are zero)
+    uint4 qa[2][2];
+    {
+        const bool hv = g < G;
+        const uint16_t* qrow = q + ((size_t)b * D.n_qo + m * G + (hv ? g : 0)) * kHeadDim;
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+                qa[bb][e] = hv ? *reinterpret_cast<const uint4*>(qrow + 64 * bb + 16 * t + 8 * e)
+                               : make_uint4(0u, 0u, 0u, 0u);
+    }
+    // the segment's pages in chunks of <= 32 (one page-table entry per lane)
+    for (int cb = pa; cb < pb; cb += 32) {
+        const int np = min(32, pb - cb);
+        // page table of the segment, one page per lane: first K row in the arena tensor and
+        // valid tokens -- one batch of independent loads instead of a dependent load per slab
+        int my_row = 0, my_valid = 0, my_dst = 0;
+        if (lane < np) {
+            my_row = prow[cb + lane];
+            my_valid = X.page_valid[(size_t)u * D.P_max + cb + lane];
+            if (my_valid & 0x80) my_dst = X.page_dst[(size_t)u * D.P_max + cb + lane];
+        }
+        const unsigned host_mask = __ballot_sync(0xffffffffu, my_valid & 0x80);  // pages read from the host pool
+        const int nx = np * spp;
+        if (lane == 0) trace_stamp(X.trace, tcls, w, 1);
+        auto slab_of = [&](int x, int& row) {  // warp-uniform; spp = 1 << lspp
+            const int pi = x >> lspp, sl = x & (spp - 1);
+            row = __shfl_sync(0xffffffffu, my_row, pi) + sl * 16;
+            return (__shfl_sync(0xffffffffu, my_valid, pi) & 0x7f) - sl * 16;
+        };
+        auto is_host = [&](int x) { return (host_mask >> (x >> lspp)) & 1u; };
+        // prologue: first kStages slabs of this segment in flight
+        int rows[kStages], valids[kStages];
+#pragma unroll
+        for (int i = 0; i < kStages; ++i) valids[i] = i < nx ? slab_of(i, rows[i]) : 0;
+        if (lane == 0) {
+#pragma unroll
+            for (int i = 0; i < kStages; ++i)
+                if (valids[i] > 0)
+                    issue_slab(is_host(i) ? &tmap_h : &tmap, ring + i * kSlabBytes, &bars[i], rows[i], D.p);
+        }
+        for (int i = 0; i < nx; ++i) {
+            const int stg = i % kStages;
+            int row;
+            const int valid = slab_of(i, row);
+            int row2 = 0, valid2 = 0;
+            if (i + kStages < nx) valid2 = slab_of(i + kStages, row2);
+            const int dst = host_mask ? __shfl_sync(0xffffffffu, my_dst, i >> lspp) + (i & (spp - 1)) * 16 : 0;
+            if (valid > 0) {
+                mbar_wait(&bars[stg], (phase_bits >> stg) & 1u);
+                phase_bits ^= 1u << stg;
+                if (i == 0 && lane == 0) trace_stamp(X.trace, tcls, w, 2);
+                compute_slab(ring + stg * kSlabBytes, valid, qa, sc, g, t, m_run, l_run, oacc);
+            }
+            __syncwarp();  // every lane is done with this stage before it is refilled
+            if (lane == 0) {
+                if (valid > 0 && is_host(i)) {
+                    store_slab(&tmap, ring + stg * kSlabBytes, dst, D.p);  // recall fused: cache the page
+                    if (valid2 > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                }
+                if (valid2 > 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    issue_slab(is_host(i + kStages) ? &tmap_h : &tmap, ring + stg * kSlabBytes, &bars[stg],
+                               row2, D.p);
+                }
+            }
+        }
+        if (host_mask && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+}
+
 __device__ __forceinline__ long long range_start(long long w, long long V, long long T) { return w * V / T; }
 
 // Units attended in `phase`: all (0), unflagged (1), corrected (2).  Phases 1/2 lay only
@@ -319,8 +414,7 @@ __global__ void __launch_bounds__(WPC * 32, WPC == 8 ? 1 : (NST == 2 ? 3 : 2)) f
     __syncwarp();
     uint32_t phase_bits = 0u;  // parity of each stage's next completion
     pdl_wait();  // the select kernel's page lists and flags are complete
-    const int G = D.G, spp = D.p >> 4, lspp = spp == 1 ? 0 : (spp == 2 ? 1 : 2);
-    const float sc = D.attn_c;
+    const int G = D.G;
     // this phase's virtual page list: its units end to end, P_max pages each
     int nu = D.U;
     if (phase != 0) {
@@ -341,85 +435,15 @@ __global__ void __launch_bounds__(WPC * 32, WPC == 8 ? 1 : (NST == 2 ? 3 : 2)) f
         const long long seg_end = min(s1, (long long)(r + 1) * D.P_max);
         const int pa = (int)(seg - (long long)r * D.P_max);
         seg = seg_end;
-        const int32_t* prow = X.page_rows + (size_t)u * D.P_max;  // written by the select kernel
-        const int pb = min((int)(seg_end - (long long)r * D.P_max), X.page_cnt[u]);
-        const int b = u / D.n_kv, m = u % D.n_kv;
-        // Q fragments: lane (g, t) holds Q[head g][64b + 16t + 8e .. +8] (heads >= G are zero)
-        uint4 qa[2][2];
-        {
-            const bool hv = g < G;
-            const uint16_t* qrow = q + ((size_t)b * D.n_qo + m * G + (hv ? g : 0)) * kHeadDim;
-#pragma unroll
-            for (int bb = 0; bb < 2; ++bb)
-#pragma unroll
-                for (int e = 0; e < 2; ++e)
-                    qa[bb][e] = hv ? *reinterpret_cast<const uint4*>(qrow + 64 * bb + 16 * t + 8 * e)
-                                   : make_uint4(0u, 0u, 0u, 0u);
-        }
+        const int pb_cap = (int)(seg_end - (long long)r * D.P_max);
         float oacc[8][4];
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
             for (int k = 0; k < 4; ++k) oacc[i][k] = 0.0f;
         float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.0f, 0.0f};  // heads 2t, 2t+1
-        // the segment's pages in chunks of <= 32 (one page-table entry per lane)
-        for (int cb = pa; cb < pb; cb += 32) {
-            const int np = min(32, pb - cb);
-            // page table of the segment, one page per lane: first K row in the arena tensor and
-            // valid tokens -- one batch of independent loads instead of a dependent load per slab
-            int my_row = 0, my_valid = 0, my_dst = 0;
-            if (lane < np) {
-                my_row = prow[cb + lane];
-                my_valid = X.page_valid[(size_t)u * D.P_max + cb + lane];
-                if (my_valid & 0x80) my_dst = X.page_dst[(size_t)u * D.P_max + cb + lane];
-            }
-            const unsigned host_mask = __ballot_sync(0xffffffffu, my_valid & 0x80);  // pages read from the host pool
-            const int nx = np * spp;
-            if (lane == 0) trace_stamp(X.trace, tcls, w, 1);
-            auto slab_of = [&](int x, int& row) {  // warp-uniform; spp = 1 << lspp
-                const int pi = x >> lspp, sl = x & (spp - 1);
-                row = __shfl_sync(0xffffffffu, my_row, pi) + sl * 16;
-                return (__shfl_sync(0xffffffffu, my_valid, pi) & 0x7f) - sl * 16;
-            };
-            auto is_host = [&](int x) { return (host_mask >> (x >> lspp)) & 1u; };
-            // prologue: first kStages slabs of this segment in flight
-            int rows[kStages], valids[kStages];
-#pragma unroll
-            for (int i = 0; i < kStages; ++i) valids[i] = i < nx ? slab_of(i, rows[i]) : 0;
-            if (lane == 0) {
-#pragma unroll
-                for (int i = 0; i < kStages; ++i)
-                    if (valids[i] > 0)
-                        issue_slab(is_host(i) ? &tmap_h : &tmap, ring + i * kSlabBytes, &bar[warp][i], rows[i], D.p);
-            }
-            for (int i = 0; i < nx; ++i) {
-                const int stg = i % kStages;
-                int row;
-                const int valid = slab_of(i, row);
-                int row2 = 0, valid2 = 0;
-                if (i + kStages < nx) valid2 = slab_of(i + kStages, row2);
-                const int dst = host_mask ? __shfl_sync(0xffffffffu, my_dst, i >> lspp) + (i & (spp - 1)) * 16 : 0;
-                if (valid > 0) {
-                    mbar_wait(&bar[warp][stg], (phase_bits >> stg) & 1u);
-                    phase_bits ^= 1u << stg;
-                    if (i == 0 && lane == 0) trace_stamp(X.trace, tcls, w, 2);
-                    compute_slab(ring + stg * kSlabBytes, valid, qa, sc, g, t, m_run, l_run, oacc);
-                }
-                __syncwarp();  // every lane is done with this stage before it is refilled
-                if (lane == 0) {
-                    if (valid > 0 && is_host(i)) {
-                        store_slab(&tmap, ring + stg * kSlabBytes, dst, D.p);  // recall fused: cache the page
-                        if (valid2 > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                    }
-                    if (valid2 > 0) {
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                        issue_slab(is_host(i + kStages) ? &tmap_h : &tmap, ring + stg * kSlabBytes, &bar[warp][stg],
-                                   row2, D.p);
-                    }
-                }
-            }
-            if (host_mask && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        }
+        attend_pages<NST>(D, X, q, &tmap, &tmap_h, u, pa, pb_cap, ring, bar[warp], phase_bits, m_run, l_run, oacc,
+                          tcls, w);
         if (lane == 0) trace_stamp(X.trace, tcls, w, 3);
         // ---- partial record (w, k_rec) of unit u: unnormalised, relative to m_run.  Lane (g, t)
         // holds heads 2t, 2t+1; l is summed over the 8 lanes g of the same t
@@ -458,6 +482,205 @@ __global__ void __launch_bounds__(WPC * 32, WPC == 8 ? 1 : (NST == 2 ? 3 : 2)) f
         }
     }
     if (lane == 0) trace_stamp(X.trace, tcls, w, 4);
+}
+
+static int attn_stages();
+
+// ---- clustered attention: one cluster of C CTAs (4 warps each) per unit; warp k of the
+// 4C warps attends pages [k P_max / 4C, (k+1) P_max / 4C) of the unit's list, leaves its
+// partial record (unnormalised o, running max m, sum l per head) in its own shared memory,
+// and after one cluster barrier the leader CTA merges the 4C records over DSMEM, writes
+// the output and commits the speculative advance (row a8) -- no global records, no second
+// kernel.  Units have (almost) equal page counts, so the per-unit split stays balanced.
+template <int NST, int C>
+__global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2)
+    fkv_attn_cluster_kernel(FkvDims D, FkvLayer L, FkvScratch X, const uint16_t* __restrict__ q,
+                            float* __restrict__ out, int phase, const __grid_constant__ CUtensorMap tmap,
+                            const __grid_constant__ CUtensorMap tmap_h, int commit) {
+    constexpr int kStages = NST, W = kAttnWarpsPerCta, NW = W * C;
+    extern __shared__ __align__(1024) uint8_t s_stage[];  // [W][kStages][8 KiB]; then the records
+    __shared__ __align__(8) uint64_t bar[W][kStages];
+    cg::cluster_group cl = cg::this_cluster();
+    const int crank = (int)cl.block_rank();
+    const int rk = blockIdx.x / C;  // rank of this cluster's unit among the phase's units
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+    const int g = lane >> 2, t = lane & 3;
+    const int G = D.G;
+    pdl_trigger();
+    const int tcls = 4 + phase;
+    const int w = rk * NW + crank * W + warp;  // trace entity
+    if (lane == 0) trace_stamp(X.trace, tcls, w, 0);
+    uint8_t* ring = s_stage + warp * (kStages * kSlabBytes);
+    if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < kStages; ++i) mbar_init(&bar[warp][i], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    uint32_t phase_bits = 0u;
+    pdl_wait();  // the select kernel's page lists and flags are complete
+    int u = rk, nu = D.U;
+    if (phase != 0) {
+        int d1;
+        nu = phase_units(D, L, phase, rk, lane, u, d1);
+    }
+    if (rk >= nu) return;  // cluster-uniform: no unit for this cluster in this phase
+    const int k = crank * W + warp;
+    const int pa = (int)((long long)k * D.P_max / NW), pbc = (int)((long long)(k + 1) * D.P_max / NW);
+    float oacc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) oacc[i][j] = 0.0f;
+    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.0f, 0.0f};
+    attend_pages<NST>(D, X, q, &tmap, &tmap_h, u, pa, pbc, ring, bar[warp], phase_bits, m_run, l_run, oacc, tcls, w);
+    if (lane == 0) trace_stamp(X.trace, tcls, w, 3);
+    // ---- this warp's record, in its own (now idle) ring: o [G][128], then m [G], l [G]
+    __syncwarp();
+    float* rec = reinterpret_cast<float*>(ring);
+    float l0 = l_run[0], l1 = l_run[1];
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+        l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    }
+    if (g == 0) {
+        if (2 * t < G) {
+            rec[G * kHeadDim + 2 * t] = m_run[0];
+            rec[G * kHeadDim + G + 2 * t] = l0;
+        }
+        if (2 * t + 1 < G) {
+            rec[G * kHeadDim + 2 * t + 1] = m_run[1];
+            rec[G * kHeadDim + G + 2 * t + 1] = l1;
+        }
+    }
+    const int base0 = 64 * (g >> 2) + 8 * (g & 3);  // see the split kernel's record layout
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+        const int h = 2 * t + hh;
+        if (h < G) {
+            float* dst = rec + h * kHeadDim + base0;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                float4* d4 = reinterpret_cast<float4*>(dst + 32 * half);
+                const int mb = 4 * half;
+                d4[0] = make_float4(oacc[mb][hh], oacc[mb][2 + hh], oacc[mb + 1][hh], oacc[mb + 1][2 + hh]);
+                d4[1] = make_float4(oacc[mb + 2][hh], oacc[mb + 2][2 + hh], oacc[mb + 3][hh], oacc[mb + 3][2 + hh]);
+            }
+        }
+    }
+    cl.sync();  // every record of the unit is in its CTA's shared memory
+    if (crank == 0) {
+        if (tid == 0) trace_stamp(X.trace, 7, rk, 0);
+        // thread -> (head h, 4 channels); records read over DSMEM, merged with an online max
+        const int b = u / D.n_kv, m = u % D.n_kv;
+        for (int e = tid; e < G * (kHeadDim / 4); e += blockDim.x) {
+            const int h = e / (kHeadDim / 4), c4 = e % (kHeadDim / 4);
+            constexpr int RB = NW < 8 ? NW : 8;  // records per batch (loads in flight together)
+            float M = -INFINITY, Ls = 0.0f;
+            float4 O = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+            for (int r0 = 0; r0 < NW; r0 += RB) {
+                float mv[RB], lv[RB];
+                float4 ov[RB];
+#pragma unroll
+                for (int i = 0; i < RB; ++i) {
+                    const int r = r0 + i;
+                    const float* rr = cl.map_shared_rank(
+                        reinterpret_cast<float*>(s_stage + (r % W) * (kStages * kSlabBytes)), r / W);
+                    mv[i] = rr[G * kHeadDim + h];
+                    lv[i] = rr[G * kHeadDim + G + h];
+                    ov[i] = reinterpret_cast<const float4*>(rr + h * kHeadDim)[c4];
+                }
+                float Mb = M;
+#pragma unroll
+                for (int i = 0; i < RB; ++i) Mb = fmaxf(Mb, mv[i]);
+                if (Mb != -INFINITY) {
+                    const float scl = exp2f(M - Mb);  // M = -inf -> 0
+                    Ls *= scl;
+                    O.x *= scl;
+                    O.y *= scl;
+                    O.z *= scl;
+                    O.w *= scl;
+#pragma unroll
+                    for (int i = 0; i < RB; ++i) {
+                        const float wgt = mv[i] == -INFINITY ? 0.0f : exp2f(mv[i] - Mb);
+                        Ls += wgt * lv[i];
+                        O.x += wgt * ov[i].x;
+                        O.y += wgt * ov[i].y;
+                        O.z += wgt * ov[i].z;
+                        O.w += wgt * ov[i].w;
+                    }
+                    M = Mb;
+                }
+            }
+            const size_t row = (size_t)b * D.n_qo + m * G + h;
+            reinterpret_cast<float4*>(out + row * kHeadDim)[c4] = make_float4(O.x / Ls, O.y / Ls, O.z / Ls, O.w / Ls);
+            reinterpret_cast<uint2*>(L.q_prev + row * kHeadDim)[c4] = reinterpret_cast<const uint2*>(q + row * kHeadDim)[c4];
+        }
+        if (commit == 0) {  // commit: R := S_i
+            for (int i = tid; i < D.K; i += blockDim.x) {
+                L.res_pages[(size_t)u * D.K + i] = L.pend_pages[(size_t)u * D.K + i];
+                L.res_slot[(size_t)u * D.K + i] = L.pend_slot[(size_t)u * D.K + i];
+            }
+            if (tid == 0) {
+                L.res_front[u] = L.pend_front[u];
+                L.res_cnt[u] = L.pend_cnt[u];
+                L.res_valid[u] = 1;
+            }
+        }
+        if (tid == 0) trace_stamp(X.trace, 7, rk, 1);
+    }
+    cl.sync();  // the leader has read every record: the other CTAs may exit
+}
+
+template <int NST, int C>
+static cudaError_t launch_cluster_c(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
+                                    float* out, int phase, const CUtensorMap& tmap, const CUtensorMap& tmap_h,
+                                    int commit, bool pdl, cudaStream_t s) {
+    auto kern = fkv_attn_cluster_kernel<NST, C>;
+    const int smem = kAttnWarpsPerCta * NST * kSlabBytes;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(D.U * C);
+    cfg.blockDim = dim3(kAttnWarpsPerCta * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, kern, D, L, X, q, out, phase, tmap, tmap_h, commit);
+}
+
+// Clustered attention + merge + commit (replaces split + combine); c = CTAs per unit (1..8)
+cudaError_t launch_attn_cluster(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
+                                float* out, int phase, const CUtensorMap& tmap, const CUtensorMap& tmap_h,
+                                int commit, int c, bool pdl, cudaStream_t s) {
+    const int nst = attn_stages();
+#define FKV_CL(NS)                                                                                          \
+    do {                                                                                                    \
+        if (c == 1) return launch_cluster_c<NS, 1>(D, L, X, q, out, phase, tmap, tmap_h, commit, pdl, s); \
+        if (c == 2) return launch_cluster_c<NS, 2>(D, L, X, q, out, phase, tmap, tmap_h, commit, pdl, s); \
+        if (c == 4) return launch_cluster_c<NS, 4>(D, L, X, q, out, phase, tmap, tmap_h, commit, pdl, s); \
+        return launch_cluster_c<NS, 8>(D, L, X, q, out, phase, tmap, tmap_h, commit, pdl, s);             \
+    } while (0)
+    if (nst == 2) FKV_CL(2);
+    FKV_CL(3);
+#undef FKV_CL
 }
 
 // Merge a unit's partial records and commit the speculative advance (row a8).

@@ -226,6 +226,9 @@ cudaError_t attn_resident_warps(int cps, int* warps);  // warps of the split ker
 cudaError_t launch_attn_split(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                               int phase, const CUtensorMap& tmap, const CUtensorMap& tmap_host,
                               const uint16_t* arena, bool pdl, cudaStream_t s, int wpc = 4);
+cudaError_t launch_attn_cluster(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
+                                float* out, int phase, const CUtensorMap& tmap, const CUtensorMap& tmap_h,
+                                int commit, int c, bool pdl, cudaStream_t s);
 // commit: 0 = every unit (R := S_i, q_prev := q_i), 2 = corrected units only (pipelined step:
 // the background select kernel commits the others)
 cudaError_t launch_attn_combine(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,

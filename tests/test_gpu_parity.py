@@ -257,3 +257,11 @@ def test_parity_select_threads(threads, monkeypatch):
     monkeypatch.setenv("FREEKV_SELECT_THREADS", threads)
     run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=4)
     run_parity(G=8, n_kv=1, batch=1, page=16, sink=64, window=64, budget=640, L0=9000, steps=3, n_layers=1)
+
+
+def test_parity_split_attention(monkeypatch):
+    """FREEKV_ATTN=split: balanced split-KV attention + combine kernels (the default attends
+    each unit with a cluster of CTAs and merges the partial records over DSMEM)."""
+    monkeypatch.setenv("FREEKV_ATTN", "split")
+    run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=5)
+    run_parity(G=4, n_kv=2, batch=1, page=32, L0=900, steps=4, use_primitives=True)
