@@ -569,12 +569,38 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2)
             }
         }
     }
+    // the leader's commit / q_prev inputs, loaded before the barrier (independent of the records)
+    constexpr int kQv = (kMaxG * (kHeadDim / 4) + kAttnWarpsPerCta * 32 - 1) / (kAttnWarpsPerCta * 32);
+    uint2 qv[kQv];
+    int cp_page = 0, cp_slot = 0, cp_front = 0, cp_cnt = 0;
+    if (crank == 0) {
+        const int b = u / D.n_kv, m = u % D.n_kv;
+#pragma unroll
+        for (int i = 0; i < kQv; ++i) {
+            const int e = tid + i * (int)blockDim.x;
+            if (e < G * (kHeadDim / 4)) {
+                const size_t row = (size_t)b * D.n_qo + m * G + e / (kHeadDim / 4);
+                qv[i] = reinterpret_cast<const uint2*>(q + row * kHeadDim)[e % (kHeadDim / 4)];
+            }
+        }
+        if (commit == 0 && tid < D.K) {
+            cp_page = L.pend_pages[(size_t)u * D.K + tid];
+            cp_slot = L.pend_slot[(size_t)u * D.K + tid];
+        }
+        if (commit == 0 && tid == 0) {
+            cp_front = L.pend_front[u];
+            cp_cnt = L.pend_cnt[u];
+        }
+    }
     cl.sync();  // every record of the unit is in its CTA's shared memory
     if (crank == 0) {
         if (tid == 0) trace_stamp(X.trace, 7, rk, 0);
         // thread -> (head h, 4 channels); records read over DSMEM, merged with an online max
         const int b = u / D.n_kv, m = u % D.n_kv;
-        for (int e = tid; e < G * (kHeadDim / 4); e += blockDim.x) {
+#pragma unroll
+        for (int qi = 0; qi < kQv; ++qi) {
+            const int e = tid + qi * (int)blockDim.x;
+            if (e >= G * (kHeadDim / 4)) break;
             const int h = e / (kHeadDim / 4), c4 = e % (kHeadDim / 4);
             constexpr int RB = NW < 8 ? NW : 8;  // records per batch (loads in flight together)
             float M = -INFINITY, Ls = 0.0f;
@@ -616,16 +642,20 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2)
             }
             const size_t row = (size_t)b * D.n_qo + m * G + h;
             reinterpret_cast<float4*>(out + row * kHeadDim)[c4] = make_float4(O.x / Ls, O.y / Ls, O.z / Ls, O.w / Ls);
-            reinterpret_cast<uint2*>(L.q_prev + row * kHeadDim)[c4] = reinterpret_cast<const uint2*>(q + row * kHeadDim)[c4];
+            reinterpret_cast<uint2*>(L.q_prev + row * kHeadDim)[c4] = qv[qi];  // q_prev := q_i
         }
         if (commit == 0) {  // commit: R := S_i
-            for (int i = tid; i < D.K; i += blockDim.x) {
+            if (tid < D.K) {
+                L.res_pages[(size_t)u * D.K + tid] = cp_page;
+                L.res_slot[(size_t)u * D.K + tid] = cp_slot;
+            }
+            for (int i = tid + (int)blockDim.x; i < D.K; i += blockDim.x) {  // K > block size
                 L.res_pages[(size_t)u * D.K + i] = L.pend_pages[(size_t)u * D.K + i];
                 L.res_slot[(size_t)u * D.K + i] = L.pend_slot[(size_t)u * D.K + i];
             }
             if (tid == 0) {
-                L.res_front[u] = L.pend_front[u];
-                L.res_cnt[u] = L.pend_cnt[u];
+                L.res_front[u] = cp_front;
+                L.res_cnt[u] = cp_cnt;
                 L.res_valid[u] = 1;
             }
         }

@@ -213,7 +213,8 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
 
     __shared__ float s_redm[kWarps][kMaxG], s_redz[kWarps][kMaxG];
     __shared__ float s_cos[kMaxG];
-    __shared__ __align__(16) int s_h[kHistBins];  // radix histogram
+    __shared__ __align__(16) int s_h[kHistBins];           // radix histogram
+    __shared__ __align__(16) int s_sup[kHistBins / 32];    // its sums over 32-bin groups
     __shared__ int s_dig[4], s_abv[4];
     __shared__ uint32_t s_bk[32];  // boundary-bin keys and ids
     __shared__ int s_bid[32], s_bn;
@@ -268,6 +269,7 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
     }
     for (int i = tid; i < 2 * K; i += kThreads) s_used[i] = 0;
     for (int i = tid; i < kHistBins; i += kThreads) s_h[i] = 0;
+    for (int i = tid; i < kHistBins / 32; i += kThreads) s_sup[i] = 0;
     if (tid == 0) s_bn = 0;
     const size_t srow = (size_t)D.n_page_max;
     __syncthreads();  // staging visible
@@ -385,7 +387,7 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
 #pragma unroll
                 for (int g = 0; g < GM; ++g) {
                     if (g < G) {
-                        const float pg = __fdiv_rn(sv[g][l], Z[g]);
+                        const float pg = (D.dbg & 4) ? sv[g][l] * (1.0f / Z[g]) : __fdiv_rn(sv[g][l], Z[g]);
                         pi = g == 0 ? pg : __fadd_rn(pi, pg);
                     }
                 }
@@ -404,63 +406,75 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
             const int shift = pass == 0 ? 20 : (pass == 1 ? 8 : 0);
             const int nbits = pass == 2 ? 8 : 12;
             const uint32_t dmask = (1u << nbits) - 1u;
+            if (tid == 0) trace_stamp(trace, 11, u, pass);  // diagnostics: radix passes taken
             if (pass > 0) {  // fallback passes (rare): clear the histogram first
                 __syncthreads();
                 for (int i = tid; i < kHistBins; i += kThreads) s_h[i] = 0;
+                for (int i = tid; i < kHistBins / 32; i += kThreads) s_sup[i] = 0;
                 __syncthreads();
             }
+            // plain shared atomics (match.any aggregation measured ~18x slower on B200)
 #pragma unroll
             for (int l = 0; l < LPT; ++l) {
-                const int dg = (cand[l] && (key[l] & mask) == prefix) ? (int)((key[l] >> shift) & dmask) : -1;
-                const unsigned grp = __match_any_sync(0xffffffffu, dg);
-                if (dg >= 0 && lane == __ffs(grp) - 1) atomicAdd(&s_h[dg], __popc(grp));
+                if (cand[l] && (key[l] & mask) == prefix) {
+                    const int dg = (int)((key[l] >> shift) & dmask);
+                    atomicAdd(&s_h[dg], 1);
+                    atomicAdd(&s_sup[dg >> 5], 1);
+                }
             }
             __syncthreads();
             if (warp == 0) {
-                // lane owns bins [lane * per, (lane + 1) * per); suffix scan over lanes (descending bins)
-                const int per = (int)(dmask + 1u) >> 5;
-                int lsum = 0;
-                for (int i = 0; i < per; i += 4) {
-                    const int4 h4 = *reinterpret_cast<const int4*>(&s_h[lane * per + i]);
-                    lsum += h4.x + h4.y + h4.z + h4.w;
+                // level 1: 32-bin groups (lane owns up to 4 contiguous groups, one conflict-free
+                // 16-byte load); level 2: the 32 bins of the boundary group, one per lane
+                const int nsup = (int)(dmask + 1u) >> 5;  // 128 or 8
+                int4 c4 = make_int4(0, 0, 0, 0);
+                if (nsup == 128) {
+                    c4 = *reinterpret_cast<const int4*>(&s_sup[lane * 4]);
+                } else if (lane < nsup) {
+                    c4.x = s_sup[lane];  // one group per lane, in c4.x
                 }
-                int suf = lsum;
+                const int s4 = c4.x + c4.y + c4.z + c4.w;
+                int suf = s4;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const int y = __shfl_down_sync(0xffffffffu, suf, o);
                     if (lane + o < 32) suf += y;
                 }
-                const int above = suf - lsum;  // keys in bins of higher lanes
-                const unsigned hit = __ballot_sync(0xffffffffu, above < k_rem && above + lsum >= k_rem);
-                const int lb = __ffs(hit) - 1;  // the lane whose bins hold the boundary
-                const int above_lb = __shfl_sync(0xffffffffu, above, lb);
-                // refine inside lane lb's bins, 4 per lane, again by a suffix scan
-                const int nl = per >> 2;
-                int4 c4 = make_int4(0, 0, 0, 0);
-                if (lane < nl) c4 = *reinterpret_cast<const int4*>(&s_h[lb * per + 4 * lane]);
-                const int s4 = c4.x + c4.y + c4.z + c4.w;
-                int suf2 = s4;
+                int a = suf - s4;  // keys in groups of higher lanes
+                int grp = 0;
+                if (a < k_rem && a + s4 >= k_rem) {  // exactly one lane
+                    if (nsup == 128) {
+                        if (a + c4.w >= k_rem) {
+                            grp = 3;
+                        } else if ((a += c4.w) + c4.z >= k_rem) {
+                            grp = 2;
+                        } else if ((a += c4.z) + c4.y >= k_rem) {
+                            grp = 1;
+                        } else {
+                            a += c4.y;
+                            grp = 0;
+                        }
+                        grp += lane * 4;
+                    } else {
+                        grp = lane;
+                    }
+                }
+                const unsigned hit = __ballot_sync(0xffffffffu, a < k_rem && a + s4 >= k_rem);
+                const int hl = __ffs(hit) - 1;
+                grp = __shfl_sync(0xffffffffu, grp, hl);
+                const int above_g = __shfl_sync(0xffffffffu, a, hl);
+                const int cb = s_h[grp * 32 + lane];
+                int suf2 = cb;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const int y = __shfl_down_sync(0xffffffffu, suf2, o);
                     if (lane + o < 32) suf2 += y;
                 }
-                int a = above_lb + suf2 - s4;
-                if (lane < nl && a < k_rem && a + s4 >= k_rem) {
-                    int bin, c;
-                    if (a + c4.w >= k_rem) {
-                        bin = 3, c = c4.w;
-                    } else if ((a += c4.w) + c4.z >= k_rem) {
-                        bin = 2, c = c4.z;
-                    } else if ((a += c4.z) + c4.y >= k_rem) {
-                        bin = 1, c = c4.y;
-                    } else {
-                        a += c4.y;
-                        bin = 0, c = c4.x;
-                    }
-                    s_dig[0] = lb * per + 4 * lane + bin;
-                    s_abv[0] = a;
-                    s_dig[1] = c;
+                const int ab = above_g + suf2 - cb;  // keys in higher bins
+                if (ab < k_rem && ab + cb >= k_rem) {
+                    s_dig[0] = grp * 32 + lane;
+                    s_abv[0] = ab;
+                    s_dig[1] = cb;
                 }
             }
             __syncthreads();
@@ -490,16 +504,15 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
                 const int n = s_bn;
                 const uint32_t mk = lane < n ? s_bk[lane] : 0u;
                 const int mi = lane < n ? s_bid[lane] : 0x7fffffff;
-                int rank = 0;
+                int rank = 0, gt = 0;
                 for (int i = 0; i < n; ++i) {
                     const uint32_t ok = __shfl_sync(0xffffffffu, mk, i);
                     const int oi = __shfl_sync(0xffffffffu, mi, i);
                     rank += (ok > mk || (ok == mk && oi < mi)) ? 1 : 0;
+                    gt += ok > mk ? 1 : 0;
                 }
                 // the k_rem-th largest of the bin is the threshold; keys above it in the bin are taken
                 if (lane < n && rank == k_rem - 1) {
-                    int gt = 0;
-                    for (int i = 0; i < n; ++i) gt += s_bk[i] > mk ? 1 : 0;
                     s_dig[2] = (int)mk;
                     s_abv[2] = k_rem - gt;
                 }

@@ -27,7 +27,7 @@ if GRAPH:
     vb = torch.empty_like(kb)
     ob = torch.empty(L, nb, nq, d, dtype=torch.float32, device=dev)
 names = {0: "score", 1: "finalize", 2: "recall_sync", 3: "recall_bg", 4: "attn", 5: "attn_phase1", 6: "attn_phase2",
-         7: "combine", 8: "prep", 9: "score_bg", 10: "finalize_bg"}
+         7: "combine", 8: "prep", 9: "score_bg", 10: "finalize_bg", 11: "radix_passes"}
 res = {}
 def steps():
     for i in range(12):
