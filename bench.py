@@ -468,7 +468,10 @@ def main():
                 traffic = tj.get("dram_bytes_per_launch")
         except Exception:  # noqa: BLE001
             traffic = None
-    roof = {"kernel": "fkv_attn_split_kernel" + (" phase 1" if two_phase else " (all units)"), "bound": "hbm",
+    split_attn = os.environ.get("FREEKV_ATTN", "").startswith("s") or os.environ.get("FREEKV_CORR", "").startswith("r")
+    kname = ("fkv_attn_split_kernel" + (" phase 1" if two_phase else " (all units)")) if split_attn or two_phase \
+        else "fkv_attn_cluster_kernel (all units: attention + DSMEM merge + commit)"
+    roof = {"kernel": kname, "bound": "hbm",
             "achieved": round(attn_gbs, 1), "peak": hbm_peak, "unit": "GB/s", "frac": round(attn_gbs / hbm_peak, 4),
             "traffic": traffic, "algorithmic_bytes_per_launch": int(attn_bytes / max(attn_n, 1)),
             "us_per_launch": round(attn_ms / max(attn_n, 1) * 1e3, 2),
