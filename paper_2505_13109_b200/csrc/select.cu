@@ -202,7 +202,11 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
                                               const uint16_t* __restrict__ k_new,
                                               const uint16_t* __restrict__ v_new, int32_t* __restrict__ pages_out,
                                               uint8_t* __restrict__ corrected_out, int which,
-                                              const float* ssc = nullptr, const float* cos_in = nullptr) {
+                                              const float* ssc = nullptr, const float* cos_in = nullptr,
+                                              uint64_t* cos_bar = nullptr, int lc_in = -1, int noff_in = -1) {
+    // cos_bar != NULL: cos_in is written later by the helper CTA; wait on this mbarrier
+    // (phase 0) before reading it.  lc_in / noff_in >= 0: this step's context and frontier
+    // (the helper publishes them to global memory after its append, possibly later)
     // ssc != NULL: the scores are already in shared memory ([G][n_page_max], fused select);
     // cos_in != NULL (fused select, which == 0): the helper CTA has done the correction check
     // (cos_in = per-head cosines in this CTA's shared memory) and the append of this step's token
@@ -239,8 +243,8 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
     if (tid == 0) trace_stamp(trace, tcls, u, 0);
     pdl_trigger();  // attention may start its prologue
     const int pre_flag = which ? (int)L.flags[u] : 0;
-    int n_off = L.n_off[u];
-    const int ctx0 = L.ctx[u];
+    int n_off = noff_in >= 0 ? noff_in : L.n_off[u];
+    const int ctx0 = lc_in >= 0 ? lc_in : L.ctx[u];
     const int Lc_now = ctx0 + (k_new ? 1 : 0);
     if (k_new) n_off = max(n_off, frontier_for(D, Lc_now));
     const int n_cand = n_off - n_sink;
@@ -283,7 +287,7 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
     // step's token -- it only touches the ring / the page completing now (not a candidate of
     // this step) / the host pool
     if (cos_in) {
-        if (tid < G) s_cos[tid] = cos_in[tid];  // visible to warp 0 after the barriers below
+        if (!cos_bar && tid < G) s_cos[tid] = cos_in[tid];  // visible to warp 0 after the barriers below
     } else {
         if (which == 0) {
             const uint32_t* qa32 = reinterpret_cast<const uint32_t*>(q + ((size_t)b * D.n_qo + m * G) * kHeadDim);
@@ -567,6 +571,14 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
             if (which) {
                 s_flag = pre_flag;  // decided by the prep kernel (same CFR-10 arithmetic)
             } else {
+                if (cos_bar) {  // the helper's cosines arrive over DSMEM with a remote mbarrier arrive
+                    asm volatile(
+                        "{\n.reg .pred P1;\nWAIT_C_%=:\n"
+                        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], 0;\n"
+                        "@!P1 bra WAIT_C_%=;\n}\n" ::"r"(smem_u32(cos_bar))
+                        : "memory");
+                    for (int g = 0; g < G; ++g) s_cos[g] = cos_in[g];
+                }
                 float acc = s_cos[0];
                 for (int g = 1; g < G; ++g) acc = __fadd_rn(acc, s_cos[g]);
                 const float mean = __fdiv_rn(acc, (float)G);
@@ -894,6 +906,7 @@ __global__ void __launch_bounds__(NT)
     float* s_sc = reinterpret_cast<float*>(s_dyn + fused_off_sc(D));
     uint8_t* ring = s_dyn + fused_off_ring(D) + (size_t)warp * kFusedRing * kChunkBytes;
     pdl_trigger();
+    if (tid == 0) trace_stamp(trace, 0, blockIdx.x, 0);
     // ---- this CTA's summary blocks (state: readable before pdl_wait)
     const int ctx0 = L.ctx[u];
     const int n_off = max(L.n_off[u], frontier_for(D, ctx0 + (k_new ? 1 : 0)));
@@ -921,23 +934,17 @@ __global__ void __launch_bounds__(NT)
         }
     }
     pdl_wait();  // step inputs (q_i) are ready
+    if (tid == 0) trace_stamp(trace, 0, blockIdx.x, 1);
     float* s_cosx = reinterpret_cast<float*>(s_dyn + fused_smem_bytes(D));  // [kMaxG] helper -> leader
+    // the helper CTA takes the leader's prologue work -- the correction check (CFR-10) and
+    // the append of this step's token (row a9) -- after its share of the scoring, while the
+    // leader runs the select; the cosines reach the leader over DSMEM with a remote arrive
+    // on an mbarrier in the leader's shared memory, which it waits on just before the flag
     const bool helped = CL == 2 && which == 0 && !(D.dbg & 2);  // FREEKV_DEBUG_EXP bit 1: off (A/B)
-    if (CL == 2 && rank == 1 && helped) {
-        // the helper CTA takes the leader's prologue: the correction check (CFR-10) on lanes
-        // 0..G-1 of its last warp, and the append of this step's token (row a9), while its
-        // first summary chunks are in flight
-        if (warp == NT / 32 - 1 && lane < G) {
-            const size_t row = ((size_t)b * D.n_qo + m * G + lane) * kHeadDim;
-            *cg::this_cluster().map_shared_rank(&s_cosx[lane], 0) = cos_cfr10(q + row, L.q_prev + row);
-        }
-        if (k_new) {
-            append_unit(D, L, u, ctx0, k_new, v_new, 1, reinterpret_cast<uint4*>(s_dyn));
-            if (tid == 0) {
-                L.ctx[u] = ctx0 + 1;
-                L.n_off[u] = n_off;
-            }
-        }
+    __shared__ __align__(8) uint64_t s_cosbar;
+    if (helped && rank == 0 && tid == 0) {
+        mbar_init(&s_cosbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int i = tid; i < GP * kHeadDim; i += blockDim.x) {
         const int h = i / kHeadDim, c = i % kHeadDim;
@@ -947,6 +954,7 @@ __global__ void __launch_bounds__(NT)
         qm[c][h] = x >= 0.0f ? 0xffffffffu : 0u;  // CFR-2: q_c >= 0 (incl. -0) uses the max
     }
     __syncthreads();
+    if (tid == 0) trace_stamp(trace, 0, blockIdx.x, 2);
     float* dst_sc = s_sc;  // scores land in the leader
     if (CL == 2 && rank) dst_sc = cg::this_cluster().map_shared_rank(s_sc, 0);
     if (scorer) {
@@ -978,9 +986,37 @@ __global__ void __launch_bounds__(NT)
             }
         }
     }
+    if (tid == 0) trace_stamp(trace, 0, blockIdx.x, 3);
     if (CL == 2) {
         cg::this_cluster().sync();  // every score is in the leader's shared memory
-        if (rank) return;
+        if (tid == 0) trace_stamp(trace, 0, blockIdx.x, 4);
+        if (rank) {
+            if (helped) {
+                if (warp == NT / 32 - 1 && lane < G) {
+                    const size_t row = ((size_t)b * D.n_qo + m * G + lane) * kHeadDim;
+                    *cg::this_cluster().map_shared_rank(&s_cosx[lane], 0) = cos_cfr10(q + row, L.q_prev + row);
+                }
+                __syncwarp();
+                if (warp == NT / 32 - 1 && lane == 0) {
+                    // release the DSMEM stores above, then arrive on the leader's barrier
+                    const uint32_t rb = (uint32_t)__cvta_generic_to_shared(cg::this_cluster().map_shared_rank(&s_cosbar, 0));
+                    asm volatile(
+                        "{\n.reg .b32 ra;\n"
+                        "mapa.shared::cluster.u32 ra, %0, 0;\n"
+                        "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}\n" ::"r"(smem_u32(&s_cosbar))
+                        : "memory");
+                    (void)rb;
+                }
+                if (k_new) {
+                    append_unit(D, L, u, ctx0, k_new, v_new, 1, reinterpret_cast<uint4*>(s_dyn));
+                    if (tid == 0) {
+                        L.ctx[u] = ctx0 + 1;
+                        L.n_off[u] = n_off;
+                    }
+                }
+            }
+            return;
+        }
     } else {
         __syncthreads();
     }
@@ -988,7 +1024,8 @@ __global__ void __launch_bounds__(NT)
     // and the correction check were done by the helper CTA
     finalize_unit<LPT, GM, NT>(u, D, L, page_rows, page_valid, page_dst, page_cnt, trace, nullptr, q,
                                helped ? nullptr : k_new, helped ? nullptr : v_new, pages_out, corrected_out, which,
-                               s_sc, helped ? s_cosx : nullptr);
+                               s_sc, helped ? s_cosx : nullptr, helped ? &s_cosbar : nullptr,
+                               helped ? ctx0 + (k_new ? 1 : 0) : -1, helped ? n_off : -1);
 }
 
 template <int LPT, int GM, int NT, int CL>
