@@ -267,7 +267,9 @@ __device__ __forceinline__ void attend_pages(const FkvDims& D, const FkvScratch&
                                              const CUtensorMap* tmap_p, const CUtensorMap* tmap_hp, int u, int pa,
                                              int pb_cap, uint8_t* ring, uint64_t* bars, uint32_t& phase_bits,
                                              float (&m_run)[2], float (&l_run)[2], float (&oacc)[8][4], int tcls,
-                                             int w) {
+                                             int w, int pre = 0) {
+    // pre: the first `pre` slabs of page pa are already in flight in stages 0..pre-1 (issued
+    // before the PDL wait from the same rows the page list now holds)
     constexpr int kStages = NST;
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const int G = D.G, spp = D.p >> 4, lspp = spp == 1 ? 0 : (spp == 2 ? 1 : 2);
@@ -316,7 +318,7 @@ __device__ __forceinline__ void attend_pages(const FkvDims& D, const FkvScratch&
         if (lane == 0) {
 #pragma unroll
             for (int i = 0; i < kStages; ++i)
-                if (valids[i] > 0)
+                if (valids[i] > 0 && !(cb == pa && i < pre))
                     issue_slab(is_host(i) ? &tmap_h : &tmap, ring + i * kSlabBytes, &bars[i], rows[i], D.p);
         }
         for (int i = 0; i < nx; ++i) {
@@ -518,6 +520,39 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2)
     }
     __syncwarp();
     uint32_t phase_bits = 0u;
+    const int k = crank * W + warp;
+    const int pa = (int)((long long)k * D.P_max / NW), pbc = (int)((long long)(k + 1) * D.P_max / NW);
+    // ---- speculative prefetch (phase 0): while the select kernel drains, issue this warp's
+    // first slabs if they lie in the sink + resident part of the unit's page list -- rows
+    // from the resident set of step i-1, which the select does not modify.  A unit that is
+    // not corrected at this step attends exactly these rows; a corrected one drains
+    // them and starts over from its new page list.
+    int pre = 0;
+    const int spp = D.p >> 4;
+    if (phase == 0 && rk < D.U && pa < pbc && !(D.dbg & 8)) {  // FREEKV_DEBUG_EXP bit 3: off (A/B)
+        const int u0 = rk;
+        const int rv = L.res_valid[u0], rc = L.res_cnt[u0], ctx_any = L.ctx[u0];
+        if (rv && !D.full_refresh && ctx_any >= D.S_tok) {
+            const int n_spec = D.n_sink + rc;
+            const size_t pe = page_elems(D);
+            int row[kStages];
+#pragma unroll
+            for (int x = 0; x < kStages; ++x) {
+                const int pi = pa + x / spp;
+                row[x] = -1;
+                if (pi < pbc && pi < n_spec) {
+                    const uint16_t* base =
+                        pi < D.n_sink
+                            ? L.sink + ((size_t)u0 * D.n_sink + pi) * pe
+                            : L.slots + ((size_t)u0 * 2 * D.K + L.res_slot[(size_t)u0 * D.K + (pi - D.n_sink)]) * pe;
+                    row[x] = (int)((base - L.arena) / kHeadDim) + (x % spp) * 16;
+                }
+            }
+            while (pre < kStages && row[pre] >= 0) ++pre;
+            if (lane == 0)
+                for (int x = 0; x < pre; ++x) issue_slab(&tmap, ring + x * kSlabBytes, &bar[warp][x], row[x], D.p);
+        }
+    }
     pdl_wait();  // the select kernel's page lists and flags are complete
     int u = rk, nu = D.U;
     if (phase != 0) {
@@ -525,15 +560,21 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2)
         nu = phase_units(D, L, phase, rk, lane, u, d1);
     }
     if (rk >= nu) return;  // cluster-uniform: no unit for this cluster in this phase
-    const int k = crank * W + warp;
-    const int pa = (int)((long long)k * D.P_max / NW), pbc = (int)((long long)(k + 1) * D.P_max / NW);
+    if (pre > 0 && L.flags[u]) {  // corrected unit: drain the speculative slabs
+        for (int x = 0; x < pre; ++x) {
+            mbar_wait(&bar[warp][x], 0u);
+            phase_bits ^= 1u << x;
+        }
+        pre = 0;
+    }
     float oacc[8][4];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) oacc[i][j] = 0.0f;
     float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.0f, 0.0f};
-    attend_pages<NST>(D, X, q, &tmap, &tmap_h, u, pa, pbc, ring, bar[warp], phase_bits, m_run, l_run, oacc, tcls, w);
+    attend_pages<NST>(D, X, q, &tmap, &tmap_h, u, pa, pbc, ring, bar[warp], phase_bits, m_run, l_run, oacc, tcls, w,
+                      pre);
     if (lane == 0) trace_stamp(X.trace, tcls, w, 3);
     // ---- this warp's record, in its own (now idle) ring: o [G][128], then m [G], l [G]
     __syncwarp();
