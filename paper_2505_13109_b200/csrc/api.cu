@@ -669,6 +669,8 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         h->D.full_refresh = (fr && fr[0] == '1') ? 1 : 0;
         const char* dx = getenv("FREEKV_DEBUG_EXP");
         h->D.dbg = dx ? atoi(dx) : 0;
+        const char* sp = getenv("FREEKV_ATTN_SPEC");
+        h->D.attn_spec = (sp && sp[0] == '1') ? 1 : 0;
     }
     {
         const char* sr = getenv("FREEKV_SERIAL_RECALL");

@@ -258,50 +258,65 @@ __device__ __forceinline__ void compute_slab(const uint8_t* st, int valid, const
     }
 }
 
-// Attend pages [pa, pb) of unit u's page list (sink, selected/resident, local; written by
-// the select or prep kernel): online softmax over every token of those pages into
-// (m_run, l_run, oacc) -- lane (g, t) holds heads 2t, 2t+1.  One warp; ring/bar are the
-// warp's NST slab stages, phase_bits their parities (carried across calls).
-template <int NST>
-__device__ __forceinline__ void attend_pages(const FkvDims& D, const FkvScratch& X, const uint16_t* __restrict__ q,
-                                             const CUtensorMap* tmap_p, const CUtensorMap* tmap_hp, int u, int pa,
-                                             int pb_cap, uint8_t* ring, uint64_t* bars, uint32_t& phase_bits,
+// Page sources of attend_pages: entry i of unit u's page list -> (first K row in the arena
+// or host tensor, valid tokens | 0x80 for a host row, write-back row).
+struct TableSrc {  // the list written by the select (or prep) kernel of this step
+    const int32_t* rows;
+    const uint8_t* valid;
+    const int32_t* dst;
+    __device__ __forceinline__ void load(int i, int& r, int& v, int& d) const {
+        r = rows[i];
+        v = valid[i];
+        d = dst[i];
+    }
+};
+struct SpecSrc {  // sink pages, then the resident set R of step i-1 (all full pages)
+    int sink_row0, slot_row0, page_rows, n_sink;
+    const int32_t* res_slot;
+    int p;
+    __device__ __forceinline__ void load(int i, int& r, int& v, int& d) const {
+        r = i < n_sink ? sink_row0 + i * page_rows : slot_row0 + res_slot[i - n_sink] * page_rows;
+        v = p;
+        d = 0;
+    }
+};
+
+// Q fragments: lane (g, t) holds Q[head g][64b + 16t + 8e .. +8] (heads >= G are zero)
+__device__ __forceinline__ void load_q_frags(const FkvDims& D, const uint16_t* __restrict__ q, int u,
+                                             uint4 (&qa)[2][2]) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int b = u / D.n_kv, m = u % D.n_kv;
+    const bool hv = g < D.G;
+    const uint16_t* qrow = q + ((size_t)b * D.n_qo + m * D.G + (hv ? g : 0)) * kHeadDim;
+#pragma unroll
+    for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+            qa[bb][e] = hv ? *reinterpret_cast<const uint4*>(qrow + 64 * bb + 16 * t + 8 * e) : make_uint4(0u, 0u, 0u, 0u);
+}
+
+// Attend entries [pa, pb) of a page list: online softmax over every token of those pages
+// into (m_run, l_run, oacc) -- lane (g, t) holds heads 2t, 2t+1.  One warp; ring/bar are
+// the warp's NST slab stages, phase_bits their parities (carried across calls).
+template <int NST, class Src>
+__device__ __forceinline__ void attend_pages(const FkvDims& D, const FkvScratch& X, const uint4 (&qa)[2][2],
+                                             const CUtensorMap* tmap_p, const CUtensorMap* tmap_hp, const Src& src,
+                                             int pa, int pb, uint8_t* ring, uint64_t* bars, uint32_t& phase_bits,
                                              float (&m_run)[2], float (&l_run)[2], float (&oacc)[8][4], int tcls,
-                                             int w, int pre = 0) {
-    // pre: the first `pre` slabs of page pa are already in flight in stages 0..pre-1 (issued
-    // before the PDL wait from the same rows the page list now holds)
+                                             int w) {
     constexpr int kStages = NST;
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-    const int G = D.G, spp = D.p >> 4, lspp = spp == 1 ? 0 : (spp == 2 ? 1 : 2);
+    const int spp = D.p >> 4, lspp = spp == 1 ? 0 : (spp == 2 ? 1 : 2);
     const float sc = D.attn_c;
     const CUtensorMap& tmap = *tmap_p;
     const CUtensorMap& tmap_h = *tmap_hp;
-    const int32_t* prow = X.page_rows + (size_t)u * D.P_max;  // written by the select kernel
-    const int pb = min(pb_cap, X.page_cnt[u]);
-    const int b = u / D.n_kv, m = u % D.n_kv;
-    // Q fragments: lane (g, t) holds Q[head g][64b + 16t + 8e .. +8] (heads >= G are zero)
-    uint4 qa[2][2];
-    {
-        const bool hv = g < G;
-        const uint16_t* qrow = q + ((size_t)b * D.n_qo + m * G + (hv ? g : 0)) * kHeadDim;
-#pragma unroll
-        for (int bb = 0; bb < 2; ++bb)
-#pragma unroll
-            for (int e = 0; e < 2; ++e)
-                qa[bb][e] = hv ? *reinterpret_cast<const uint4*>(qrow + 64 * bb + 16 * t + 8 * e)
-                               : make_uint4(0u, 0u, 0u, 0u);
-    }
     // the segment's pages in chunks of <= 32 (one page-table entry per lane)
     for (int cb = pa; cb < pb; cb += 32) {
         const int np = min(32, pb - cb);
-        // page table of the segment, one page per lane: first K row in the arena tensor and
-        // valid tokens -- one batch of independent loads instead of a dependent load per slab
+        // page list of the segment, one page per lane: first K row and valid tokens -- one
+        // batch of independent loads instead of a dependent load per slab
         int my_row = 0, my_valid = 0, my_dst = 0;
-        if (lane < np) {
-            my_row = prow[cb + lane];
-            my_valid = X.page_valid[(size_t)u * D.P_max + cb + lane];
-            if (my_valid & 0x80) my_dst = X.page_dst[(size_t)u * D.P_max + cb + lane];
-        }
+        if (lane < np) src.load(cb + lane, my_row, my_valid, my_dst);
         const unsigned host_mask = __ballot_sync(0xffffffffu, my_valid & 0x80);  // pages read from the host pool
         const int nx = np * spp;
         if (lane == 0) trace_stamp(X.trace, tcls, w, 1);
@@ -318,7 +333,7 @@ __device__ __forceinline__ void attend_pages(const FkvDims& D, const FkvScratch&
         if (lane == 0) {
 #pragma unroll
             for (int i = 0; i < kStages; ++i)
-                if (valids[i] > 0 && !(cb == pa && i < pre))
+                if (valids[i] > 0)
                     issue_slab(is_host(i) ? &tmap_h : &tmap, ring + i * kSlabBytes, &bars[i], rows[i], D.p);
         }
         for (int i = 0; i < nx; ++i) {
@@ -444,8 +459,12 @@ __global__ void __launch_bounds__(WPC * 32, WPC == 8 ? 1 : (NST == 2 ? 3 : 2)) f
 #pragma unroll
             for (int k = 0; k < 4; ++k) oacc[i][k] = 0.0f;
         float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.0f, 0.0f};  // heads 2t, 2t+1
-        attend_pages<NST>(D, X, q, &tmap, &tmap_h, u, pa, pb_cap, ring, bar[warp], phase_bits, m_run, l_run, oacc,
-                          tcls, w);
+        uint4 qa[2][2];
+        load_q_frags(D, q, u, qa);
+        const TableSrc tsrc{X.page_rows + (size_t)u * D.P_max, X.page_valid + (size_t)u * D.P_max,
+                            X.page_dst + (size_t)u * D.P_max};
+        attend_pages<NST>(D, X, qa, &tmap, &tmap_h, tsrc, pa, min(pb_cap, X.page_cnt[u]), ring, bar[warp], phase_bits,
+                          m_run, l_run, oacc, tcls, w);
         if (lane == 0) trace_stamp(X.trace, tcls, w, 3);
         // ---- partial record (w, k_rec) of unit u: unnormalised, relative to m_run.  Lane (g, t)
         // holds heads 2t, 2t+1; l is summed over the 8 lanes g of the same t
@@ -522,35 +541,39 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2)
     uint32_t phase_bits = 0u;
     const int k = crank * W + warp;
     const int pa = (int)((long long)k * D.P_max / NW), pbc = (int)((long long)(k + 1) * D.P_max / NW);
-    // ---- speculative prefetch (phase 0): while the select kernel drains, issue this warp's
-    // first slabs if they lie in the sink + resident part of the unit's page list -- rows
-    // from the resident set of step i-1, which the select does not modify.  A unit that is
-    // not corrected at this step attends exactly these rows; a corrected one drains
-    // them and starts over from its new page list.
-    int pre = 0;
-    const int spp = D.p >> 4;
-    if (phase == 0 && rk < D.U && pa < pbc && !(D.dbg & 8)) {  // FREEKV_DEBUG_EXP bit 3: off (A/B)
+    float oacc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) oacc[i][j] = 0.0f;
+    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.0f, 0.0f};
+    uint4 qa[2][2];
+    // ---- speculative attention (phase 0), before the PDL wait: the sink pages and the
+    // resident set R of step i-1 form the head of every page list a unit without a
+    // correction attends at step i -- R is state the select kernel does not modify,
+    // so this warp streams its part of it while the select is still running.  After the wait
+    // a corrected unit discards that work and starts over from its new page list; the rest
+    // continue with the local pages (which include this step's token).  The select triggers
+    // this launch only after its own PDL wait, so the previous layer is complete and q_i may
+    // be read here.
+    int spec_end = pa;  // entries [pa, spec_end) attended speculatively
+    if (phase == 0 && rk < D.U && pa < pbc && D.attn_spec) {  // FREEKV_ATTN_SPEC=1 (off by default: measured
+                                                               // slower, it competes with the select)
         const int u0 = rk;
         const int rv = L.res_valid[u0], rc = L.res_cnt[u0], ctx_any = L.ctx[u0];
+        load_q_frags(D, q, u0, qa);
         if (rv && !D.full_refresh && ctx_any >= D.S_tok) {
-            const int n_spec = D.n_sink + rc;
-            const size_t pe = page_elems(D);
-            int row[kStages];
-#pragma unroll
-            for (int x = 0; x < kStages; ++x) {
-                const int pi = pa + x / spp;
-                row[x] = -1;
-                if (pi < pbc && pi < n_spec) {
-                    const uint16_t* base =
-                        pi < D.n_sink
-                            ? L.sink + ((size_t)u0 * D.n_sink + pi) * pe
-                            : L.slots + ((size_t)u0 * 2 * D.K + L.res_slot[(size_t)u0 * D.K + (pi - D.n_sink)]) * pe;
-                    row[x] = (int)((base - L.arena) / kHeadDim) + (x % spp) * 16;
-                }
+            spec_end = min(pbc, D.n_sink + rc);
+            if (spec_end > pa) {
+                const int pr = 2 * D.p;  // arena rows per page
+                const SpecSrc ssrc{(int)((L.sink - L.arena) / kHeadDim) + u0 * D.n_sink * pr,
+                                   (int)((L.slots - L.arena) / kHeadDim) + u0 * 2 * D.K * pr, pr, D.n_sink,
+                                   L.res_slot + (size_t)u0 * D.K, D.p};
+                attend_pages<NST>(D, X, qa, &tmap, &tmap_h, ssrc, pa, spec_end, ring, bar[warp], phase_bits, m_run,
+                                  l_run, oacc, tcls, w);
+            } else {
+                spec_end = pa;
             }
-            while (pre < kStages && row[pre] >= 0) ++pre;
-            if (lane == 0)
-                for (int x = 0; x < pre; ++x) issue_slab(&tmap, ring + x * kSlabBytes, &bar[warp][x], row[x], D.p);
         }
     }
     pdl_wait();  // the select kernel's page lists and flags are complete
@@ -560,21 +583,22 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2)
         nu = phase_units(D, L, phase, rk, lane, u, d1);
     }
     if (rk >= nu) return;  // cluster-uniform: no unit for this cluster in this phase
-    if (pre > 0 && L.flags[u]) {  // corrected unit: drain the speculative slabs
-        for (int x = 0; x < pre; ++x) {
-            mbar_wait(&bar[warp][x], 0u);
-            phase_bits ^= 1u << x;
-        }
-        pre = 0;
+    if (spec_end > pa && L.flags[u]) {  // corrected unit: its pages are S_i, not R -- start over
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) oacc[i][j] = 0.0f;
+        m_run[0] = m_run[1] = -INFINITY;
+        l_run[0] = l_run[1] = 0.0f;
+        spec_end = pa;
     }
-    float oacc[8][4];
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) oacc[i][j] = 0.0f;
-    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.0f, 0.0f};
-    attend_pages<NST>(D, X, q, &tmap, &tmap_h, u, pa, pbc, ring, bar[warp], phase_bits, m_run, l_run, oacc, tcls, w,
-                      pre);
+    if (spec_end == pa) load_q_frags(D, q, u, qa);
+    {
+        const TableSrc tsrc{X.page_rows + (size_t)u * D.P_max, X.page_valid + (size_t)u * D.P_max,
+                            X.page_dst + (size_t)u * D.P_max};
+        attend_pages<NST>(D, X, qa, &tmap, &tmap_h, tsrc, spec_end, min(pbc, X.page_cnt[u]), ring, bar[warp],
+                          phase_bits, m_run, l_run, oacc, tcls, w);
+    }
     if (lane == 0) trace_stamp(X.trace, tcls, w, 3);
     // ---- this warp's record, in its own (now idle) ring: o [G][128], then m [G], l [G]
     __syncwarp();

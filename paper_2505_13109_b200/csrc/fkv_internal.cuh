@@ -27,6 +27,7 @@ struct FkvDims {
     int mode;
     int full_refresh; // diagnostics (env FREEKV_DEBUG_FULL_REFRESH=1): no slot reuse, all pages re-fetched
     int dbg;          // timing experiments only (env FREEKV_DEBUG_EXP, bit flags; results not valid)
+    int attn_spec;    // speculative attention over R before the PDL wait (env FREEKV_ATTN_SPEC=1)
     float tau;
     float score_r;    // CFR-3: fl32(log2(e)/sqrt(d))
     float attn_c;     // log2(e)/sqrt(d) for attention softmax (not CFR)

@@ -107,7 +107,6 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims 
     __shared__ __align__(16) float qv[kHeadDim][GP];      // q_c per head
     __shared__ __align__(16) uint32_t qm[kHeadDim][GP];   // ~0 if q_c >= 0 (take max) else 0 (take min)
     __shared__ __align__(8) uint64_t bar[kScoreWarps][kRing];
-    pdl_trigger();  // the select-finalize kernel may start its prologue now
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tcls = 0;  // trace class
     uint8_t* ring = s_raw + warp * (kRing * kChunkBytes);
@@ -140,6 +139,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims 
         // q_i is this layer's input: with PDL the kernel may start while the previous layer's
         // last kernel drains; everything above (state and summaries of this layer) is independent
         pdl_wait();
+        pdl_trigger();  // dependents launch once the previous layer is complete (see the select)
         for (int i = threadIdx.x; i < GP * kHeadDim; i += blockDim.x) {
             const int h = i / kHeadDim, c = i % kHeadDim;
             float x = 0.0f;
@@ -193,6 +193,13 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims 
 constexpr int kMaxK = 256;
 constexpr int kHistBins = 4096;
 
+// The resident set of unit u as one thread (tid < K: entry tid) loaded it earlier, e.g. in the
+// fused select's prologue before the PDL wait (R is state, untouched by this step's kernels).
+struct ResPre {
+    int have = 0;
+    int valid = 0, front = 0, cnt = 0, page = -1, slot = -1;
+};
+
 template <int LPT, int GM, int NT>
 __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, const FkvLayer& L,
                                               int32_t* __restrict__ page_rows, uint8_t* __restrict__ page_valid,
@@ -203,7 +210,8 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
                                               const uint16_t* __restrict__ v_new, int32_t* __restrict__ pages_out,
                                               uint8_t* __restrict__ corrected_out, int which,
                                               const float* ssc = nullptr, const float* cos_in = nullptr,
-                                              uint64_t* cos_bar = nullptr, int lc_in = -1, int noff_in = -1) {
+                                              uint64_t* cos_bar = nullptr, int lc_in = -1, int noff_in = -1,
+                                              ResPre pre = ResPre()) {
     // cos_bar != NULL: cos_in is written later by the helper CTA; wait on this mbarrier
     // (phase 0) before reading it.  lc_in / noff_in >= 0: this step's context and frontier
     // (the helper publishes them to global memory after its append, possibly later)
@@ -241,7 +249,6 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
     // units' lists are written here)
     const int tcls = 1;  // trace class
     if (tid == 0) trace_stamp(trace, tcls, u, 0);
-    pdl_trigger();  // attention may start its prologue
     const int pre_flag = which ? (int)L.flags[u] : 0;
     int n_off = noff_in >= 0 ? noff_in : L.n_off[u];
     const int ctx0 = lc_in >= 0 ? lc_in : L.ctx[u];
@@ -264,12 +271,13 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
     // the previous layer's last kernel has completed (its prologue overlaps it)
     // debug mode 3 (FREEKV_DEBUG_FULL_REFRESH): forget the resident set every step, so every
     // unit re-fetches all K pages synchronously -- the GEN-X recall-bandwidth stress case
-    const int res_valid = D.full_refresh ? 0 : L.res_valid[u];
-    const int res_front = L.res_front[u];  // hoisted: used by the page list at the end
-    const int res_cnt = L.res_cnt[u];
+    const int res_valid = pre.have ? pre.valid : (D.full_refresh ? 0 : L.res_valid[u]);
+    const int res_front = pre.have ? pre.front : L.res_front[u];  // hoisted: used by the page list at the end
+    const int res_cnt = pre.have ? pre.cnt : L.res_cnt[u];
     for (int i = tid; i < K; i += kThreads) {
-        s_res[i] = res_valid ? L.res_pages[(size_t)u * K + i] : -1;
-        s_res_slot[i] = res_valid ? L.res_slot[(size_t)u * K + i] : -1;
+        const bool mine = pre.have && i == tid;
+        s_res[i] = res_valid ? (mine ? pre.page : L.res_pages[(size_t)u * K + i]) : -1;
+        s_res_slot[i] = res_valid ? (mine ? pre.slot : L.res_slot[(size_t)u * K + i]) : -1;
     }
     for (int i = tid; i < 2 * K; i += kThreads) s_used[i] = 0;
     for (int i = tid; i < kHistBins; i += kThreads) s_h[i] = 0;
@@ -283,6 +291,7 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
         s_used[s_res_slot[tid]] = 1;
     }
     pdl_wait();  // the previous kernel (score) has completed: scores and step inputs are ready
+    pdl_trigger();  // the attention may launch (and read q_i, attend speculatively) from here on
     // ---- step inputs: q_i, q_{i-1} (correction check), and the fused append (row a9) of this
     // step's token -- it only touches the ring / the page completing now (not a candidate of
     // this step) / the host pool
@@ -729,7 +738,6 @@ __global__ void __launch_bounds__(kPrepThreads) fkv_prep_kernel(FkvDims D, FkvLa
     __shared__ int s_flag;
     const int u = blockIdx.x, b = u / D.n_kv, m = u % D.n_kv, G = D.G, tid = threadIdx.x;
     if (tid == 0) trace_stamp(X.trace, 8, u, 0);
-    pdl_trigger();
     // state loads first (with PDL they overlap the previous layer's last kernel) ...
     const int L0 = L.ctx[u];
     int n_off = L.n_off[u];
@@ -737,6 +745,7 @@ __global__ void __launch_bounds__(kPrepThreads) fkv_prep_kernel(FkvDims D, FkvLa
     const int res_front = L.res_front[u], res_cnt = L.res_cnt[u];
     const int my_slot = tid < D.K ? L.res_slot[(size_t)u * D.K + tid] : 0;
     pdl_wait();  // ... step inputs (q_i, the new token) only after the previous layer has completed
+    pdl_trigger();
     {
         const uint32_t* qa32 = reinterpret_cast<const uint32_t*>(q + ((size_t)b * D.n_qo + m * G) * kHeadDim);
         const uint32_t* qb32 = reinterpret_cast<const uint32_t*>(L.q_prev + ((size_t)b * D.n_qo + m * G) * kHeadDim);
@@ -905,7 +914,6 @@ __global__ void __launch_bounds__(NT)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     float* s_sc = reinterpret_cast<float*>(s_dyn + fused_off_sc(D));
     uint8_t* ring = s_dyn + fused_off_ring(D) + (size_t)warp * kFusedRing * kChunkBytes;
-    pdl_trigger();
     if (tid == 0) trace_stamp(trace, 0, blockIdx.x, 0);
     // ---- this CTA's summary blocks (state: readable before pdl_wait)
     const int ctx0 = L.ctx[u];
@@ -933,7 +941,21 @@ __global__ void __launch_bounds__(NT)
             bulk_g2s(ring + c * kChunkBytes, chunk_src(c), kChunkBytes, &bar[warp][c]);
         }
     }
+    ResPre pre;  // the leader's resident set, loaded while the previous kernel drains
+    if (rank == 0) {
+        pre.have = 1;
+        pre.valid = D.full_refresh ? 0 : L.res_valid[u];
+        pre.front = L.res_front[u];
+        pre.cnt = L.res_cnt[u];
+        if (tid < D.K) {
+            pre.page = L.res_pages[(size_t)u * D.K + tid];
+            pre.slot = L.res_slot[(size_t)u * D.K + tid];
+        }
+    }
     pdl_wait();  // step inputs (q_i) are ready
+    // dependents (the attention) launch only once every CTA of this kernel is past its wait:
+    // the previous layer is then complete, so they may read q_i (and attend speculatively)
+    pdl_trigger();
     if (tid == 0) trace_stamp(trace, 0, blockIdx.x, 1);
     float* s_cosx = reinterpret_cast<float*>(s_dyn + fused_smem_bytes(D));  // [kMaxG] helper -> leader
     // the helper CTA takes the leader's prologue work -- the correction check (CFR-10) and
@@ -1025,7 +1047,7 @@ __global__ void __launch_bounds__(NT)
     finalize_unit<LPT, GM, NT>(u, D, L, page_rows, page_valid, page_dst, page_cnt, trace, nullptr, q,
                                helped ? nullptr : k_new, helped ? nullptr : v_new, pages_out, corrected_out, which,
                                s_sc, helped ? s_cosx : nullptr, helped ? &s_cosbar : nullptr,
-                               helped ? ctx0 + (k_new ? 1 : 0) : -1, helped ? n_off : -1);
+                               helped ? ctx0 + (k_new ? 1 : 0) : -1, helped ? n_off : -1, pre);
 }
 
 template <int LPT, int GM, int NT, int CL>

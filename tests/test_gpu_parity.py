@@ -265,3 +265,10 @@ def test_parity_split_attention(monkeypatch):
     monkeypatch.setenv("FREEKV_ATTN", "split")
     run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=5)
     run_parity(G=4, n_kv=2, batch=1, page=32, L0=900, steps=4, use_primitives=True)
+
+
+def test_parity_speculative_attention(monkeypatch):
+    """FREEKV_ATTN_SPEC=1: units attend their resident set before the select finishes; corrected
+    units discard that work (results identical)."""
+    monkeypatch.setenv("FREEKV_ATTN_SPEC", "1")
+    run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=6)
