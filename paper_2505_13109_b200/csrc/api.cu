@@ -61,8 +61,7 @@ struct freekv_handle {
     int sel_cluster = 8, sel_lptm = 1;  // fused select: CTAs per unit, max leaves per thread
     bool fused_select = false;          // FREEKV_SELECT=fused selects the one-launch cluster kernel
     int c2_nt = 512, c2_lpt = 2;        // threads per CTA / leaves per thread of the fused select
-    bool c2_select = false;             // score + select fused in 2-CTA clusters (default when it fits;
-                                        // FREEKV_SELECT=split keeps two launches)
+    bool c2_select = false;             // score + select fused in 2-CTA clusters (FREEKV_SELECT=c2)
     bool pdl = true;                    // programmatic dependent launch (FREEKV_PDL=0 disables)
     bool serial_recall = false;  // diagnostics: FREEKV_SERIAL_RECALL=1 runs background recall on the compute stream
     // profiling (freekv_profile_begin/end)
@@ -91,7 +90,7 @@ struct Sizes {
         o_pend_cnt,
         o_pend_pages, o_pend_slot, o_pend_front, o_flags, o_cbar, o_fetch_page, o_fetch_slot, o_n_fetch, o_ctx,
         o_n_off;
-    size_t o_scores, o_part_o, o_part_ml, o_page_rows, o_page_cnt, o_page_valid, o_page_dst;
+    size_t o_scores, o_part_o, o_part_ml, o_page_rows, o_page_cnt, o_page_valid, o_page_dst, o_cosv;
 };
 
 freekv_status validate(const freekv_config* c, FkvDims* D) {
@@ -188,6 +187,7 @@ Sizes compute_sizes(const freekv_config* c, const FkvDims& D) {
     s.o_page_cnt = take(U * 4);
     s.o_page_valid = take(U * D.P_max);
     s.o_page_dst = take(U * D.P_max * 4);
+    s.o_cosv = take(U * kMaxG * 4);
     s.scratch_bytes = o;
     s.dev_bytes = s.layer_bytes * c->n_layers + s.scratch_bytes;
     s.host_layer_bytes = (size_t)D.nb * D.n_page_host * D.n_kv * pe_b;
@@ -262,13 +262,21 @@ freekv_status do_select(freekv_handle* h, int layer, const void* q, int32_t* pag
     } else {
         const int mno =
             h->capturing ? max_n_off(h->D, h->D.max_ctx) : max_n_off(h->D, h->ctx_host[layer] + pending);
-        if (h->capturing || mno - h->D.n_sink > h->D.K)
+        // with a score launch, its last-scoring CTA of each unit also appends the token and runs
+        // the correction check, so the select kernel starts on the scores
+        const bool score = h->capturing || mno - h->D.n_sink > h->D.K;
+        const int pre_in_score = (score && k_new) ? 1 : 0;
+        if (score)
             FKV_CUDA(timed(h, K_SCORE, s, [&] {
-                return launch_score(h->D, h->layers[layer], h->X, (const uint16_t*)q, mno, pending, 0, h->pdl, s);
+                return launch_score(h->D, h->layers[layer], h->X, (const uint16_t*)q, mno, pending, 0, h->pdl, s,
+                                    pre_in_score ? (const uint16_t*)k_new : nullptr,
+                                    pre_in_score ? (const uint16_t*)v_new : nullptr);
             }));
         FKV_CUDA(timed(h, K_FINALIZE, s, [&] {
-            return launch_finalize(h->D, h->layers[layer], h->X, (const uint16_t*)q, (const uint16_t*)k_new,
-                                   (const uint16_t*)v_new, pages_out, corr_out, h->lpt1k, 1024, h->pdl, 0, s);
+            return launch_finalize(h->D, h->layers[layer], h->X, (const uint16_t*)q,
+                                   pre_in_score ? nullptr : (const uint16_t*)k_new,
+                                   pre_in_score ? nullptr : (const uint16_t*)v_new, pages_out, corr_out, h->lpt1k,
+                                   1024, h->pdl, 0, s, pre_in_score);
         }));
     }
     if (k_new && !h->capturing) h->ctx_host[layer] += 1;
@@ -579,6 +587,7 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
     h->X.page_cnt = (int32_t*)(sb + s.o_page_cnt);
     h->X.page_valid = (uint8_t*)(sb + s.o_page_valid);
     h->X.page_dst = (int32_t*)(sb + s.o_page_dst);
+    h->X.cosv = (float*)(sb + s.o_cosv);
 
     {
         // leaves of the select tree: page ids [0, n_off); n_off never exceeds
@@ -597,12 +606,14 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         if (h->fused_select) h->D.direct = 0;  // the cluster select writes slot rows only
         {
             const char* ne = getenv("FREEKV_SELECT_THREADS");  // 256, 512 (default) or 1024
-            h->c2_nt = ne ? atoi(ne) : 512;
-            if (h->c2_nt != 256 && h->c2_nt != 1024) h->c2_nt = 512;
+            h->c2_nt = ne ? atoi(ne) : 1024;
+            if (h->c2_nt != 256 && h->c2_nt != 512) h->c2_nt = 1024;
             h->c2_lpt = P2 <= h->c2_nt ? 1 : P2 / h->c2_nt;
             if (h->c2_nt == 256 && h->c2_lpt < 2) h->c2_lpt = 2;  // (instantiated: 2..8)
         }
-        h->c2_select = !h->fused_select && !(fs && fs[0] == 's') && select_c2_fits(h->D, h->c2_lpt, h->c2_nt);
+        // the fused 2-CTA select is opt-in (FREEKV_SELECT=c2): its scoring is ALU-bound on two SMs per
+        // unit, while the score kernel spreads it over all SMs -- measured faster end to end
+        h->c2_select = fs && fs[0] == 'c' && select_c2_fits(h->D, h->c2_lpt, h->c2_nt);
         const char* pp = getenv("FREEKV_PIPELINE");
         h->pipelined = h->D.direct && pp && pp[0] == '1';
         h->one_graph = h->D.direct;  // recalls are forked branches of the one step graph

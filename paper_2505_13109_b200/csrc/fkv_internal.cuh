@@ -77,6 +77,7 @@ struct FkvScratch {
     int32_t* page_cnt;    // [U]
     float* part_o;        // [2 phases][attn_warps][2 segments][G][d] per-warp, per-unit-segment partial outputs
     float* part_ml;       // [2 phases][attn_warps][2 segments][G][2] (running max, running sum)
+    float* cosv;          // [U][kMaxG] per-head correction cosines from the score kernel
 };
 
 __host__ __device__ inline size_t page_elems(const FkvDims& D) { return (size_t)2 * D.p * D.d; }
@@ -207,7 +208,8 @@ cudaError_t launch_summarize(const FkvDims& D, const FkvLayer& L, int page_begin
                              cudaStream_t s);
 // which (score / finalize): 0 every unit, 1 unflagged units only, 2 corrected units only
 cudaError_t launch_score(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                         int max_n_off, int pending, int which, bool pdl, cudaStream_t s);
+                         int max_n_off, int pending, int which, bool pdl, cudaStream_t s,
+                         const uint16_t* k_new = nullptr, const uint16_t* v_new = nullptr);
 cudaError_t launch_prep(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                         const uint16_t* k_new, const uint16_t* v_new, uint8_t* corrected_out, bool pdl,
                         cudaStream_t s);
@@ -216,7 +218,8 @@ cudaError_t launch_select_fused(const FkvDims& D, const FkvLayer& L, const FkvSc
                                 uint8_t* corrected_out, int cluster, int lptm, cudaStream_t s);
 cudaError_t launch_finalize(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                             const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
-                            uint8_t* corrected_out, int lpt, int nt, bool pdl, int which, cudaStream_t s);
+                            uint8_t* corrected_out, int lpt, int nt, bool pdl, int which, cudaStream_t s,
+                            int appended = 0);
 bool select_c2_fits(const FkvDims& D, int lpt, int nt);
 cudaError_t launch_select_c2(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                              const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,

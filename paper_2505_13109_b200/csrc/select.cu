@@ -101,7 +101,13 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims 
                                                                         float* __restrict__ scores,
                                                                         const uint16_t* __restrict__ q, int pending,
                                                                         unsigned long long* __restrict__ trace,
-                                                                        int which, int gy) {
+                                                                        int which, int gy,
+                                                                        const uint16_t* __restrict__ k_new,
+                                                                        const uint16_t* __restrict__ v_new,
+                                                                        float* __restrict__ cosv) {
+    // k_new != NULL: the unit's last-scoring CTA also appends this step's token (row a9) and
+    // runs the correction check (row a1, CFR-10 -> cosv[u][g]) after its scoring, so the
+    // select kernel starts on the scores directly; ctx / n_off are published by the select
     constexpr int GP = (G + 3) / 4 * 4;
     extern __shared__ __align__(128) uint8_t s_raw[];
     __shared__ __align__(16) float qv[kHeadDim][GP];      // q_c per head
@@ -120,11 +126,14 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims 
     // grid is smaller (the background score runs on a bounded number of CTAs)
     for (int item = blockIdx.x; item < D.U * gy; item += gridDim.x) {
         const int u = item / gy, yb = item - u * gy, b = u / D.n_kv, m = u % D.n_kv;
-        const int n_off = max(L.n_off[u], frontier_for(D, L.ctx[u] + pending));
-        if (yb * kScoreWarps * 32 >= n_off) continue;  // uniform: no candidate in this item
+        const int ctx0 = L.ctx[u];
+        const int n_off = max(L.n_off[u], frontier_for(D, ctx0 + pending));
+        // with k_new the grid has one extra CTA per unit (yb == gy - 1), which only does a1 + a9
+        const bool pre_cta = k_new && yb == gy - 1;
+        if (yb * kScoreWarps * 32 >= n_off && !pre_cta) continue;  // uniform: no candidate in this item
         __syncthreads();  // the previous item's q staging is no longer read
         const int blk = yb * kScoreWarps + warp;
-        const bool active = blk * 32 < n_off && blk * 32 + 31 >= D.n_sink;
+        const bool active = !pre_cta && blk * 32 < n_off && blk * 32 + 31 >= D.n_sink;
         const int tent = item;
         if (threadIdx.x == 0) trace_stamp(trace, tcls, tent, 0);
         const uint8_t* src = reinterpret_cast<const uint8_t*>(L.summ + summ_chunk_offset(D, u, blk * 32, 0, 0));
@@ -149,7 +158,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims 
         }
         __syncthreads();
         if (threadIdx.x == 0) trace_stamp(trace, tcls, tent, 1);
-        if (!active) continue;
+        if (active) {
         float acc[G];
 #pragma unroll
         for (int h = 0; h < G; ++h) acc[h] = 0.0f;
@@ -177,6 +186,16 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims 
 #pragma unroll
             for (int h = 0; h < G; ++h)
                 scores[((size_t)u * G + h) * D.n_page_max + j] = __fmul_rn(acc[h], D.score_r);  // CFR-3
+        }
+        }  // active
+        if (pre_cta) {
+            // rows a1 + a9 for the unit, on this CTA's now idle ring as the page staging
+            if (threadIdx.x < G) {
+                const size_t row = ((size_t)b * D.n_qo + m * G + threadIdx.x) * kHeadDim;
+                cosv[(size_t)u * kMaxG + threadIdx.x] = cos_cfr10(q + row, L.q_prev + row);
+            }
+            __syncthreads();  // every warp is done with the ring
+            append_unit(D, L, u, ctx0, k_new, v_new, 1, reinterpret_cast<uint4*>(s_raw));
         }
         if (threadIdx.x == 0) trace_stamp(trace, tcls, tent, 3);
     }
@@ -211,7 +230,9 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
                                               uint8_t* __restrict__ corrected_out, int which,
                                               const float* ssc = nullptr, const float* cos_in = nullptr,
                                               uint64_t* cos_bar = nullptr, int lc_in = -1, int noff_in = -1,
-                                              ResPre pre = ResPre()) {
+                                              ResPre pre = ResPre(), int appended = 0) {
+    // appended: the score kernel has appended this step's token and written the cosines
+    // (cos_in, global); this kernel publishes ctx / n_off
     // cos_bar != NULL: cos_in is written later by the helper CTA; wait on this mbarrier
     // (phase 0) before reading it.  lc_in / noff_in >= 0: this step's context and frontier
     // (the helper publishes them to global memory after its append, possibly later)
@@ -252,8 +273,8 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
     const int pre_flag = which ? (int)L.flags[u] : 0;
     int n_off = noff_in >= 0 ? noff_in : L.n_off[u];
     const int ctx0 = lc_in >= 0 ? lc_in : L.ctx[u];
-    const int Lc_now = ctx0 + (k_new ? 1 : 0);
-    if (k_new) n_off = max(n_off, frontier_for(D, Lc_now));
+    const int Lc_now = ctx0 + ((k_new || appended) ? 1 : 0);
+    if (k_new || appended) n_off = max(n_off, frontier_for(D, Lc_now));
     const int n_cand = n_off - n_sink;
     const bool rank_all = n_cand <= K;  // A-11: all candidates selected, no ranking
     if (tid == 0) trace_stamp(trace, tcls, u, 1);
@@ -297,6 +318,10 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
     // this step) / the host pool
     if (cos_in) {
         if (!cos_bar && tid < G) s_cos[tid] = cos_in[tid];  // visible to warp 0 after the barriers below
+        if (appended && tid == 0) {
+            L.ctx[u] = Lc_now;
+            L.n_off[u] = n_off;
+        }
     } else {
         if (which == 0) {
             const uint32_t* qa32 = reinterpret_cast<const uint32_t*>(q + ((size_t)b * D.n_qo + m * G) * kHeadDim);
@@ -710,10 +735,13 @@ __global__ void __launch_bounds__(NT) fkv_select_finalize_kernel(FkvDims D, FkvL
                                                                        const uint16_t* __restrict__ v_new,
                                                                        int32_t* __restrict__ pages_out,
                                                                        uint8_t* __restrict__ corrected_out,
-                                                                       int which) {
+                                                                       int which, const float* __restrict__ cosv) {
+    // cosv != NULL: the score kernel appended the token and wrote the cosines ([U][kMaxG])
     for (int u = blockIdx.x; u < D.U; u += gridDim.x) {
-        finalize_unit<LPT, GM, NT>(u, D, L, page_rows, page_valid, page_dst, page_cnt, trace, scores, q, k_new, v_new,
-                               pages_out, corrected_out, which);
+        finalize_unit<LPT, GM, NT>(u, D, L, page_rows, page_valid, page_dst, page_cnt, trace, scores, q,
+                                   cosv ? nullptr : k_new, cosv ? nullptr : v_new, pages_out, corrected_out, which,
+                                   nullptr, cosv ? cosv + (size_t)u * kMaxG : nullptr, nullptr, -1, -1, ResPre(),
+                                   cosv ? 1 : 0);
         __syncthreads();  // shared state of this unit is dead before the next unit reuses it
     }
 }
@@ -844,10 +872,11 @@ cudaError_t launch_prep(const FkvDims& D, const FkvLayer& L, const FkvScratch& X
 
 template <int G>
 static void launch_score_g(const FkvDims& D, const FkvLayer& L, float* scores, const uint16_t* q, int max_n_off,
-                           int pending, unsigned long long* trace, int which, bool pdl, cudaStream_t s) {
+                           int pending, unsigned long long* trace, int which, bool pdl, cudaStream_t s,
+                           const uint16_t* k_new, const uint16_t* v_new, float* cosv) {
     const int per_cta = kScoreWarps * 32;
     const int gy = (max_n_off + per_cta - 1) / per_cta;
-    if (gy <= 0) return;
+    if (gy <= 0 && !k_new) return;  // (with k_new the append + correction CTA still runs)
     const int smem = kScoreWarps * kRing * kChunkBytes;
     static bool configured = false;
     if (!configured) {
@@ -856,21 +885,24 @@ static void launch_score_g(const FkvDims& D, const FkvLayer& L, float* scores, c
                              cudaSharedmemCarveoutMaxShared);
         configured = true;
     }
-    const int grid = D.U * gy;  // one (unit, 128-page block) item per CTA
-    launch_ex(fkv_score_kernel<G>, dim3(grid), dim3(per_cta), smem, s, pdl, D, L, scores, q, pending, trace, which, gy);
+    const int gyl = std::max(gy, 0) + (k_new ? 1 : 0);  // + one CTA per unit for the append + correction check
+    const int grid = D.U * gyl;             // one (unit, 128-page block) item per CTA
+    launch_ex(fkv_score_kernel<G>, dim3(grid), dim3(per_cta), smem, s, pdl, D, L, scores, q, pending, trace, which, gyl,
+              k_new, v_new, cosv);
 }
 
 cudaError_t launch_score(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                         int max_n_off, int pending, int which, bool pdl, cudaStream_t s) {
+                         int max_n_off, int pending, int which, bool pdl, cudaStream_t s,
+                         const uint16_t* k_new, const uint16_t* v_new) {
     switch (D.G) {
-        case 1: launch_score_g<1>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s); break;
-        case 2: launch_score_g<2>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s); break;
-        case 3: launch_score_g<3>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s); break;
-        case 4: launch_score_g<4>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s); break;
-        case 5: launch_score_g<5>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s); break;
-        case 6: launch_score_g<6>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s); break;
-        case 7: launch_score_g<7>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s); break;
-        case 8: launch_score_g<8>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s); break;
+        case 1: launch_score_g<1>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s, k_new, v_new, X.cosv); break;
+        case 2: launch_score_g<2>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s, k_new, v_new, X.cosv); break;
+        case 3: launch_score_g<3>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s, k_new, v_new, X.cosv); break;
+        case 4: launch_score_g<4>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s, k_new, v_new, X.cosv); break;
+        case 5: launch_score_g<5>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s, k_new, v_new, X.cosv); break;
+        case 6: launch_score_g<6>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s, k_new, v_new, X.cosv); break;
+        case 7: launch_score_g<7>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s, k_new, v_new, X.cosv); break;
+        case 8: launch_score_g<8>(D, L, X.scores, q, max_n_off, pending, X.trace, which, pdl, s, k_new, v_new, X.cosv); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -1139,7 +1171,8 @@ cudaError_t launch_select_c2(const FkvDims& D, const FkvLayer& L, const FkvScrat
 template <int LPT, int GM, int NT>
 static cudaError_t launch_fin_g(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                                 const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
-                                uint8_t* corrected_out, size_t smem, bool pdl, int which, cudaStream_t s) {
+                                uint8_t* corrected_out, size_t smem, bool pdl, int which, cudaStream_t s,
+                                int appended) {
     static size_t configured = 0;
     if (smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(fkv_select_finalize_kernel<LPT, GM, NT>,
@@ -1153,17 +1186,18 @@ static cudaError_t launch_fin_g(const FkvDims& D, const FkvLayer& L, const FkvSc
     const int grid = D.U;
     return launch_ex(fkv_select_finalize_kernel<LPT, GM, NT>, dim3(grid), dim3(NT), smem, s, pdl, D, L, X.page_rows,
                      X.page_valid, X.page_dst, X.page_cnt, X.trace, (const float*)X.scores, q, k_new, v_new, pages_out,
-                     corrected_out, which);
+                     corrected_out, which, (const float*)(appended ? X.cosv : nullptr));
 }
 
 template <int LPT, int NT>
 static cudaError_t launch_fin(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                               const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
-                              uint8_t* corrected_out, size_t smem, bool pdl, int which, cudaStream_t s) {
-    if (D.G <= 1) return launch_fin_g<LPT, 1, NT>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
-    if (D.G <= 2) return launch_fin_g<LPT, 2, NT>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
-    if (D.G <= 4) return launch_fin_g<LPT, 4, NT>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
-    return launch_fin_g<LPT, 8, NT>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s);
+                              uint8_t* corrected_out, size_t smem, bool pdl, int which, cudaStream_t s,
+                              int appended) {
+    if (D.G <= 1) return launch_fin_g<LPT, 1, NT>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s, appended);
+    if (D.G <= 2) return launch_fin_g<LPT, 2, NT>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s, appended);
+    if (D.G <= 4) return launch_fin_g<LPT, 4, NT>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s, appended);
+    return launch_fin_g<LPT, 8, NT>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s, appended);
 }
 
 // nt = threads per CTA (512 or 1024); lpt = leaves per thread: nt * lpt >= next_pow2(n_off) for every
@@ -1171,9 +1205,11 @@ static cudaError_t launch_fin(const FkvDims& D, const FkvLayer& L, const FkvScra
 // fuses this step's single-token append (row a9) into the kernel.
 cudaError_t launch_finalize(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                             const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
-                            uint8_t* corrected_out, int lpt, int nt, bool pdl, int which, cudaStream_t s) {
+                            uint8_t* corrected_out, int lpt, int nt, bool pdl, int which, cudaStream_t s,
+                            int appended) {
     const size_t smem = page_elems(D) * sizeof(uint16_t) + (size_t)D.n_page_max * sizeof(uint16_t);
-#define FKV_FIN(LP, N) return launch_fin<LP, N>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s)
+#define FKV_FIN(LP, N) \
+    return launch_fin<LP, N>(D, L, X, q, k_new, v_new, pages_out, corrected_out, smem, pdl, which, s, appended)
     if (nt == 1024) {
         switch (lpt) {
             case 1: FKV_FIN(1, 1024);

@@ -243,17 +243,18 @@ def test_parity_window_zero():
     run_parity(G=4, n_kv=2, batch=1, page=32, sink=64, window=0, budget=256, L0=1000, steps=40, n_layers=1)
 
 
-def test_parity_split_select(monkeypatch):
-    """FREEKV_SELECT=split: separate score and select kernels (the default fuses them in
-    2-CTA clusters when the shapes fit)."""
-    monkeypatch.setenv("FREEKV_SELECT", "split")
+def test_parity_fused_c2_select(monkeypatch):
+    """FREEKV_SELECT=c2: score + select fused in 2-CTA clusters (helper CTA scores half of the
+    pages over DSMEM and does the append and correction check); default is two kernels."""
+    monkeypatch.setenv("FREEKV_SELECT", "c2")
     run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=5)
     run_parity(G=4, n_kv=1, batch=1, page=16, sink=64, window=64, budget=640, L0=20000, steps=3, n_layers=1)
 
 
-@pytest.mark.parametrize("threads", ["256", "1024"])
+@pytest.mark.parametrize("threads", ["256", "512", "1024"])
 def test_parity_select_threads(threads, monkeypatch):
     """The fused select at other CTA sizes (leaves per thread change; the tree does not)."""
+    monkeypatch.setenv("FREEKV_SELECT", "c2")
     monkeypatch.setenv("FREEKV_SELECT_THREADS", threads)
     run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=4)
     run_parity(G=8, n_kv=1, batch=1, page=16, sink=64, window=64, budget=640, L0=9000, steps=3, n_layers=1)
