@@ -1,5 +1,5 @@
 """Summarise an ncu --csv launch list (gpu__time_duration.sum [+ dram bytes]) per kernel."""
-import collections, csv, sys
+import collections, csv, statistics, sys
 
 UNIT = {"ns": 1e-3, "us": 1.0, "ms": 1e3, "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6,
         "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
@@ -18,17 +18,20 @@ def summarise(path):
         v = float(r[vi].replace(",", "")) * UNIT.get(r[ui], 1.0)
         per[r[ii]][r[mi]] = v
         per[r[ii]]["name"] = name
-    agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
+    agg = collections.defaultdict(list)
     for d in per.values():
-        a = agg[d["name"]]
-        a[0] += 1
-        a[1] += d.get("gpu__time_duration.sum", 0.0)
-        a[2] += d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
-    tot = sum(a[1] for a in agg.values())
-    lines = [f"{'kernel':34s} {'n':>4s} {'avg_us':>9s} {'dram_MB/launch':>15s} {'GB/s':>8s} {'share':>6s}"]
-    for k, a in sorted(agg.items(), key=lambda x: -x[1][1]):
-        gbs = a[2] / (a[1] * 1e3) if a[1] else 0.0
-        lines.append(f"{k:34s} {a[0]:4d} {a[1] / a[0]:9.2f} {a[2] / a[0] / 1e6:15.2f} {gbs:8.1f} {a[1] / tot * 100:5.1f}%")
+        agg[d["name"]].append((d.get("gpu__time_duration.sum", 0.0),
+                               d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)))
+    tot = sum(sum(t for t, _ in v) for v in agg.values())
+    med_tot = sum(statistics.median(t for t, _ in v) for k, v in agg.items() if k != "fkv_append_kernel")
+    lines = [f"{'kernel':30s} {'n':>4s} {'avg_us':>9s} {'median_us':>10s} {'share(total)':>13s} "
+             f"{'share(step, medians)':>21s}"]
+    for k, v in sorted(agg.items(), key=lambda x: -sum(t for t, _ in x[1])):
+        ts = [t for t, _ in v]
+        med = statistics.median(ts)
+        step_share = f"{med / med_tot * 100:5.1f}%" if k != "fkv_append_kernel" and med_tot else "   --"
+        lines.append(f"{k:30s} {len(ts):4d} {sum(ts) / len(ts):9.2f} {med:10.2f} {sum(ts) / tot * 100:12.1f}% "
+                     f"{step_share:>21s}")
     return "\n".join(lines)
 
 
