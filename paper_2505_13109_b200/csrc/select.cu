@@ -344,11 +344,57 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
             if (cos_lane) cos_all();
         }
     }
+    // ---- work of the last warp that needs no selection, done in the shadow of the ranking:
+    // the correction flag (CFR-10 pooling, A-12, A-13) and the free-slot list (slots of R are
+    // used, the others free; slot double-buffering)
+    __shared__ int s_nfree;
+    const int cnt_final = rank_all ? (n_cand > 0 ? n_cand : 0) : K;
+    auto early_tail = [&]() {
+        if (lane == 0) {
+            if (which) {
+                s_flag = pre_flag;  // decided by the prep kernel (same CFR-10 arithmetic)
+            } else {
+                if (cos_bar) {  // the helper's cosines arrive over DSMEM with a remote mbarrier arrive
+                    asm volatile(
+                        "{\n.reg .pred P1;\nWAIT_C_%=:\n"
+                        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], 0;\n"
+                        "@!P1 bra WAIT_C_%=;\n}\n" ::"r"(smem_u32(cos_bar))
+                        : "memory");
+                    for (int g = 0; g < G; ++g) s_cos[g] = cos_in[g];
+                }
+                float acc = s_cos[0];
+                for (int g = 1; g < G; ++g) acc = __fadd_rn(acc, s_cos[g]);
+                const float mean = __fdiv_rn(acc, (float)G);
+                int flag;
+                if (D.mode == 1 || D.tau >= 1.0f) flag = 1;
+                else if (D.mode == 2 || D.tau <= 0.0f) flag = 0;
+                else flag = mean < D.tau;
+                if (!res_valid) flag = 1;
+                s_flag = flag;
+                L.flags[u] = (uint8_t)flag;
+                L.cbar[u] = mean;
+                if (corrected_out) corrected_out[u] = (uint8_t)flag;
+            }
+            L.pend_front[u] = n_off;
+            L.pend_cnt[u] = cnt_final;
+        }
+        int nfree = 0;
+        for (int base = 0; base < 2 * K; base += 32) {
+            const int sl = base + lane;
+            const bool fr = sl < 2 * K && !s_used[sl];
+            const unsigned bal = __ballot_sync(0xffffffffu, fr);
+            if (fr) s_free[nfree + __popc(bal & ((1u << lane) - 1u))] = sl;
+            nfree += __popc(bal);
+        }
+        if (lane == 0) s_nfree = nfree;
+    };
     int cnt;
     if (rank_all) {
         for (int i = tid; i < K; i += kThreads) s_sel[i] = i < n_cand ? n_sink + i : -1;
         cnt = n_cand > 0 ? n_cand : 0;
         __syncthreads();
+        if (warp == kWarps - 1) early_tail();
+        __syncthreads();  // s_free / s_flag ready for warp 0's delta
     } else {
         if (tid == 0) trace_stamp(trace, tcls, u, 2);
         const int jb = tid * LPT;
@@ -376,6 +422,7 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
 #pragma unroll
             for (int g = 0; g < GM; ++g) s_redm[warp][g] = M[g];
         __syncthreads();
+        if (warp == kWarps - 1) early_tail();
 #pragma unroll
         for (int g = 0; g < GM; ++g) M[g] = warp_max_f32(lane < kWarps ? s_redm[lane][g] : -INFINITY);
         // ---- CFR-5/6: e = cexp2(s - m); Z = pairwise tree in page-id order: thread-local tree over
@@ -601,43 +648,6 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
     // the page -> index table built before the scores arrived (entries validated against s_res)
     if (tid == 0) trace_stamp(trace, tcls, u, 5);
     if (warp == 0) {
-        if (lane == 0) {
-            if (which) {
-                s_flag = pre_flag;  // decided by the prep kernel (same CFR-10 arithmetic)
-            } else {
-                if (cos_bar) {  // the helper's cosines arrive over DSMEM with a remote mbarrier arrive
-                    asm volatile(
-                        "{\n.reg .pred P1;\nWAIT_C_%=:\n"
-                        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], 0;\n"
-                        "@!P1 bra WAIT_C_%=;\n}\n" ::"r"(smem_u32(cos_bar))
-                        : "memory");
-                    for (int g = 0; g < G; ++g) s_cos[g] = cos_in[g];
-                }
-                float acc = s_cos[0];
-                for (int g = 1; g < G; ++g) acc = __fadd_rn(acc, s_cos[g]);
-                const float mean = __fdiv_rn(acc, (float)G);
-                int flag;
-                if (D.mode == 1 || D.tau >= 1.0f) flag = 1;
-                else if (D.mode == 2 || D.tau <= 0.0f) flag = 0;
-                else flag = mean < D.tau;
-                if (!res_valid) flag = 1;
-                s_flag = flag;
-                L.flags[u] = (uint8_t)flag;
-                L.cbar[u] = mean;
-                if (corrected_out) corrected_out[u] = (uint8_t)flag;
-            }
-            L.pend_front[u] = n_off;
-            L.pend_cnt[u] = cnt;
-        }
-        int nfree = 0;
-        for (int base = 0; base < 2 * K; base += 32) {
-            const int sl = base + lane;
-            const bool fr = sl < 2 * K && !s_used[sl];
-            const unsigned bal = __ballot_sync(0xffffffffu, fr);
-            if (fr) s_free[nfree + __popc(bal & ((1u << lane) - 1u))] = sl;
-            nfree += __popc(bal);
-        }
-        __syncwarp();
         int nf = 0;
         for (int base = 0; base < K; base += 32) {
             const int a = base + lane;

@@ -15,6 +15,9 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libfreekv.so")
+# A/B measurements only: FREEKV_LIB_SUFFIX=_X loads libfreekv_X.so from the same directory
+if os.environ.get("FREEKV_LIB_SUFFIX"):
+    LIB_PATH = LIB_PATH.replace("libfreekv.so", "libfreekv" + os.environ["FREEKV_LIB_SUFFIX"] + ".so")
 
 MODE_SPECULATIVE, MODE_ALWAYS_CORRECT, MODE_NEVER_CORRECT = 0, 1, 2
 
