@@ -58,6 +58,7 @@ struct freekv_handle {
     std::vector<int> ctx_host;
     std::vector<int> recall_pending;
     int lpt = 1, lpt1k = 1;  // leaves per thread of the 512 / 1024-thread select tree (fixed per handle, CFR-6)
+    int fin_nt = 512;        // threads of the select kernel (FREEKV_FIN_THREADS=1024 for the wide variant)
     int sel_cluster = 8, sel_lptm = 1;  // fused select: CTAs per unit, max leaves per thread
     bool fused_select = false;          // FREEKV_SELECT=fused selects the one-launch cluster kernel
     int c2_nt = 512, c2_lpt = 2;        // threads per CTA / leaves per thread of the fused select
@@ -275,8 +276,8 @@ freekv_status do_select(freekv_handle* h, int layer, const void* q, int32_t* pag
         FKV_CUDA(timed(h, K_FINALIZE, s, [&] {
             return launch_finalize(h->D, h->layers[layer], h->X, (const uint16_t*)q,
                                    pre_in_score ? nullptr : (const uint16_t*)k_new,
-                                   pre_in_score ? nullptr : (const uint16_t*)v_new, pages_out, corr_out, h->lpt1k,
-                                   1024, h->pdl, 0, s, pre_in_score);
+                                   pre_in_score ? nullptr : (const uint16_t*)v_new, pages_out, corr_out,
+                                   h->fin_nt == 512 ? h->lpt : h->lpt1k, h->fin_nt, h->pdl, 0, s, pre_in_score);
         }));
     }
     if (k_new && !h->capturing) h->ctx_host[layer] += 1;
@@ -604,6 +605,10 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         const char* fs = getenv("FREEKV_SELECT");
         h->fused_select = fs && fs[0] == 'f';
         if (h->fused_select) h->D.direct = 0;  // the cluster select writes slot rows only
+        {
+            const char* ft = getenv("FREEKV_FIN_THREADS");
+            h->fin_nt = (ft && atoi(ft) == 1024) ? 1024 : 512;  // 512: measured slightly faster
+        }
         {
             const char* ne = getenv("FREEKV_SELECT_THREADS");  // 256, 512 (default) or 1024
             h->c2_nt = ne ? atoi(ne) : 1024;
