@@ -39,7 +39,7 @@ constexpr int kRecallMaxU = 4096;
 
 __global__ void __launch_bounds__(kRecallThreads) fkv_recall_kernel(FkvDims D, FkvLayer L, int sync_mode,
                                                                     unsigned long long* __restrict__ trace,
-                                                                    int use_tma) {
+                                                                    int use_tma, int frag) {
     __shared__ int s_off[kRecallMaxU + 1];  // exclusive prefix of the eligible units' fetch counts
     __shared__ int s_wsum[kRecallThreads / 32];
     if (threadIdx.x == 0) trace_stamp(trace, 2 + (sync_mode ? 0 : 1), blockIdx.x, 0);
@@ -109,7 +109,12 @@ __global__ void __launch_bounds__(kRecallThreads) fkv_recall_kernel(FkvDims D, F
                 uint16_t* dst = L.slots + ((size_t)u * 2 * D.K + slot) * pe;
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // s_page free again
                 mbar_expect_tx(&bar, bytes);
-                bulk_g2s(s_page, src, bytes, &bar);
+                if (frag > 0 && frag < (int)bytes) {  // ablation: many small transfers per page
+                    for (uint32_t off = 0; off < bytes; off += (uint32_t)frag)
+                        bulk_g2s(s_page + off, reinterpret_cast<const uint8_t*>(src) + off, (uint32_t)frag, &bar);
+                } else {
+                    bulk_g2s(s_page, src, bytes, &bar);
+                }
                 mbar_wait(&bar, ph);
                 ph ^= 1u;
                 asm volatile(
@@ -196,7 +201,15 @@ cudaError_t launch_recall(const FkvDims& D, const FkvLayer& L, int sync_mode, cu
         if (e != cudaSuccess) return e;
         smem_set = smem;
     }
-    fkv_recall_kernel<<<grid, kRecallThreads, smem, s>>>(D, L, sync_mode, trace, mode);
+    // FREEKV_RECALL_FRAG=<bytes> (ablation): move each page as <bytes>-sized
+    // transfers, e.g. 256 = one (token, head) row of an NHD host layout, instead of one 16 KiB page
+    static int frag = -1;
+    if (frag < 0) {
+        const char* e = getenv("FREEKV_RECALL_FRAG");
+        frag = e ? std::max(0, atoi(e)) : 0;
+        if (frag % 16) frag = 0;  // bulk copies move multiples of 16 bytes
+    }
+    fkv_recall_kernel<<<grid, kRecallThreads, smem, s>>>(D, L, sync_mode, trace, mode, frag);
     return cudaGetLastError();
 }
 
