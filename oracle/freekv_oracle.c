@@ -176,6 +176,94 @@ int fko_select_unit(const uint16_t* q, const uint16_t* summ, int G, int d,
     return cnt;
 }
 
+/* ---- group-consistency variants (f3), see freekv_oracle.h ---- */
+
+/* CFR-2 with an fp32 query: u = fma(q_c, m_c, u) (exact product, one rounding) */
+static float page_bound_f32q(const float* q, const uint16_t* mn, const uint16_t* mx, int d) {
+    float u = 0.0f;
+    for (int c = 0; c < d; ++c) {
+        float m = (q[c] >= 0.0f) ? fko_bf16_to_f32(mx[c]) : fko_bf16_to_f32(mn[c]);
+        u = fmaf(q[c], m, u);
+    }
+    return u;
+}
+
+/* softmax over candidates per head g < G (CFR-4..7), then pooled_j = max_g p_gj */
+static void pool_max_s(const float* s, int G, int ld, int j_begin, int j_end, float* pooled) {
+    float* one = (float*)calloc((size_t)ld, sizeof(float));
+    for (int g = 0; g < G; ++g) {
+        fko_pool_means(s + (size_t)g * ld, 1, ld, j_begin, j_end, one); /* one head's p */
+        for (int j = j_begin; j < j_end; ++j) pooled[j] = (g == 0 || one[j] > pooled[j]) ? one[j] : pooled[j];
+    }
+    free(one);
+}
+
+int fko_select_unit_pool(const uint16_t* q, const uint16_t* summ, int G, int d, int n_sink, int n_off, int K,
+                         int pool, int32_t* sel, float* pooled_out) {
+    if (pool == FKO_POOL_MEAN_S) return fko_select_unit(q, summ, G, d, n_sink, n_off, K, sel, pooled_out);
+    int n = n_off - n_sink;
+    if (n <= K) return fko_topk(NULL, n_sink, n_off, K, sel); /* A-11 */
+    float r = fko_score_scale(d);
+    float* s = (float*)calloc((size_t)G * n_off, sizeof(float));
+    float* pooled = (float*)calloc((size_t)n_off, sizeof(float));
+    if (pool == FKO_POOL_MEAN_Q || pool == FKO_POOL_MAX_Q) {
+        /* (i) pool the queries, score once */
+        float* qb = (float*)calloc((size_t)d, sizeof(float));
+        for (int c = 0; c < d; ++c) {
+            float a = fko_bf16_to_f32(q[c]);
+            for (int g = 1; g < G; ++g) {
+                float x = fko_bf16_to_f32(q[(size_t)g * d + c]);
+                a = (pool == FKO_POOL_MEAN_Q) ? a + x : (x > a ? x : a);
+            }
+            qb[c] = (pool == FKO_POOL_MEAN_Q) ? a / (float)G : a;
+        }
+        for (int j = n_sink; j < n_off; ++j) {
+            const uint16_t* mn = summ + (size_t)j * 2 * d;
+            s[j] = page_bound_f32q(qb, mn, mn + d, d) * r;
+        }
+        fko_pool_means(s, 1, n_off, n_sink, n_off, pooled);
+        free(qb);
+    } else {
+        for (int g = 0; g < G; ++g)
+            for (int j = n_sink; j < n_off; ++j) {
+                const uint16_t* mn = summ + (size_t)j * 2 * d;
+                s[(size_t)g * n_off + j] = fko_page_bound(q + (size_t)g * d, mn, mn + d, d) * r;
+            }
+        if (pool == FKO_POOL_MAX_S) {
+            pool_max_s(s, G, n_off, n_sink, n_off, pooled);
+        } else { /* (ii) pool the scores, one softmax */
+            float* sb = (float*)calloc((size_t)n_off, sizeof(float));
+            for (int j = n_sink; j < n_off; ++j) {
+                float a = s[j];
+                for (int g = 1; g < G; ++g) {
+                    float x = s[(size_t)g * n_off + j];
+                    a = (pool == FKO_POOL_MEAN_QK) ? a + x : (x > a ? x : a);
+                }
+                sb[j] = (pool == FKO_POOL_MEAN_QK) ? a / (float)G : a;
+            }
+            fko_pool_means(sb, 1, n_off, n_sink, n_off, pooled);
+            free(sb);
+        }
+    }
+    int cnt = fko_topk(pooled, n_sink, n_off, K, sel);
+    if (pooled_out)
+        for (int j = n_sink; j < n_off; ++j) pooled_out[j] = pooled[j];
+    free(s);
+    free(pooled);
+    return cnt;
+}
+
+int fko_pool_correct_v(const float* C, int G, float tau, int mode, int cpool, float* cbar) {
+    if (cpool == 0) return fko_pool_correct(C, G, tau, mode, cbar);
+    float mn = C[0];
+    for (int g = 1; g < G; ++g)
+        if (C[g] < mn) mn = C[g];
+    if (cbar) *cbar = mn;
+    if (mode == FKO_MODE_ALWAYS || tau >= 1.0f) return 1;
+    if (mode == FKO_MODE_NEVER || tau <= 0.0f) return 0;
+    return mn < tau;
+}
+
 float fko_cosine(const uint16_t* a, const uint16_t* b, int d) {
     float dot = 0.0f, n1 = 0.0f, n2 = 0.0f;
     for (int c = 0; c < d; ++c) {

@@ -75,6 +75,29 @@ float fko_cosine(const uint16_t* a, const uint16_t* b, int d);
  * Returns flag (1 = corrected); writes the pooled mean to *cbar. */
 int fko_pool_correct(const float* C, int G, float tau, int mode, float* cbar);
 
+/* ---- group-consistency variants (exp:abl-g-cons,
+ * Table tab:abl-g-cons, Table tab:abl-g-corr).  The paper pools, max or mean over
+ * the G heads of a group, (i) the query vectors (Q), (ii) the attention weights between the
+ * queries and the page summaries (QK) or (iii) the softmax-normalised weights (S); FreeKV uses
+ * MeanS.  CFR for the variants: MeanQ q_c = fl(seq-sum_g q_gc / G) in fp32,
+ * MaxQ q_c = max_g q_gc, then CFR-2 with u = fma(q_c, m_c, u) and one softmax (G = 1);
+ * MeanQK s_j = fl(seq-sum_g s_gj / G), MaxQK s_j = max_g s_gj, then one softmax; MaxS
+ * pooled_j = max_g p_gj.  Ranking as CFR-9. */
+#define FKO_POOL_MEAN_S 0
+#define FKO_POOL_MAX_S 1
+#define FKO_POOL_MEAN_QK 2
+#define FKO_POOL_MAX_QK 3
+#define FKO_POOL_MEAN_Q 4
+#define FKO_POOL_MAX_Q 5
+int fko_select_unit_pool(const uint16_t* q, const uint16_t* summ, int G, int d, int n_sink, int n_off, int K,
+                         int pool, int32_t* sel, float* pooled_out);
+/* Correction pooling (tab:abl-g-corr): cpool 0 = mean of C_g (FreeKV); cpool 1 = the paper's
+ * "max pooling over group C_i", read as max pooling of the need to correct, i.e. the unit is
+ * corrected when its least similar head is below tau (min_g C_g < tau) -- the paper says it
+ * "triggers more corrections" than mean pooling, which max_g C_g would not (reading
+ * R-11).  cbar = the pooled value. */
+int fko_pool_correct_v(const float* C, int G, float tau, int mode, int cpool, float* cbar);
+
 /* Correction decision for one unit: cosine per head then fko_pool_correct.
  * bootstrap != 0 (no resident selection yet, A-12) -> flagged. */
 int fko_correct_unit(const uint16_t* q, const uint16_t* q_prev, int G, int d,

@@ -93,6 +93,11 @@ def lib():
         L.fko_attn_batch.argtypes = [ctypes.c_int, _u16p, ctypes.POINTER(_u16p), ctypes.POINTER(_u16p),
                                      ctypes.c_int, ctypes.c_int, ctypes.POINTER(_i32p), _i32p, _f64p]
         L.fko_num_threads.restype = ctypes.c_int
+        L.fko_select_unit_pool.restype = ctypes.c_int
+        L.fko_select_unit_pool.argtypes = [_u16p, _u16p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_int, ctypes.c_int, _i32p, _f32p]
+        L.fko_pool_correct_v.restype = ctypes.c_int
+        L.fko_pool_correct_v.argtypes = [_f32p, ctypes.c_int, ctypes.c_float, ctypes.c_int, ctypes.c_int, _f32p]
         _lib = L
     return _lib
 
@@ -175,6 +180,31 @@ def select_unit(q, summ, n_sink: int, n_off: int, K: int, want_pooled: bool = Fa
     return (sel, pooled) if want_pooled else sel
 
 
+# group-consistency variants (tab:abl-g-cons)
+POOL_MEAN_S, POOL_MAX_S, POOL_MEAN_QK, POOL_MAX_QK, POOL_MEAN_Q, POOL_MAX_Q = range(6)
+POOL_NAMES = ["MeanS", "MaxS", "MeanQK", "MaxQK", "MeanQ", "MaxQ"]
+
+
+def select_unit_pool(q, summ, n_sink: int, n_off: int, K: int, pool: int, want_pooled: bool = False):
+    """select_unit with the group pooling `pool` (POOL_*)."""
+    q = _u16(q)
+    summ = _u16(summ)
+    G, d = q.shape
+    sel = np.empty(K, np.int32)
+    pooled = np.zeros(max(n_off, 1), np.float32)
+    lib().fko_select_unit_pool(_p(q, _u16p), _p(summ, _u16p), G, d, n_sink, n_off, K, pool,
+                               _p(sel, _i32p), _p(pooled, _f32p))
+    return (sel, pooled) if want_pooled else sel
+
+
+def pool_correct_v(C, tau: float, mode: int, cpool: int) -> tuple[int, np.float32]:
+    """Correction pooling: cpool 0 mean (FreeKV), 1 max pooling of the need to correct (R-11)."""
+    C = np.ascontiguousarray(np.asarray(C, dtype=np.float32))
+    cbar = ctypes.c_float()
+    f = lib().fko_pool_correct_v(_p(C, _f32p), C.shape[0], tau, mode, cpool, ctypes.byref(cbar))
+    return f, np.float32(cbar.value)
+
+
 def cosine(a, b) -> np.float32:
     a, b = _u16(a), _u16(b)
     return np.float32(lib().fko_cosine(_p(a, _u16p), _p(b, _u16p), a.shape[0]))
@@ -226,6 +256,8 @@ class OracleConfig:
     tau: float = 0.8
     mode: int = MODE_SPECULATIVE
     first_layer_dense: bool = False
+    pool: int = 0       # POOL_* (f3); 0 = MeanS, FreeKV's choice
+    corr_pool: int = 0  # 0 = mean over the group (FreeKV), 1 = max pooling of the need to correct
 
     @property
     def G(self) -> int:
@@ -316,15 +348,25 @@ class OracleEngine:
             b, m = divmod(u, n_kv)
             qg = q[b, m * G:(m + 1) * G]
             qp = self.q_prev[layer][b, m * G:(m + 1) * G]
-            f, c = correct_unit(qg, qp, cfg.tau, cfg.mode, self.R[layer][u] is None)
+            if cfg.corr_pool == 0:
+                f, c = correct_unit(qg, qp, cfg.tau, cfg.mode, self.R[layer][u] is None)
+            else:
+                C = [cosine(qg[g], qp[g]) for g in range(G)]
+                f, c = pool_correct_v(C, cfg.tau, cfg.mode, cfg.corr_pool)
+                if self.R[layer][u] is None:
+                    f = 1  # A-12
             flags[u], cbar[u] = f, c
         # O-3: selection with q_i for every unit
         qs = np.ascontiguousarray(q.reshape(U, G, d))
         summ_ptrs = (_u16p * U)(*[self.summ[layer][u].ctypes.data_as(_u16p) for u in range(U)])
         n_off = np.array(self.n_off[layer], np.int32)
         sel = np.empty((U, cfg.K), np.int32)
-        lib().fko_select_batch(U, _p(qs, _u16p), summ_ptrs, G, d, cfg.n_sink, _p(n_off, _i32p),
-                               cfg.K, _p(sel, _i32p))
+        if cfg.pool == POOL_MEAN_S:
+            lib().fko_select_batch(U, _p(qs, _u16p), summ_ptrs, G, d, cfg.n_sink, _p(n_off, _i32p),
+                                   cfg.K, _p(sel, _i32p))
+        else:
+            for u in range(U):
+                sel[u] = select_unit_pool(qs[u], self.summ[layer][u], cfg.n_sink, int(n_off[u]), cfg.K, cfg.pool)
         # O-4: pages used by this step's attention
         used_sel, used_f, fetch_sync, fetch_bg = [], [], [], []
         for u in range(U):

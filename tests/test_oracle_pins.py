@@ -385,3 +385,93 @@ def test_first_layer_dense():
             G = eng.cfg.G
             ref = _sdpa64(r["q"][b, m * G:(m + 1) * G], eng.Kc[0][u, :Lc], eng.Vc[0][u, :Lc])
             assert np.allclose(r["out"][b, m * G:(m + 1) * G], ref, atol=1e-10)
+
+
+# ---- group-consistency variants (tab:abl-g-cons) ----------
+def _rand_unit(rng, G, d, n_pages):
+    q = O.f32_to_bf16(rng.standard_normal((G, d)).astype(np.float32))
+    summ = O.f32_to_bf16(np.sort(rng.standard_normal((n_pages, 2, d)).astype(np.float32), axis=1))
+    return q, summ
+
+
+def _variant_pooled_fp64(q, summ, n_sink, n_off, pool):
+    """The variant's pooled page weights, written from the paper's definitions in fp64 (independent of
+    the oracle): Q = pool the query vectors, QK = pool the page scores, S = pool the softmax weights."""
+    qf = O.bf16_to_f32(q).astype(np.float64)
+    mn = O.bf16_to_f32(summ[:, 0]).astype(np.float64)[n_sink:n_off]
+    mx = O.bf16_to_f32(summ[:, 1]).astype(np.float64)[n_sink:n_off]
+    d = qf.shape[1]
+
+    def bound(qv):  # Quest upper bound of q.k over the page (P:231, A-1)
+        return np.maximum(qv[None, :] * mn, qv[None, :] * mx).sum(axis=1) / math.sqrt(d)
+
+    def softmax(x):
+        e = np.exp(x - x.max())
+        return e / e.sum()
+
+    if pool in (O.POOL_MEAN_Q, O.POOL_MAX_Q):
+        qp = qf.mean(axis=0) if pool == O.POOL_MEAN_Q else qf.max(axis=0)
+        return softmax(bound(qp))
+    s = np.stack([bound(qf[g]) for g in range(qf.shape[0])])  # [G][pages]
+    if pool in (O.POOL_MEAN_QK, O.POOL_MAX_QK):
+        return softmax(s.mean(axis=0) if pool == O.POOL_MEAN_QK else s.max(axis=0))
+    p = np.stack([softmax(s[g]) for g in range(s.shape[0])])
+    return p.sum(axis=0) if pool == O.POOL_MEAN_S else p.max(axis=0)
+
+
+@pytest.mark.parametrize("pool", range(6))
+def test_pooling_variants_match_fp64_definitions(pool):
+    """Each pooling variant's top-K equals the top-K of its fp64 definition whenever the K-th and
+    (K+1)-th pooled weights are well separated (no near-tie for fp32 to flip)."""
+    rng = np.random.default_rng(100 + pool)
+    checked = 0
+    for trial in range(40):
+        G = [2, 4, 7, 8][trial % 4]
+        n_sink, n_off, K = 2, 200 + 13 * trial, 16
+        q, summ = _rand_unit(rng, G, 128, n_off)
+        ref = _variant_pooled_fp64(q, summ, n_sink, n_off, pool)
+        order = np.argsort(-ref, kind="stable")
+        if ref[order[K - 1]] - ref[order[K]] < 1e-5 * ref[order[K - 1]]:
+            continue
+        want = np.sort(order[:K] + n_sink)
+        got = O.select_unit_pool(q, summ, n_sink, n_off, K, pool)
+        assert np.array_equal(got, want), (pool, trial)
+        checked += 1
+    assert checked >= 20
+
+
+def test_pooling_variants_coincide_for_one_head():
+    """With G = 1 every pooling is the identity, so all six variants select MeanS's pages."""
+    rng = np.random.default_rng(7)
+    for trial in range(10):
+        q, summ = _rand_unit(rng, 1, 128, 300)
+        base = O.select_unit(q, summ, 2, 300, 24)
+        for pool in range(1, 6):
+            assert np.array_equal(O.select_unit_pool(q, summ, 2, 300, 24, pool), base), pool
+
+
+def test_pooling_variants_differ_from_means():
+    """The variants are real alternatives: on random units each one disagrees with MeanS somewhere."""
+    rng = np.random.default_rng(11)
+    units = [_rand_unit(rng, 4, 128, 300) for _ in range(8)]
+    for pool in range(1, 6):
+        assert any(not np.array_equal(O.select_unit_pool(q, s, 2, 300, 16, pool), O.select_unit(q, s, 2, 300, 16))
+                   for q, s in units), pool
+
+
+def test_correction_pooling_max_reading():
+    """Max-pooled correction (tab:abl-g-corr; reading R-11): a unit is corrected when any head's
+    similarity is below tau, so it corrects at least as often as mean pooling."""
+    rng = np.random.default_rng(5)
+    n_mean = n_max = 0
+    for _ in range(2000):
+        G = int(rng.integers(1, 9))
+        C = rng.uniform(0.5, 1.0, G).astype(np.float32)
+        f_max, c_max = O.pool_correct_v(C, 0.8, O.MODE_SPECULATIVE, 1)
+        f_mean, _ = O.pool_correct_v(C, 0.8, O.MODE_SPECULATIVE, 0)
+        assert f_max == int(bool((C < np.float32(0.8)).any()))
+        assert c_max == C.min()
+        assert f_max >= f_mean
+        n_mean += f_mean
+        n_max += f_max
+    assert n_max > n_mean
