@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define FREEKV_ABI_VERSION 1
+#define FREEKV_ABI_VERSION 2
 
 typedef int32_t freekv_status;
 enum {
@@ -68,7 +68,20 @@ typedef struct freekv_config {
     /* multi-GPU shard description; informational in ABI v1 */
     int32_t kv_head_begin, kv_head_end, batch_begin, batch_end;
     int32_t n_ranks, rank;
+    /* ABI v2 -- group-consistency variants:
+     * pool: FREEKV_POOL_* how the G heads of a group agree on one selection (FreeKV: MeanS);
+     * corr_pool: 0 = mean of the heads' cosines < tau (FreeKV), 1 = "max pooling":
+     * corrected when the least similar head is below tau (reading R-11). */
+    int32_t pool;
+    int32_t corr_pool;
 } freekv_config;
+
+#define FREEKV_POOL_MEAN_S 0  /* mean of per-head softmax weights (FreeKV) */
+#define FREEKV_POOL_MAX_S 1   /* max of per-head softmax weights */
+#define FREEKV_POOL_MEAN_QK 2 /* mean of per-head page scores, one softmax */
+#define FREEKV_POOL_MAX_QK 3  /* max of per-head page scores, one softmax */
+#define FREEKV_POOL_MEAN_Q 4  /* mean query vector of the group, scored once */
+#define FREEKV_POOL_MAX_Q 5   /* element-wise max query vector, scored once */
 
 typedef struct freekv_buffers {
     void* dev;          /* device arena, >= dev_bytes, 256-byte aligned */

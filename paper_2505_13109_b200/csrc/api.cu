@@ -123,6 +123,8 @@ freekv_status validate(const freekv_config* c, FkvDims* D) {
     if (!std::isfinite(c->tau)) return fail(FREEKV_EINVAL, "tau must be finite");
     if (c->first_layer_dense) return fail(FREEKV_EUNSUPPORTED, "first_layer_dense is not served by ABI v1");
     if ((long long)c->batch * c->n_kv > 4096) return fail(FREEKV_EUNSUPPORTED, "batch * n_kv must be <= 4096");
+    if (c->pool < 0 || c->pool > 5) return fail(FREEKV_EINVAL, "pool must be a FREEKV_POOL_* value");
+    if (c->corr_pool < 0 || c->corr_pool > 1) return fail(FREEKV_EINVAL, "corr_pool must be 0 or 1");
     FkvDims d{};
     d.nb = c->batch;
     d.n_qo = c->n_qo;
@@ -144,6 +146,8 @@ freekv_status validate(const freekv_config* c, FkvDims* D) {
     d.score_r = (float)(1.4426950408889634074 / std::sqrt((double)kHeadDim));  // CFR-3
     d.attn_c = (float)(1.4426950408889634074 / std::sqrt((double)kHeadDim));
     d.P_max = d.n_sink + K + d.R_loc;
+    d.pool = c->pool;
+    d.corr_pool = c->corr_pool;
     d.attn_warps = std::min(kMaxAttnWarps, d.U * d.P_max);
     *D = d;
     return FREEKV_OK;
@@ -603,7 +607,7 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         h->sel_cluster = (P2 >= 2048 && D.U * 8 < 2 * sms) ? 16 : 8;  // few units: wider clusters
         h->sel_lptm = std::max(1, P2 / (h->sel_cluster * 128));
         const char* fs = getenv("FREEKV_SELECT");
-        h->fused_select = fs && fs[0] == 'f';
+        h->fused_select = fs && fs[0] == 'f' && h->D.pool == 0 && h->D.corr_pool == 0;
         if (h->fused_select) h->D.direct = 0;  // the cluster select writes slot rows only
         {
             const char* ft = getenv("FREEKV_FIN_THREADS");
@@ -618,7 +622,7 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         }
         // the fused 2-CTA select is opt-in (FREEKV_SELECT=c2): its scoring is ALU-bound on two SMs per
         // unit, while the score kernel spreads it over all SMs -- measured faster end to end
-        h->c2_select = fs && fs[0] == 'c' && select_c2_fits(h->D, h->c2_lpt, h->c2_nt);
+        h->c2_select = fs && fs[0] == 'c' && h->D.pool == 0 && select_c2_fits(h->D, h->c2_lpt, h->c2_nt);
         const char* pp = getenv("FREEKV_PIPELINE");
         h->pipelined = h->D.direct && pp && pp[0] == '1';
         h->one_graph = h->D.direct;  // recalls are forked branches of the one step graph

@@ -28,6 +28,8 @@ struct FkvDims {
     int full_refresh; // diagnostics (env FREEKV_DEBUG_FULL_REFRESH=1): no slot reuse, all pages re-fetched
     int dbg;          // timing experiments only (env FREEKV_DEBUG_EXP, bit flags; results not valid)
     int attn_spec;    // speculative attention over R before the PDL wait (env FREEKV_ATTN_SPEC=1)
+    int pool;         // FREEKV_POOL_* group pooling of the selection (f3); 0 = MeanS
+    int corr_pool;    // 0 = mean of the cosines, 1 = corrected when the least similar head is below tau
     float tau;
     float score_r;    // CFR-3: fl32(log2(e)/sqrt(d))
     float attn_c;     // log2(e)/sqrt(d) for attention softmax (not CFR)

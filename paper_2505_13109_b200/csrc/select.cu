@@ -40,6 +40,14 @@ __device__ __forceinline__ float cexp2_cfr(float x) {
     return __uint_as_float(__float_as_uint(P) + ((uint32_t)ni << 23));
 }
 
+// Group pooling of the heads' cosines (CFR-10): 0 = mean (sequential sum / G, FreeKV);
+// 1 = minimum, the "max pooling over group C_i" of tab:abl-g-corr (reading R-11)
+__device__ __forceinline__ float pool_cos(const float* c, int G, int corr_pool) {
+    float acc = c[0];
+    for (int g = 1; g < G; ++g) acc = corr_pool ? (c[g] < acc ? c[g] : acc) : __fadd_rn(acc, c[g]);
+    return corr_pool ? acc : __fdiv_rn(acc, (float)G);
+}
+
 // ----------------------------------------------------------- a2: scoring
 constexpr int kScoreWarps = 4;
 constexpr int kSummBlockBytes = 32 * 2 * kHeadDim * 2;  // 16 KiB: 32 pages x {min,max} x 128 ch
@@ -152,7 +160,19 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims 
         for (int i = threadIdx.x; i < GP * kHeadDim; i += blockDim.x) {
             const int h = i / kHeadDim, c = i % kHeadDim;
             float x = 0.0f;
-            if (h < G) x = bf16f(q[((size_t)b * D.n_qo + m * G + h) * kHeadDim + c]);
+            if (h < G) {
+                const uint16_t* qc = q + ((size_t)b * D.n_qo + m * G) * kHeadDim + c;
+                if (D.pool >= 4) {  // MeanQ / MaxQ (f3): every head scores the group's pooled query
+                    float a = bf16f(qc[0]);
+                    for (int g = 1; g < G; ++g) {
+                        const float y = bf16f(qc[(size_t)g * kHeadDim]);
+                        a = D.pool == 4 ? __fadd_rn(a, y) : (y > a ? y : a);
+                    }
+                    x = D.pool == 4 ? __fdiv_rn(a, (float)G) : a;
+                } else {
+                    x = bf16f(qc[(size_t)h * kHeadDim]);
+                }
+            }
             qv[c][h] = x;
             qm[c][h] = x >= 0.0f ? 0xffffffffu : 0u;  // CFR-2: q_c >= 0 (incl. -0) uses the max
         }
@@ -362,9 +382,7 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
                         : "memory");
                     for (int g = 0; g < G; ++g) s_cos[g] = cos_in[g];
                 }
-                float acc = s_cos[0];
-                for (int g = 1; g < G; ++g) acc = __fadd_rn(acc, s_cos[g]);
-                const float mean = __fdiv_rn(acc, (float)G);
+                const float mean = pool_cos(s_cos, G, D.corr_pool);
                 int flag;
                 if (D.mode == 1 || D.tau >= 1.0f) flag = 1;
                 else if (D.mode == 2 || D.tau <= 0.0f) flag = 0;
@@ -409,6 +427,19 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
 #pragma unroll
             for (int l = 0; l < LPT; ++l)
                 sv[g][l] = (g < G && cand[l]) ? (ssc ? ssc[g * srow + jb + l] : sg[g * srow + jb + l]) : -INFINITY;
+        // group-consistency variants (f3): QK pools the heads' scores into head 0; Q pools
+        // the queries before scoring (every head then holds the same scores); both use one softmax
+        const int Gs = D.pool >= 2 ? 1 : G;
+        if (D.pool == 2 || D.pool == 3) {
+#pragma unroll
+            for (int l = 0; l < LPT; ++l) {
+                float a = sv[0][l];
+#pragma unroll
+                for (int g = 1; g < GM; ++g)
+                    if (g < G) a = D.pool == 2 ? __fadd_rn(a, sv[g][l]) : (sv[g][l] > a ? sv[g][l] : a);
+                if (cand[l]) sv[0][l] = D.pool == 2 ? __fdiv_rn(a, (float)G) : a;
+            }
+        }
         // ---- CFR-4: max per head (exact, order-free): one warp-wide redux per head, twice
         float M[GM];
 #pragma unroll
@@ -433,7 +464,7 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
         for (int g = 0; g < GM; ++g) {
 #pragma unroll
             for (int l = 0; l < LPT; ++l)
-                sv[g][l] = (g < G && cand[l]) ? cexp2_cfr(__fsub_rn(sv[g][l], M[g])) : 0.0f;  // sv := e
+                sv[g][l] = (g < Gs && cand[l]) ? cexp2_cfr(__fsub_rn(sv[g][l], M[g])) : 0.0f;  // sv := e
             float t[LPT];
 #pragma unroll
             for (int l = 0; l < LPT; ++l) t[l] = sv[g][l];
@@ -471,9 +502,10 @@ __device__ __forceinline__ void finalize_unit(const int u, const FkvDims& D, con
             if (cand[l]) {
 #pragma unroll
                 for (int g = 0; g < GM; ++g) {
-                    if (g < G) {
+                    if (g < Gs) {
                         const float pg = (D.dbg & 4) ? sv[g][l] * (1.0f / Z[g]) : __fdiv_rn(sv[g][l], Z[g]);
-                        pi = g == 0 ? pg : __fadd_rn(pi, pg);
+                        // CFR-8 (MeanS: sequential sum) or MaxS
+                        pi = g == 0 ? pg : (D.pool == 1 ? (pg > pi ? pg : pi) : __fadd_rn(pi, pg));
                     }
                 }
             }
@@ -808,9 +840,7 @@ __global__ void __launch_bounds__(kPrepThreads) fkv_prep_kernel(FkvDims D, FkvLa
         for (int i = tid; i < G * kHeadDim / 2; i += kPrepThreads) qp[i] = s_qa[i];
     }
     if (tid == 0) {
-        float acc = s_cos[0];
-        for (int g = 1; g < G; ++g) acc = __fadd_rn(acc, s_cos[g]);
-        const float mean = __fdiv_rn(acc, (float)G);
+        const float mean = pool_cos(s_cos, G, D.corr_pool);
         int flag;
         if (D.mode == 1 || D.tau >= 1.0f) flag = 1;
         else if (D.mode == 2 || D.tau <= 0.0f) flag = 0;

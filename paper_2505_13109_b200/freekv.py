@@ -44,7 +44,7 @@ class _Config(ctypes.Structure):
         "n_layers", "batch", "n_qo", "n_kv", "head_dim", "page_size", "budget_tokens", "sink_tokens",
         "window_tokens", "max_ctx_tokens")] + [("tau", ctypes.c_float)] + [(n, ctypes.c_int32) for n in (
             "mode", "first_layer_dense", "kv_head_begin", "kv_head_end", "batch_begin", "batch_end",
-            "n_ranks", "rank")]
+            "n_ranks", "rank", "pool", "corr_pool")]
 
 
 class _Buffers(ctypes.Structure):
@@ -73,6 +73,8 @@ class FreeKVConfig:
     batch_end: int = 0
     n_ranks: int = 1
     rank: int = 0
+    pool: int = 0       # FREEKV_POOL_* (SURVEY §8(f) f3); 0 = MeanS (FreeKV)
+    corr_pool: int = 0  # 0 = mean of the cosines (FreeKV), 1 = max pooling of the need to correct
 
     @property
     def G(self) -> int:

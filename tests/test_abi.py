@@ -32,7 +32,7 @@ def test_library_exports_every_header_symbol():
     L = P.load_library()
     for s in syms:
         assert hasattr(L, s)
-    assert L.freekv_abi_version() == 1
+    assert L.freekv_abi_version() == 2
 
 
 def test_library_is_sm100a():

@@ -31,7 +31,7 @@ def rel_err(out, ref):
 
 def run_parity(G=4, n_kv=2, batch=2, page=32, sink=64, window=64, budget=256, L0=700, steps=6,
                n_layers=2, tau=0.8, mode=O.MODE_SPECULATIVE, event_rate=0.3, seed=11, tie_pages=False,
-               check_summaries=True, use_primitives=False, check_fetch=True):
+               check_summaries=True, use_primitives=False, check_fetch=True, pool=0, corr_pool=0):
     _need_gpu()
     import paper_2505_13109_b200 as P
     d = 128
@@ -39,11 +39,11 @@ def run_parity(G=4, n_kv=2, batch=2, page=32, sink=64, window=64, budget=256, L0
     max_ctx = L0 + steps + 3
     cfg = P.FreeKVConfig(n_layers=n_layers, batch=batch, n_qo=n_qo, n_kv=n_kv, head_dim=d, page_size=page,
                          budget_tokens=budget, sink_tokens=sink, window_tokens=window, max_ctx_tokens=max_ctx,
-                         tau=tau, mode=mode)
+                         tau=tau, mode=mode, pool=pool, corr_pool=corr_pool)
     fkv = P.FreeKV(cfg)
     ocfg = O.OracleConfig(n_layers=n_layers, batch=batch, n_qo=n_qo, n_kv=n_kv, head_dim=d, page_size=page,
                           budget_tokens=budget, sink_tokens=sink, window_tokens=window, max_ctx_tokens=max_ctx,
-                          tau=tau, mode=mode)
+                          tau=tau, mode=mode, pool=pool, corr_pool=corr_pool)
     eng = O.OracleEngine(ocfg)
     dev = fkv.device
     for layer in range(n_layers):
@@ -273,3 +273,22 @@ def test_parity_speculative_attention(monkeypatch):
     units discard that work (results identical)."""
     monkeypatch.setenv("FREEKV_ATTN_SPEC", "1")
     run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=6)
+
+
+@pytest.mark.parametrize("pool", [1, 2, 3, 4, 5])
+def test_parity_pooling_variants(pool):
+    """Group-consistency variants: MaxS, MeanQK, MaxQK, MeanQ, MaxQ --
+    bit-exact selections against the oracle, G = 4 and G = 7."""
+    run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=4, pool=pool)
+    run_parity(G=7, n_kv=1, batch=1, page=16, sink=64, window=64, budget=640, L0=5000, steps=3, n_layers=1,
+               pool=pool)
+
+
+@pytest.mark.parametrize("pipeline", ["0", "1"])
+def test_parity_max_pooled_correction(pipeline, monkeypatch):
+    """Max-pooled correction (tab:abl-g-corr, reading R-11): corrected when any head's similarity
+    is below tau; more units corrected than with mean pooling on the same inputs."""
+    monkeypatch.setenv("FREEKV_PIPELINE", pipeline)
+    nf_max, _, _ = run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=5, corr_pool=1, event_rate=0.3)
+    nf_mean, _, _ = run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=5, corr_pool=0, event_rate=0.3)
+    assert nf_max >= nf_mean

@@ -19,6 +19,8 @@ ap.add_argument("--n_kv", type=int, default=8)
 ap.add_argument("--event_rate", type=float, default=0.05)
 ap.add_argument("--tau", type=float, default=0.8)
 ap.add_argument("--mode", type=int, default=0, help="0 speculative, 1 always correct, 2 never correct")
+ap.add_argument("--pool", type=int, default=0, help="FREEKV_POOL_* group pooling (f3)")
+ap.add_argument("--corr_pool", type=int, default=0)
 ap.add_argument("--no-profile", action="store_true")
 ap.add_argument("--graph", action="store_true", help="whole-step graph replay with in-graph event profiling")
 a = ap.parse_args()
@@ -26,7 +28,7 @@ dev = torch.device("cuda", 0)
 nb, nq, nk, d, p = a.batch, a.n_qo, a.n_kv, 128, 32
 G = nq // nk
 cfg = P.FreeKVConfig(n_layers=a.layers, batch=nb, n_qo=nq, n_kv=nk, max_ctx_tokens=a.ctx + a.warmup + a.steps + 2,
-                     tau=a.tau, mode=a.mode)
+                     tau=a.tau, mode=a.mode, pool=a.pool, corr_pool=a.corr_pool)
 fkv = P.FreeKV(cfg)
 s = fkv.stream
 seed = synth.SEED0 + 2
