@@ -303,7 +303,9 @@ __device__ __forceinline__ void attend_pages(const FkvDims& D, const FkvScratch&
                                              const CUtensorMap* tmap_p, const CUtensorMap* tmap_hp, const Src& src,
                                              int pa, int pb, uint8_t* ring, uint64_t* bars, uint32_t& phase_bits,
                                              float (&m_run)[2], float (&l_run)[2], float (&oacc)[8][4], int tcls,
-                                             int w) {
+                                             int w, int pre = 0) {
+    // pre: the first `pre` slabs of entry pa are already in flight in stages 0..pre-1 (issued
+    // from the same rows before the PDL wait)
     constexpr int kStages = NST;
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const int spp = D.p >> 4, lspp = spp == 1 ? 0 : (spp == 2 ? 1 : 2);
@@ -333,7 +335,7 @@ __device__ __forceinline__ void attend_pages(const FkvDims& D, const FkvScratch&
         if (lane == 0) {
 #pragma unroll
             for (int i = 0; i < kStages; ++i)
-                if (valids[i] > 0)
+                if (valids[i] > 0 && !(cb == pa && i < pre))
                     issue_slab(is_host(i) ? &tmap_h : &tmap, ring + i * kSlabBytes, &bars[i], rows[i], D.p);
         }
         for (int i = 0; i < nx; ++i) {
@@ -557,6 +559,36 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2)
     // this launch only after its own PDL wait, so the previous layer is complete and q_i may
     // be read here.
     int spec_end = pa;  // entries [pa, spec_end) attended speculatively
+    int pre = 0;        // slabs of entry pa prefetched speculatively (default mode)
+    if (phase == 0 && rk < D.U && pa < pbc && !D.attn_spec && !(D.dbg & 8)) {
+        // default: only prefetch this warp's first slabs if they lie in the sink + R head of the
+        // list (rows from state the select does not modify); a corrected unit drains them
+        const int u0 = rk;
+        const int rv = L.res_valid[u0], rc = L.res_cnt[u0], ctx_any = L.ctx[u0];
+        const int spp = D.p >> 4;
+        int slot_of[kStages];
+#pragma unroll
+        for (int x = 0; x < kStages; ++x) {
+            const int a = pa + x / spp - D.n_sink;
+            slot_of[x] = (a >= 0 && a < D.K) ? L.res_slot[(size_t)u0 * D.K + a] : 0;
+        }
+        if (rv && !D.full_refresh && ctx_any >= D.S_tok) {
+            const int n_spec = D.n_sink + rc, pr = 2 * D.p;
+            int row[kStages];
+#pragma unroll
+            for (int x = 0; x < kStages; ++x) {
+                const int pi = pa + x / spp;
+                row[x] = -1;
+                if (pi < pbc && pi < n_spec)
+                    row[x] = (pi < D.n_sink ? (int)((L.sink - L.arena) / kHeadDim) + (u0 * D.n_sink + pi) * pr
+                                            : (int)((L.slots - L.arena) / kHeadDim) + (u0 * 2 * D.K + slot_of[x]) * pr) +
+                             (x % spp) * 16;
+            }
+            while (pre < kStages && row[pre] >= 0) ++pre;
+            if (lane == 0)
+                for (int x = 0; x < pre; ++x) issue_slab(&tmap, ring + x * kSlabBytes, &bar[warp][x], row[x], D.p);
+        }
+    }
     if (phase == 0 && rk < D.U && pa < pbc && D.attn_spec) {  // FREEKV_ATTN_SPEC=1 (off by default: measured
                                                                // slower, it competes with the select)
         const int u0 = rk;
@@ -593,11 +625,18 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2)
         spec_end = pa;
     }
     if (spec_end == pa) load_q_frags(D, q, u, qa);
+    if (pre > 0 && L.flags[u]) {  // corrected unit: the prefetched slabs are not its pages
+        for (int x = 0; x < pre; ++x) {
+            mbar_wait(&bar[warp][x], (phase_bits >> x) & 1u);
+            phase_bits ^= 1u << x;
+        }
+        pre = 0;
+    }
     {
         const TableSrc tsrc{X.page_rows + (size_t)u * D.P_max, X.page_valid + (size_t)u * D.P_max,
                             X.page_dst + (size_t)u * D.P_max};
         attend_pages<NST>(D, X, qa, &tmap, &tmap_h, tsrc, spec_end, min(pbc, X.page_cnt[u]), ring, bar[warp],
-                          phase_bits, m_run, l_run, oacc, tcls, w);
+                          phase_bits, m_run, l_run, oacc, tcls, w, pre);
     }
     if (lane == 0) trace_stamp(X.trace, tcls, w, 3);
     // ---- this warp's record, in its own (now idle) ring: o [G][128], then m [G], l [G]
