@@ -92,6 +92,44 @@ __device__ __forceinline__ void score_channels(const uint4* blk, int c8_begin, i
     }
 }
 
+// Even G: the same recipe with the select folded into the arithmetic and two heads per
+// instruction.  With q+ = max(q, 0), q- = min(q, 0): u = fma(q-_c, mn_c, fma(q+_c, mx_c, u)) --
+// one product is a signed zero, so each step is CFR-2's single rounding (equal up to the sign
+// of zero, which CFR-2 allows) -- evaluated for heads (h, h+1) at once with FFMA2
+// (fma.rn.f32x2, sm_100a).  qp/qn hold q+ / q- per channel and head.
+template <int G>
+__device__ __forceinline__ void score_channels_x2(const uint4* blk, int c8_begin, int lane,
+                                                  const float (*qp)[(G + 3) / 4 * 4],
+                                                  const float (*qn)[(G + 3) / 4 * 4],
+                                                  unsigned long long (&acc2)[G / 2]) {
+#pragma unroll 2
+    for (int c8 = c8_begin; c8 < c8_begin + 4; ++c8) {
+        const uint4 mn4 = blk[(c8 * 2 + 0) * 32 + lane];
+        const uint4 mx4 = blk[(c8 * 2 + 1) * 32 + lane];
+        const uint32_t mnw[4] = {mn4.x, mn4.y, mn4.z, mn4.w};
+        const uint32_t mxw[4] = {mx4.x, mx4.y, mx4.z, mx4.w};
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                const int c = c8 * 8 + 2 * w + half;
+                const uint32_t mnb = half ? (mnw[w] & 0xffff0000u) : (mnw[w] << 16);
+                const uint32_t mxb = half ? (mxw[w] & 0xffff0000u) : (mxw[w] << 16);
+                unsigned long long mx2, mn2;
+                asm("mov.b64 %0, {%1, %1};" : "=l"(mx2) : "r"(mxb));
+                asm("mov.b64 %0, {%1, %1};" : "=l"(mn2) : "r"(mnb));
+#pragma unroll
+                for (int k = 0; k < G / 2; ++k) {
+                    const unsigned long long p2 = *reinterpret_cast<const unsigned long long*>(&qp[c][2 * k]);
+                    const unsigned long long n2 = *reinterpret_cast<const unsigned long long*>(&qn[c][2 * k]);
+                    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc2[k]) : "l"(p2), "l"(mx2));
+                    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc2[k]) : "l"(n2), "l"(mn2));
+                }
+            }
+        }
+    }
+}
+
 // Thread per page, warp per 32-page summary block, CTA = 4 consecutive blocks of
 // one unit (so q is staged once per CTA).  Each warp streams its 16 KiB block
 // through a 3-slot ring of 4 KiB chunks (4 channel-groups of 32 channels) filled
@@ -173,8 +211,13 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims 
                     x = bf16f(qc[(size_t)h * kHeadDim]);
                 }
             }
-            qv[c][h] = x;
-            qm[c][h] = x >= 0.0f ? 0xffffffffu : 0u;  // CFR-2: q_c >= 0 (incl. -0) uses the max
+            if (G % 2 == 0) {  // FFMA2 form: q+ / q- (qm holds q- as float bits)
+                qv[c][h] = x >= 0.0f ? x : 0.0f;
+                qm[c][h] = __float_as_uint(x >= 0.0f ? 0.0f : x);
+            } else {
+                qv[c][h] = x;
+                qm[c][h] = x >= 0.0f ? 0xffffffffu : 0u;  // CFR-2: q_c >= 0 (incl. -0) uses the max
+            }
         }
         __syncthreads();
         if (threadIdx.x == 0) trace_stamp(trace, tcls, tent, 1);
@@ -182,14 +225,21 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims 
         float acc[G];
 #pragma unroll
         for (int h = 0; h < G; ++h) acc[h] = 0.0f;
+        unsigned long long acc2[G / 2 > 0 ? G / 2 : 1];
+#pragma unroll
+        for (int k = 0; k < (G / 2 > 0 ? G / 2 : 1); ++k) acc2[k] = 0ull;
 #pragma unroll 1
         for (int k = 0; k < 4; ++k) {
             const int slot = k % kRing;
             mbar_wait(&bar[warp][slot], (ph >> slot) & 1u);
             ph ^= 1u << slot;
             if (k == 0 && threadIdx.x == 0) trace_stamp(trace, tcls, tent, 2);
-            score_channels<G>(reinterpret_cast<const uint4*>(ring + slot * kChunkBytes) - (k * 4) * 2 * 32, k * 4,
-                              lane, qv, qm, acc);
+            if constexpr (G % 2 == 0)
+                score_channels_x2<G>(reinterpret_cast<const uint4*>(ring + slot * kChunkBytes) - (k * 4) * 2 * 32,
+                                     k * 4, lane, qv, reinterpret_cast<const float(*)[(G + 3) / 4 * 4]>(qm), acc2);
+            else
+                score_channels<G>(reinterpret_cast<const uint4*>(ring + slot * kChunkBytes) - (k * 4) * 2 * 32, k * 4,
+                                  lane, qv, qm, acc);
             if (k + kRing < 4) {
                 __syncwarp();  // all lanes are done with this slot
                 if (lane == 0) {
@@ -201,6 +251,15 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 4) fkv_score_kernel(FkvDims 
             }
         }
         __syncwarp();  // every lane is done with the ring before the next item refills it
+        if constexpr (G % 2 == 0) {
+#pragma unroll
+            for (int k2 = 0; k2 < G / 2; ++k2) {
+                uint32_t lo, hi;
+                asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(acc2[k2]));
+                acc[2 * k2] = __uint_as_float(lo);
+                acc[2 * k2 + 1] = __uint_as_float(hi);
+            }
+        }
         const int j = blk * 32 + lane;
         if (j >= D.n_sink && j < n_off) {
 #pragma unroll
