@@ -303,9 +303,10 @@ __device__ __forceinline__ void attend_pages(const FkvDims& D, const FkvScratch&
                                              const CUtensorMap* tmap_p, const CUtensorMap* tmap_hp, const Src& src,
                                              int pa, int pb, uint8_t* ring, uint64_t* bars, uint32_t& phase_bits,
                                              float (&m_run)[2], float (&l_run)[2], float (&oacc)[8][4], int tcls,
-                                             int w, int pre = 0) {
-    // pre: the first `pre` slabs of entry pa are already in flight in stages 0..pre-1 (issued
-    // from the same rows before the PDL wait)
+                                             int w, int pre = 0, int skip = 0, int trim = 0) {
+    // pre: the first `pre` slabs of this range are already in flight in stages 0..pre-1 (issued
+    // from the same rows before the PDL wait).  skip / trim: the range starts `skip` slabs into
+    // entry pa and ends `trim` slabs before the end of entry pb - 1 (slab-granular split)
     constexpr int kStages = NST;
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const int spp = D.p >> 4, lspp = spp == 1 ? 0 : (spp == 2 ? 1 : 2);
@@ -320,7 +321,8 @@ __device__ __forceinline__ void attend_pages(const FkvDims& D, const FkvScratch&
         int my_row = 0, my_valid = 0, my_dst = 0;
         if (lane < np) src.load(cb + lane, my_row, my_valid, my_dst);
         const unsigned host_mask = __ballot_sync(0xffffffffu, my_valid & 0x80);  // pages read from the host pool
-        const int nx = np * spp;
+        const int nx = np * spp - (cb + 32 >= pb ? trim : 0);  // last chunk: drop the trimmed slabs
+        const int i0 = cb == pa ? skip : 0;
         if (lane == 0) trace_stamp(X.trace, tcls, w, 1);
         auto slab_of = [&](int x, int& row) {  // warp-uniform; spp = 1 << lspp
             const int pi = x >> lspp, sl = x & (spp - 1);
@@ -331,15 +333,15 @@ __device__ __forceinline__ void attend_pages(const FkvDims& D, const FkvScratch&
         // prologue: first kStages slabs of this segment in flight
         int rows[kStages], valids[kStages];
 #pragma unroll
-        for (int i = 0; i < kStages; ++i) valids[i] = i < nx ? slab_of(i, rows[i]) : 0;
+        for (int i = 0; i < kStages; ++i) valids[i] = i0 + i < nx ? slab_of(i0 + i, rows[i]) : 0;
         if (lane == 0) {
 #pragma unroll
             for (int i = 0; i < kStages; ++i)
                 if (valids[i] > 0 && !(cb == pa && i < pre))
-                    issue_slab(is_host(i) ? &tmap_h : &tmap, ring + i * kSlabBytes, &bars[i], rows[i], D.p);
+                    issue_slab(is_host(i0 + i) ? &tmap_h : &tmap, ring + i * kSlabBytes, &bars[i], rows[i], D.p);
         }
-        for (int i = 0; i < nx; ++i) {
-            const int stg = i % kStages;
+        for (int i = i0; i < nx; ++i) {
+            const int stg = (i - i0) % kStages;
             int row;
             const int valid = slab_of(i, row);
             int row2 = 0, valid2 = 0;
@@ -542,7 +544,13 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2)
     __syncwarp();
     uint32_t phase_bits = 0u;
     const int k = crank * W + warp;
-    const int pa = (int)((long long)k * D.P_max / NW), pbc = (int)((long long)(k + 1) * D.P_max / NW);
+    // this warp's share of the unit's page list, in 16-token slabs (an even split of P_max * spp
+    // slabs; whole entries [pa, pbc) minus `skip` slabs at the front and `trim` at the back).
+    // The speculative-attention mode splits by whole entries.
+    const int spp = D.p >> 4, TS = D.attn_spec ? D.P_max : D.P_max * spp, gran = D.attn_spec ? 1 : spp;
+    const int sa = (int)((long long)k * TS / NW), sb = (int)((long long)(k + 1) * TS / NW);
+    const int pa = sa / gran, pbc = (sb + gran - 1) / gran;
+    const int skip = sa - pa * gran, trim = pbc * gran - sb;
     float oacc[8][4];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -565,11 +573,10 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2)
         // list (rows from state the select does not modify); a corrected unit drains them
         const int u0 = rk;
         const int rv = L.res_valid[u0], rc = L.res_cnt[u0], ctx_any = L.ctx[u0];
-        const int spp = D.p >> 4;
         int slot_of[kStages];
 #pragma unroll
         for (int x = 0; x < kStages; ++x) {
-            const int a = pa + x / spp - D.n_sink;
+            const int a = pa + (skip + x) / spp - D.n_sink;
             slot_of[x] = (a >= 0 && a < D.K) ? L.res_slot[(size_t)u0 * D.K + a] : 0;
         }
         if (rv && !D.full_refresh && ctx_any >= D.S_tok) {
@@ -577,12 +584,12 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2)
             int row[kStages];
 #pragma unroll
             for (int x = 0; x < kStages; ++x) {
-                const int pi = pa + x / spp;
+                const int pi = pa + (skip + x) / spp;
                 row[x] = -1;
-                if (pi < pbc && pi < n_spec)
+                if (pa * spp + skip + x < sb && pi < n_spec)
                     row[x] = (pi < D.n_sink ? (int)((L.sink - L.arena) / kHeadDim) + (u0 * D.n_sink + pi) * pr
                                             : (int)((L.slots - L.arena) / kHeadDim) + (u0 * 2 * D.K + slot_of[x]) * pr) +
-                             (x % spp) * 16;
+                             ((skip + x) % spp) * 16;
             }
             while (pre < kStages && row[pre] >= 0) ++pre;
             if (lane == 0)
@@ -635,8 +642,9 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, NST == 2 ? 3 : 2)
     {
         const TableSrc tsrc{X.page_rows + (size_t)u * D.P_max, X.page_valid + (size_t)u * D.P_max,
                             X.page_dst + (size_t)u * D.P_max};
-        attend_pages<NST>(D, X, qa, &tmap, &tmap_h, tsrc, spec_end, min(pbc, X.page_cnt[u]), ring, bar[warp],
-                          phase_bits, m_run, l_run, oacc, tcls, w, pre);
+        const int pe = min(pbc, X.page_cnt[u]);
+        attend_pages<NST>(D, X, qa, &tmap, &tmap_h, tsrc, spec_end, pe, ring, bar[warp], phase_bits, m_run, l_run,
+                          oacc, tcls, w, pre, spec_end == pa ? skip : 0, pe == pbc ? trim : 0);
     }
     if (lane == 0) trace_stamp(X.trace, tcls, w, 3);
     // ---- this warp's record, in its own (now idle) ring: o [G][128], then m [G], l [G]
