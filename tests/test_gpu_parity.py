@@ -292,3 +292,58 @@ def test_parity_max_pooled_correction(pipeline, monkeypatch):
     nf_max, _, _ = run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=5, corr_pool=1, event_rate=0.3)
     nf_mean, _, _ = run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=5, corr_pool=0, event_rate=0.3)
     assert nf_max >= nf_mean
+
+
+def test_parity_full_size_c2_step_graph():
+    """BASELINE.json configs[1] sizes (Llama-3.1-8B heads 32q/8kv, d=128, ctx 32K, batch 8,
+    budget 2048, S = W = 512, page 32) in the launch configuration bench.py times: the
+    whole-step CUDA graph, default kernels.  Two layers (the per-layer path is identical for
+    all 32), every unit compared with the oracle: page indices, frontier and flags
+    bit-exact, outputs within 2e-3.  Step 0 is all-flagged (synchronous full recall), the
+    later steps are speculative with seeded query dips (event rate 0.05 as in the bench)."""
+    _need_gpu()
+    import paper_2505_13109_b200 as P
+    nb, n_kv, G, d, p, n_layers, steps = 8, 8, 4, 128, 32, 2, 4
+    n_qo = G * n_kv
+    L0 = 32768 - steps                      # the last step attends over exactly 32K tokens
+    kw = dict(n_layers=n_layers, batch=nb, n_qo=n_qo, n_kv=n_kv, head_dim=d, page_size=p, budget_tokens=2048,
+              sink_tokens=512, window_tokens=512, max_ctx_tokens=L0 + steps + 2, tau=0.8,
+              mode=O.MODE_SPECULATIVE)
+    fkv = P.FreeKV(P.FreeKVConfig(**kw))
+    eng = O.OracleEngine(O.OracleConfig(**kw))
+    dev = fkv.device
+    seed = 250513119
+    for layer in range(n_layers):
+        k, v = synth.gen_prefill(nb, n_kv, d, p, L0, 512 // p, fkv.K, seed, layer, device=dev)
+        torch.cuda.synchronize()
+        fkv.append_kv(layer, k, v)
+        fkv.synchronize()
+        eng.append(layer, synth.bf16_bits(k), synth.bf16_bits(v))
+        del k, v
+    qps = [synth.QueryProcess(nb, n_qo, n_kv, d, seed, l, device=dev, event_rate=0.05) for l in range(n_layers)]
+    qb = torch.empty(n_layers, nb, n_qo, d, dtype=torch.bfloat16, device=dev)
+    kb = torch.empty(n_layers, nb, 1, n_kv, d, dtype=torch.bfloat16, device=dev)
+    vb = torch.empty_like(kb)
+    ob = torch.empty(n_layers, nb, n_qo, d, dtype=torch.float32, device=dev)
+    fkv.step_graph_capture(qb, kb, vb, ob)
+    n_flag = 0
+    for i in range(steps):
+        for l in range(n_layers):
+            q, _ = qps[l].next()
+            kn, vn = synth.gen_decode_kv(nb, n_kv, d, p, L0 + i, seed, l, device=dev)
+            qb[l].copy_(q); kb[l].copy_(kn); vb[l].copy_(vn)
+        torch.cuda.synchronize()
+        fkv.step_graph_launch()
+        fkv.synchronize()
+        for l in range(n_layers):
+            ref = eng.step(l, synth.bf16_bits(qb[l]), synth.bf16_bits(kb[l]), synth.bf16_bits(vb[l]))
+            sel = fkv.get_selection(l)
+            assert np.array_equal(sel["flags"], ref["flags"]), (i, l)
+            assert np.array_equal(sel["frontier"], ref["frontier"]), (i, l)
+            assert np.array_equal(sel["pages"], ref["sel"]), (i, l)
+            e = rel_err(ob[l].cpu().numpy().astype(np.float64), ref["out"])
+            assert e <= REL_TOL, (i, l, e)
+            if i > 0:
+                n_flag += int(ref["flags"].sum())
+    assert n_flag < (steps - 1) * n_layers * nb * n_kv   # speculative steps did not all correct
+    fkv.close()
