@@ -58,7 +58,7 @@ struct freekv_handle {
     std::vector<int> ctx_host;
     std::vector<int> recall_pending;
     int lpt = 1, lpt1k = 1;  // leaves per thread of the 512 / 1024-thread select tree (fixed per handle, CFR-6)
-    int fin_nt = 512;        // threads of the select kernel (FREEKV_FIN_THREADS=1024 for the wide variant)
+    int fin_nt = 1024;       // threads of the select kernel (FREEKV_FIN_THREADS=512 for the narrow variant)
     int sel_cluster = 8, sel_lptm = 1;  // fused select: CTAs per unit, max leaves per thread
     bool fused_select = false;          // FREEKV_SELECT=fused selects the one-launch cluster kernel
     int c2_nt = 512, c2_lpt = 2;        // threads per CTA / leaves per thread of the fused select
@@ -611,7 +611,8 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         if (h->fused_select) h->D.direct = 0;  // the cluster select writes slot rows only
         {
             const char* ft = getenv("FREEKV_FIN_THREADS");
-            h->fin_nt = (ft && atoi(ft) == 1024) ? 1024 : 512;  // 512: measured slightly faster
+            // 1024 (default): r1_v8 A/B -1.4 us/layer on c2, -5.9 on c3 (profiles/r1_v8_fin_ab.txt)
+            h->fin_nt = (ft && atoi(ft) == 512) ? 512 : 1024;
         }
         {
             const char* ne = getenv("FREEKV_SELECT_THREADS");  // 256, 512 (default) or 1024

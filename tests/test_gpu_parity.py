@@ -251,6 +251,15 @@ def test_parity_fused_c2_select(monkeypatch):
     run_parity(G=4, n_kv=1, batch=1, page=16, sink=64, window=64, budget=640, L0=20000, steps=3, n_layers=1)
 
 
+@pytest.mark.parametrize("threads", ["512", "1024"])
+def test_parity_select_finalize_threads(threads, monkeypatch):
+    """The default (unfused) select kernel at 512 and 1024 threads: leaves per thread change,
+    the pairwise tree of CFR-6 does not; |J| above 1024 too."""
+    monkeypatch.setenv("FREEKV_FIN_THREADS", threads)
+    run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=4)
+    run_parity(G=7, n_kv=1, batch=2, page=16, sink=64, window=64, budget=640, L0=20000, steps=3, n_layers=1)
+
+
 @pytest.mark.parametrize("threads", ["256", "512", "1024"])
 def test_parity_select_threads(threads, monkeypatch):
     """The fused select at other CTA sizes (leaves per thread change; the tree does not)."""
