@@ -36,6 +36,11 @@ CONFIGS = {
     # BASELINE.json configs[2]
     "c3": dict(workload="qwen2.5-7b-28layers-ctx128k-b4-budget2048", n_layers=28, batch=4, n_qo=28, n_kv=4,
                ctx=131072, budget=2048, sink=512, window=512, tau=0.8, event_rate=0.05),
+    # BASELINE.json configs[3]: DeepSeek-R1-Distill-Llama-8B shape (Llama-3.1-8B heads, 32 layers) at
+    # the end of 16K prompt + 32K generated tokens; batch 8 (the paper states none); --tau sweeps
+    # the correction threshold
+    "c4": dict(workload="r1-distill-llama-8b-32layers-ctx48k-b8-budget2048", n_layers=32, batch=8, n_qo=32,
+               n_kv=8, ctx=49152, budget=2048, sink=512, window=512, tau=0.8, event_rate=0.05),
 }
 
 METRIC = "decode-step µs/layer and tokens/s at 32K ctx; attn HBM GB/s; recall GB/s vs host link"
@@ -52,6 +57,7 @@ def parse():
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=None)
+    ap.add_argument("--tau", type=float, default=None, help="correction threshold (default: the config's)")
     ap.add_argument("--eager", action="store_true", help="per-layer C-ABI calls instead of the whole-step graph")
     return ap.parse_args()
 
@@ -471,7 +477,9 @@ def run_oracle_sample(c, seconds, seed):
 
 def main():
     args = parse()
-    c = CONFIGS[args.config]
+    c = dict(CONFIGS[args.config])
+    if args.tau is not None:
+        c["tau"] = args.tau
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
