@@ -8,14 +8,19 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "..", "build", "obj")
-LIB = os.path.join(HERE, "libfreekv.so")
+# A/B builds only: FKV_VARIANT=<name> with FKV_VARIANT_DEFS="-DX=.." builds libfreekv_<name>.so from the same
+# sources (loaded with FREEKV_LIB_SUFFIX=_<name>); the default build takes neither
+VARIANT = os.environ.get("FKV_VARIANT", "")
+VARIANT_DEFS = os.environ.get("FKV_VARIANT_DEFS", "").split() if VARIANT else []
+OBJ = os.path.join(HERE, "..", "build", "obj" + ("_" + VARIANT if VARIANT else ""))
+LIB = os.path.join(HERE, "libfreekv" + ("_" + VARIANT if VARIANT else "") + ".so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-I" + os.path.join(HERE, "..", "include")]
+FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
+                "-I" + os.path.join(HERE, "..", "include")] + VARIANT_DEFS
 
-SOURCES = ["api.cu", "append.cu", "select.cu", "select_fused.cu", "recall.cu", "attn.cu"]
-HEADERS = ["fkv_internal.cuh", "append_unit.cuh"]
+SOURCES = ["api.cu", "append.cu", "score.cu", "select.cu", "recall.cu", "attn.cu", "layer.cu"]
+HEADERS = ["fkv_internal.cuh", "append_unit.cuh", "attn_core.cuh", "select_core.cuh"]
 
 
 def _mtime(p):

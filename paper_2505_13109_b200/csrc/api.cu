@@ -19,6 +19,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -28,6 +30,25 @@
 using namespace fkv;
 
 static thread_local std::string g_last_error;
+
+namespace fkv {
+// once per (kernel, device, size): opt-in dynamic shared memory + max-shared carveout
+cudaError_t func_smem(const void* kern, size_t dyn_smem) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = done.find({kern, dev});
+    if (it != done.end() && it->second >= dyn_smem) return cudaSuccess;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    if (e == cudaSuccess) done[{kern, dev}] = dyn_smem;
+    return e;
+}
+}  // namespace fkv
 
 static freekv_status fail(freekv_status st, const std::string& msg) {
     g_last_error = msg;
@@ -49,22 +70,25 @@ struct freekv_handle {
     FkvDims D;
     std::vector<FkvLayer> layers;
     FkvScratch X;
+    int device = 0;
     cudaStream_t cs = nullptr, rs = nullptr;
-    cudaStream_t ss = nullptr;  // library-owned high-priority stream for the synchronous recall
-    std::vector<cudaEvent_t> ev_select, ev_recall, ev_sync, ev_sync_x, ev_pre, ev_fl;
-    bool pipelined = false;      // overlapped step (FREEKV_PIPELINE=1; needs direct mode)
+    cudaStream_t ss = nullptr;  // library-owned high-priority stream for the synchronous recall (recall mode)
+    std::vector<cudaEvent_t> ev_select, ev_recall, ev_sync, ev_sync_x;
     bool one_graph = false;      // direct mode: recalls are forked branches of the one step graph
-    int attn_cluster = 0;        // CTAs per unit of the clustered attention (0: split + combine kernels)
+    bool spec = false;           // speculative decode step: attention beside the side chain (attn.cu mode 1)
+    bool fused = false;          // fused decode step: one cluster kernel per layer (layer.cu), the default
+    int ly_c = 0, ly_lpt = 0;    // its CTAs per unit and pages (tree leaves) per thread
+    std::vector<cudaStream_t> side;  // side streams of the speculative step (score -> select -> recall)
+    std::vector<cudaEvent_t> ev_pre;  // fork point of each layer's side chain (after its pre kernel)
+    int prio_hi = 0;             // kernel priority of the critical path (pre, attention)
+    int attn_cluster = 1;        // CTAs per unit of the clustered attention
+    int sel_nc = 1, sel_lpt = 1; // select: CTAs per unit (cluster), leaves per thread (CFR-6 tree)
+    int fsel_nc = 1, fsel_lpt = 1;  // the corrected units' select on the critical path (speculative step)
+    int bsel_nc = 1, bsel_lpt = 1;  // the other units' select in the side chain (speculative step)
     std::vector<int> ctx_host;
     std::vector<int> recall_pending;
-    int lpt = 1, lpt1k = 1;  // leaves per thread of the 512 / 1024-thread select tree (fixed per handle, CFR-6)
-    int fin_nt = 1024;       // threads of the select kernel (FREEKV_FIN_THREADS=512 for the narrow variant)
-    int sel_cluster = 8, sel_lptm = 1;  // fused select: CTAs per unit, max leaves per thread
-    bool fused_select = false;          // FREEKV_SELECT=fused selects the one-launch cluster kernel
-    int c2_nt = 512, c2_lpt = 2;        // threads per CTA / leaves per thread of the fused select
-    bool c2_select = false;             // score + select fused in 2-CTA clusters (FREEKV_SELECT=c2)
     bool pdl = true;                    // programmatic dependent launch (FREEKV_PDL=0 disables)
-    bool serial_recall = false;  // diagnostics: FREEKV_SERIAL_RECALL=1 runs background recall on the compute stream
+    bool serial_recall = false;  // f2 ablation: FREEKV_SERIAL_RECALL=1 runs background recall on the compute stream
     // profiling (freekv_profile_begin/end)
     bool prof = false;
     uint32_t prof_mask = ~0u;  // kernel classes bracketed by events while profiling
@@ -90,8 +114,8 @@ struct Sizes {
     size_t o_summ, o_sink, o_slots, o_ring, o_qprev, o_res_pages, o_res_slot, o_res_front, o_res_valid, o_res_cnt,
         o_pend_cnt,
         o_pend_pages, o_pend_slot, o_pend_front, o_flags, o_cbar, o_fetch_page, o_fetch_slot, o_n_fetch, o_ctx,
-        o_n_off;
-    size_t o_scores, o_part_o, o_part_ml, o_page_rows, o_page_cnt, o_page_valid, o_page_dst, o_cosv;
+        o_n_off, o_qcur, o_scores, o_pend_valid, o_order, o_ord_cnt, o_score_done;
+    size_t o_part_o, o_part_ml, o_page_rows, o_page_cnt, o_page_valid, o_page_dst, o_ready;
 };
 
 freekv_status validate(const freekv_config* c, FkvDims* D) {
@@ -183,16 +207,21 @@ Sizes compute_sizes(const freekv_config* c, const FkvDims& D) {
     s.o_n_fetch = take(U * 4);
     s.o_ctx = take(U * 4);
     s.o_n_off = take(U * 4);
+    s.o_qcur = take((size_t)D.nb * D.n_qo * D.d * 2);
+    s.o_scores = take(U * D.G * D.n_page_max * 4);
+    s.o_pend_valid = take(U * 4);
+    s.o_order = take(U * 4);
+    s.o_ord_cnt = take(4 * 4);
+    s.o_score_done = take(U * 4);
     s.layer_bytes = o;
     o = 0;
-    s.o_scores = take(U * D.G * D.n_page_max * 4);
     s.o_part_o = take((size_t)4 * kMaxAttnWarps * D.G * D.d * 4);
     s.o_part_ml = take((size_t)4 * kMaxAttnWarps * D.G * 2 * 4);
     s.o_page_rows = take(U * D.P_max * 4);
     s.o_page_cnt = take(U * 4);
     s.o_page_valid = take(U * D.P_max);
     s.o_page_dst = take(U * D.P_max * 4);
-    s.o_cosv = take(U * kMaxG * 4);
+    s.o_ready = take(U * 4);
     s.scratch_bytes = o;
     s.dev_bytes = s.layer_bytes * c->n_layers + s.scratch_bytes;
     s.host_layer_bytes = (size_t)D.nb * D.n_page_host * D.n_kv * pe_b;
@@ -210,8 +239,7 @@ cudaStream_t pick(freekv_handle* h, void* s) { return s ? (cudaStream_t)s : h->c
 
 int max_n_off(const FkvDims& D, int ctx) { return std::max(D.n_sink, ctx / D.p - D.n_win); }
 
-enum { K_APPEND = 0, K_SCORE, K_FINALIZE, K_RECALL_SYNC, K_RECALL_BG, K_ATTN_SPLIT, K_ATTN_COMBINE, K_ATTN_P2,
-       K_PREP, K_SCORE_BG, K_FINALIZE_BG };
+enum { K_APPEND = 0, K_SCORE, K_FINALIZE, K_RECALL_SYNC, K_RECALL_BG, K_ATTN_SPLIT, K_ATTN_COMBINE, K_ATTN_P2, K_PRE };
 
 template <class F>
 cudaError_t timed(freekv_handle* h, int cls, cudaStream_t s, F&& launch) {
@@ -239,14 +267,13 @@ freekv_status do_append(freekv_handle* h, int layer, const void* k, const void* 
     return FREEKV_OK;
 }
 
-// k_new/v_new non-NULL: the decode step's single-token append is fused into the
-// finalize kernel (requires W >= p so the summaries of this step's candidates were
-// written at page completion in earlier steps; append_unit.cuh).
+// Rows a2-a4 on stream s (primitive API and the serial decode step): page scoring, then the
+// select kernel.  flag_src 1: the pre kernel decided the correction flags; list_all: page lists of
+// every unit for the attention.
 freekv_status do_select(freekv_handle* h, int layer, const void* q, int32_t* pages_out, uint8_t* corr_out,
-                        cudaStream_t s, const void* k_new = nullptr, const void* v_new = nullptr) {
+                        cudaStream_t s, int flag_src, int list_all) {
     if (!q) return fail(FREEKV_EINVAL, "q is NULL");
-    const int pending = k_new ? 1 : 0;
-    if (h->ctx_host[layer] + pending <= 0) return fail(FREEKV_ESTATE, "select before any token was appended");
+    if (h->ctx_host[layer] <= 0) return fail(FREEKV_ESTATE, "select before any token was appended");
     // the background recall of the previous step reads this layer's fetch list (one-graph
     // capture: the previous graph launch, which joins its recalls, has completed)
     if (h->capturing && h->one_graph) {
@@ -254,46 +281,21 @@ freekv_status do_select(freekv_handle* h, int layer, const void* q, int32_t* pag
         FKV_CUDA(cudaStreamWaitEvent(s, h->ev_recall[layer], cudaEventWaitExternal));
     else if (h->recall_pending[layer])
         FKV_CUDA(cudaStreamWaitEvent(s, h->ev_recall[layer], 0));
-    if (h->c2_select) {  // score + select in one launch (2-CTA clusters)
-        FKV_CUDA(timed(h, K_FINALIZE, s, [&] {
-            return launch_select_c2(h->D, h->layers[layer], h->X, (const uint16_t*)q, (const uint16_t*)k_new,
-                                    (const uint16_t*)v_new, pages_out, corr_out, h->c2_lpt, h->c2_nt, 2, h->pdl, 0, s);
+    const int mno = h->capturing ? max_n_off(h->D, h->D.max_ctx) : max_n_off(h->D, h->ctx_host[layer]);
+    FkvLayer& L = h->layers[layer];
+    if (h->capturing || mno - h->D.n_sink > h->D.K)
+        FKV_CUDA(timed(h, K_SCORE, s, [&] {
+            return launch_score(h->D, L, h->X, (const uint16_t*)q, mno, -1, h->pdl, 0, s);
         }));
-    } else if (h->fused_select) {
-        FKV_CUDA(timed(h, K_FINALIZE, s, [&] {
-            return launch_select_fused(h->D, h->layers[layer], h->X, (const uint16_t*)q, (const uint16_t*)k_new,
-                                       (const uint16_t*)v_new, pages_out, corr_out, h->sel_cluster, h->sel_lptm, s);
-        }));
-    } else {
-        const int mno =
-            h->capturing ? max_n_off(h->D, h->D.max_ctx) : max_n_off(h->D, h->ctx_host[layer] + pending);
-        // with a score launch, its last-scoring CTA of each unit also appends the token and runs
-        // the correction check, so the select kernel starts on the scores
-        const bool score = h->capturing || mno - h->D.n_sink > h->D.K;
-        const int pre_in_score = (score && k_new) ? 1 : 0;
-        if (score)
-            FKV_CUDA(timed(h, K_SCORE, s, [&] {
-                return launch_score(h->D, h->layers[layer], h->X, (const uint16_t*)q, mno, pending, 0, h->pdl, s,
-                                    pre_in_score ? (const uint16_t*)k_new : nullptr,
-                                    pre_in_score ? (const uint16_t*)v_new : nullptr);
-            }));
-        FKV_CUDA(timed(h, K_FINALIZE, s, [&] {
-            return launch_finalize(h->D, h->layers[layer], h->X, (const uint16_t*)q,
-                                   pre_in_score ? nullptr : (const uint16_t*)k_new,
-                                   pre_in_score ? nullptr : (const uint16_t*)v_new, pages_out, corr_out,
-                                   h->fin_nt == 512 ? h->lpt : h->lpt1k, h->fin_nt, h->pdl, 0, s, pre_in_score);
-        }));
-    }
-    if (k_new && !h->capturing) h->ctx_host[layer] += 1;
+    FKV_CUDA(timed(h, K_FINALIZE, s, [&] {
+        return launch_select(h->D, L, h->X, (const uint16_t*)q, pages_out, corr_out, flag_src, list_all, -1,
+                             h->sel_nc, h->sel_lpt, h->pdl, 0, s);
+    }));
     return FREEKV_OK;
 }
 
 freekv_status do_recall(freekv_handle* h, int layer, cudaStream_t s) {
     FKV_CUDA(timed(h, K_RECALL_SYNC, s, [&] { return launch_recall(h->D, h->layers[layer], 1, s); }));
-    if (h->capturing) {  // the background half is captured separately into the recall graph
-        FKV_CUDA(cudaEventRecordWithFlags(h->ev_select[layer], s, cudaEventRecordExternal));
-        return FREEKV_OK;
-    }
     if (h->serial_recall) {
         FKV_CUDA(timed(h, K_RECALL_BG, s, [&] { return launch_recall(h->D, h->layers[layer], 0, s); }));
         return FREEKV_OK;
@@ -306,12 +308,13 @@ freekv_status do_recall(freekv_handle* h, int layer, cudaStream_t s) {
     return FREEKV_OK;
 }
 
+// primitive attention: every unit's page list comes from select_pages (mode 0)
 freekv_status do_attn(freekv_handle* h, int layer, const void* q, float* out, cudaStream_t s) {
     if (!q || !out) return fail(FREEKV_EINVAL, "q/out is NULL");
-    if (h->attn_cluster) {
+    if (h->D.direct) {
         FKV_CUDA(timed(h, K_ATTN_SPLIT, s, [&] {
-            return launch_attn_cluster(h->D, h->layers[layer], h->X, (const uint16_t*)q, out, 0, h->tmap_kv,
-                                       h->tmap_host, 0, h->attn_cluster, false, s);
+            return launch_attn_cluster(h->D, h->layers[layer], h->X, (const uint16_t*)q, out, h->tmap_kv, h->tmap_host,
+                                       0, h->attn_cluster, false, 0, s);
         }));
         return FREEKV_OK;
     }
@@ -327,56 +330,39 @@ freekv_status do_attn(freekv_handle* h, int layer, const void* q, float* out, cu
 
 // Composite step tail (decode_step and the step graph).
 //
-// Direct mode (default): the corrected units' fetched pages are read by the attention
-// kernel straight from the host pool and written back into their slots, so the
-// synchronous recall and the second attention phase disappear from the critical
-// path; the background recall (unflagged units, for step i+1) runs on rs.
+// Direct mode (default): one attention launch.  Corrected units' fetched pages are read by the
+// attention kernel straight from the host pool and written back into their slots, so the
+// synchronous recall and a second attention phase leave the critical path; with `mode` 1 the
+// units that are not corrected attend their resident set while the select still runs.  The
+// background recall (unflagged units, for step i+1) runs on rs, forked after the attention.
 //
-// Recall mode (FREEKV_CORR=recall): the corrected units' synchronous recall runs on
-// the high-priority stream ss while the attention of every other unit (whose pages
-// are resident) runs on the compute stream; the corrected units are attended once
-// their pages have landed.  The background recall follows the synchronous one.
+// Recall mode (FREEKV_CORR=recall, the paper's order): the corrected units' synchronous recall
+// runs on the high-priority stream ss while the attention of every other unit (whose pages are
+// resident) runs on the compute stream; the corrected units are attended once their pages have
+// landed.  The background recall follows the synchronous one.
 freekv_status do_step_tail(freekv_handle* h, int layer, const void* q, float* out) {
     cudaStream_t cs = h->cs;
     const FkvDims& D = h->D;
     FkvLayer& L = h->layers[layer];
     if (D.direct) {
-        if (h->attn_cluster) {  // attention + merge + commit in one launch (clusters per unit)
-            FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] {
-                return launch_attn_cluster(D, L, h->X, (const uint16_t*)q, out, 0, h->tmap_kv, h->tmap_host, 0,
-                                           h->attn_cluster, h->pdl, cs);
-            }));
-        } else {
-            FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] {
-                return launch_attn_split(D, L, h->X, (const uint16_t*)q, 0, h->tmap_kv, h->tmap_host, h->arena,
-                                         h->pdl, cs);
-            }));
-            FKV_CUDA(timed(h, K_ATTN_COMBINE, cs, [&] {
-                return launch_attn_combine(D, L, h->X, (const uint16_t*)q, out, 0, 0, h->pdl, cs);
-            }));
-        }
-        // the background recall of this layer starts after its attention (an event node between
-        // select and attention would break their PDL edge, and the host link is then free for
-        // the attention's own host reads); it overlaps the next layers
-        if (h->serial_recall) {  // diagnostics: no overlap at all
+        FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] {
+            return launch_attn_cluster(D, L, h->X, (const uint16_t*)q, out, h->tmap_kv, h->tmap_host, 0,
+                                       h->attn_cluster, h->pdl, h->prio_hi, cs);
+        }));
+        // the background recall of this layer starts after its attention (which completes only after
+        // the select); it overlaps the next layers
+        if (h->serial_recall) {  // f2 ablation: no overlap at all
             FKV_CUDA(timed(h, K_RECALL_BG, cs, [&] { return launch_recall(D, L, 0, cs, h->X.trace); }));
-            FKV_CUDA(cudaEventRecord(h->ev_recall[layer], cs));
+            if (!h->capturing) {
+                FKV_CUDA(cudaEventRecord(h->ev_recall[layer], cs));
+                h->recall_pending[layer] = 1;
+            }
+        } else {  // forked branch (graph capture: joined at the graph's end)
+            FKV_CUDA(cudaEventRecord(h->ev_select[layer], cs));
+            FKV_CUDA(cudaStreamWaitEvent(h->rs, h->ev_select[layer], 0));
+            FKV_CUDA(timed(h, K_RECALL_BG, h->rs, [&] { return launch_recall(D, L, 0, h->rs, h->X.trace); }));
+            FKV_CUDA(cudaEventRecord(h->ev_recall[layer], h->rs));
             if (!h->capturing) h->recall_pending[layer] = 1;
-        } else if (h->capturing && h->one_graph) {  // forked branch of the step graph, joined at its end
-            FKV_CUDA(cudaEventRecord(h->ev_select[layer], cs));
-            FKV_CUDA(cudaStreamWaitEvent(h->rs, h->ev_select[layer], 0));
-            FKV_CUDA(timed(h, K_RECALL_BG, h->rs, [&] { return launch_recall(D, L, 0, h->rs, h->X.trace); }));
-            FKV_CUDA(cudaEventRecord(h->ev_recall[layer], h->rs));
-        } else if (h->capturing) {
-            FKV_CUDA(cudaEventRecordWithFlags(h->ev_select[layer], cs, cudaEventRecordExternal));
-        } else if (h->serial_recall) {
-            FKV_CUDA(timed(h, K_RECALL_BG, cs, [&] { return launch_recall(D, L, 0, cs, h->X.trace); }));
-        } else {
-            FKV_CUDA(cudaEventRecord(h->ev_select[layer], cs));
-            FKV_CUDA(cudaStreamWaitEvent(h->rs, h->ev_select[layer], 0));
-            FKV_CUDA(timed(h, K_RECALL_BG, h->rs, [&] { return launch_recall(D, L, 0, h->rs, h->X.trace); }));
-            FKV_CUDA(cudaEventRecord(h->ev_recall[layer], h->rs));
-            h->recall_pending[layer] = 1;
         }
         return FREEKV_OK;
     }
@@ -410,58 +396,90 @@ freekv_status do_step_tail(freekv_handle* h, int layer, const void* q, float* ou
     return FREEKV_OK;
 }
 
-// Overlapped decode step of one layer (FREEKV_PIPELINE=1), PAPER.md
-// the units whose correction check passes attend their
-// resident set R (selected at step i-1) while the selection of step i runs:
-//   cs: prep (append, correction flags, page lists over R) -> attention of the
-//       speculative units on the SMs the select leaves free (one 8-warp CTA per SM)
-//       -> [join] -> attention of the corrected units (their missing pages read from
-//       the host pool) -> combine + commit
-//   ss: fused score + select of every unit, one CTA per unit (flags from the prep; page
-//       lists of the corrected units only) -> [fork] rs: background recall of S_i \ R
-// The select CTA (~200 KB of shared memory) and the 8-warp attention CTA (192 KB)
-// cannot share an SM, so the two kernels partition the GPU whichever starts first.
-freekv_status do_step_pipelined(freekv_handle* h, int layer, const void* q, const void* k_new, const void* v_new,
-                                float* out) {
-    cudaStream_t cs = h->cs, ss = h->ss;
+// One layer of the decode step (decode_step and the step graph).  Every mode starts with the pre
+// kernel (deferred commit, append, correction flags, new context length) on the compute stream.
+//
+// Speculative step (default, direct mode), PAPER.md P:221-225 and P:254-258:
+//   compute stream: pre -> attention (mode 1: units that are not corrected attend R = S_{i-1} at
+//                   once; corrected units wait for their S_i)
+//   side stream:    [fork after pre] score -> select (units in priority order, corrected first;
+//                   each waits for its own score items) -> background recall of S_i minus R
+// The side chain of layer l overlaps the attention of layer l and the following layers; it is
+// joined before the same layer's next step (graph end / ev_recall).  With W = 0 the pre kernel's
+// append makes the completed page a candidate before the scoring, as the order requires.
+//
+// Serial step (FREEKV_OVERLAP=0, and the paper-order recall mode FREEKV_CORR=recall): pre ->
+// score -> select (every unit's page list) -> attention / recall tail on the compute stream.
+freekv_status do_layer_step(freekv_handle* h, int layer, const void* q, const void* k_new, const void* v_new,
+                            float* out) {
+    cudaStream_t cs = h->cs;
     const FkvDims& D = h->D;
     FkvLayer& L = h->layers[layer];
     if (!q || !out) return fail(FREEKV_EINVAL, "q/out is NULL");
-    // the previous step's recall of this layer (its slots); one-graph capture: the previous
-    // graph launch joined it
+    // the previous step's side chain / recall of this layer (its selection, its slots)
     if (!h->capturing && h->recall_pending[layer]) FKV_CUDA(cudaStreamWaitEvent(cs, h->ev_recall[layer], 0));
-    FKV_CUDA(timed(h, K_PREP, cs, [&] {
-        return launch_prep(D, L, h->X, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new, nullptr,
-                           h->pdl, cs);
+    if (h->fused) {  // the whole layer step in one launch, then the background recall (rs)
+        FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] {
+            return launch_layer(D, L, h->X, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new, out,
+                                h->tmap_kv, h->tmap_host, h->ly_c, h->ly_lpt, h->pdl, cs);
+        }));
+        if (!h->capturing) h->ctx_host[layer] += 1;
+        if (h->serial_recall) {  // f2 ablation: no overlap
+            FKV_CUDA(timed(h, K_RECALL_BG, cs, [&] { return launch_recall(D, L, 0, cs, h->X.trace); }));
+            FKV_CUDA(cudaEventRecord(h->ev_recall[layer], cs));
+        } else {
+            FKV_CUDA(cudaEventRecord(h->ev_select[layer], cs));
+            FKV_CUDA(cudaStreamWaitEvent(h->rs, h->ev_select[layer], 0));
+            FKV_CUDA(timed(h, K_RECALL_BG, h->rs, [&] { return launch_recall(D, L, 0, h->rs, h->X.trace); }));
+            FKV_CUDA(cudaEventRecord(h->ev_recall[layer], h->rs));
+        }
+        if (!h->capturing) h->recall_pending[layer] = 1;
+        return FREEKV_OK;
+    }
+    FKV_CUDA(timed(h, K_PRE, cs, [&] {
+        return launch_pre(D, L, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new, h->spec ? 1 : 0,
+                          h->pdl, h->prio_hi, cs);
     }));
     if (!h->capturing) h->ctx_host[layer] += 1;
+    if (!h->spec) {
+        freekv_status st = do_select(h, layer, q, nullptr, nullptr, cs, 1, 1);
+        if (st != FREEKV_OK) return st;
+        return do_step_tail(h, layer, q, out);
+    }
+    const int mno = h->capturing ? max_n_off(D, D.max_ctx) : max_n_off(D, h->ctx_host[layer]);
+    // the corrected units' scoring and selection (latency variants) on the high-priority stream,
+    // beside the attention, which waits for them per unit
     FKV_CUDA(cudaEventRecord(h->ev_pre[layer], cs));
-    FKV_CUDA(cudaStreamWaitEvent(ss, h->ev_pre[layer], 0));
-    FKV_CUDA(timed(h, K_FINALIZE, ss, [&] {
-        return launch_select_c2(D, L, h->X, (const uint16_t*)q, nullptr, nullptr, nullptr, nullptr, h->lpt, 512, 1,
-                                false, 3, ss);
+    FKV_CUDA(cudaStreamWaitEvent(h->ss, h->ev_pre[layer], 0));
+    FKV_CUDA(timed(h, K_SCORE, h->ss, [&] { return launch_score(D, L, h->X, L.q_cur, mno, 0, false, h->prio_hi, h->ss); }));
+    FKV_CUDA(timed(h, K_FINALIZE, h->ss, [&] {
+        return launch_select(D, L, h->X, L.q_cur, nullptr, nullptr, 1, 0, 0, h->fsel_nc, h->fsel_lpt, h->pdl,
+                             h->prio_hi, h->ss);
     }));
-    FKV_CUDA(cudaEventRecord(h->ev_fl[layer], ss));
-    if (h->serial_recall) {
-        FKV_CUDA(timed(h, K_RECALL_BG, ss, [&] { return launch_recall(D, L, 0, ss, h->X.trace); }));
-        FKV_CUDA(cudaEventRecord(h->ev_recall[layer], ss));
+    // critical path: the attention of every unit (the others attend R at once)
+    FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] {
+        return launch_attn_cluster(D, L, h->X, (const uint16_t*)q, out, h->tmap_kv, h->tmap_host, 1, h->attn_cluster,
+                                   h->pdl, h->prio_hi, cs);
+    }));
+    // side chain of the units that are not corrected (their S_i is used at step i+1), after this
+    // layer's attention: it overlaps the next layers
+    cudaStream_t ss2 = h->side[layer % h->side.size()];
+    FKV_CUDA(cudaEventRecord(h->ev_select[layer], cs));
+    FKV_CUDA(cudaStreamWaitEvent(ss2, h->ev_select[layer], 0));
+    FKV_CUDA(timed(h, K_SCORE, ss2, [&] { return launch_score(D, L, h->X, L.q_cur, mno, 1, false, 0, ss2); }));
+    FKV_CUDA(timed(h, K_FINALIZE, ss2, [&] {
+        return launch_select(D, L, h->X, L.q_cur, nullptr, nullptr, 1, 0, 1, h->bsel_nc, h->bsel_lpt, h->pdl, 0, ss2);
+    }));
+    if (h->serial_recall) {  // f2 ablation: the background recall on the compute stream (no overlap)
+        FKV_CUDA(cudaEventRecord(h->ev_sync[layer], ss2));
+        FKV_CUDA(cudaStreamWaitEvent(cs, h->ev_sync[layer], 0));
+        FKV_CUDA(timed(h, K_RECALL_BG, cs, [&] { return launch_recall(D, L, 0, cs, h->X.trace); }));
+        FKV_CUDA(cudaEventRecord(h->ev_recall[layer], cs));
     } else {
-        FKV_CUDA(cudaStreamWaitEvent(h->rs, h->ev_fl[layer], 0));
-        FKV_CUDA(timed(h, K_RECALL_BG, h->rs, [&] { return launch_recall(D, L, 0, h->rs, h->X.trace); }));
-        FKV_CUDA(cudaEventRecord(h->ev_recall[layer], h->rs));
+        FKV_CUDA(timed(h, K_RECALL_BG, ss2, [&] { return launch_recall(D, L, 0, ss2, h->X.trace); }));
+        FKV_CUDA(cudaEventRecord(h->ev_recall[layer], ss2));
     }
     if (!h->capturing) h->recall_pending[layer] = 1;
-    FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] {
-        return launch_attn_split(D, L, h->X, (const uint16_t*)q, 1, h->tmap_kv, h->tmap_host, h->arena, h->pdl, cs,
-                                 8);
-    }));
-    FKV_CUDA(cudaStreamWaitEvent(cs, h->ev_fl[layer], 0));
-    FKV_CUDA(timed(h, K_ATTN_P2, cs, [&] {
-        return launch_attn_split(D, L, h->X, (const uint16_t*)q, 2, h->tmap_kv, h->tmap_host, h->arena, false, cs);
-    }));
-    FKV_CUDA(timed(h, K_ATTN_COMBINE, cs, [&] {
-        return launch_attn_combine(D, L, h->X, (const uint16_t*)q, out, 1, 0, h->pdl, cs);
-    }));
     return FREEKV_OK;
 }
 
@@ -469,6 +487,7 @@ freekv_status sync_both(freekv_handle* h) {
     FKV_CUDA(cudaStreamSynchronize(h->cs));
     FKV_CUDA(cudaStreamSynchronize(h->ss));
     FKV_CUDA(cudaStreamSynchronize(h->rs));
+    for (cudaStream_t s : h->side) FKV_CUDA(cudaStreamSynchronize(s));
     return FREEKV_OK;
 }
 
@@ -509,6 +528,7 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         return fail(FREEKV_EINVAL, std::string("host pool is not pinned/device-mapped: ") + cudaGetErrorString(e));
 
     freekv_handle* h = new freekv_handle();
+    cudaGetDevice(&h->device);
     h->cfg = *cfg;
     h->D = D;
     h->cs = (cudaStream_t)compute_stream;
@@ -580,58 +600,85 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         L.n_fetch = (int32_t*)(base + s.o_n_fetch);
         L.ctx = (int32_t*)(base + s.o_ctx);
         L.n_off = (int32_t*)(base + s.o_n_off);
+        L.q_cur = (uint16_t*)(base + s.o_qcur);
+        L.scores = (float*)(base + s.o_scores);
+        L.pend_valid = (int32_t*)(base + s.o_pend_valid);
+        L.order = (int32_t*)(base + s.o_order);
+        L.ord_cnt = (int32_t*)(base + s.o_ord_cnt);
+        L.score_done = (int32_t*)(base + s.o_score_done);
         L.host = (uint16_t*)(hd + s.host_layer_bytes * l);
         L.host_row0 = (int)(s.host_layer_bytes * l / (kHeadDim * 2));
         L.arena = (const uint16_t*)dev;
     }
     uint8_t* sb = dev + s.layer_bytes * cfg->n_layers;
-    h->X.scores = (float*)(sb + s.o_scores);
     h->X.part_o = (float*)(sb + s.o_part_o);
     h->X.part_ml = (float*)(sb + s.o_part_ml);
     h->X.page_rows = (int32_t*)(sb + s.o_page_rows);
     h->X.page_cnt = (int32_t*)(sb + s.o_page_cnt);
     h->X.page_valid = (uint8_t*)(sb + s.o_page_valid);
     h->X.page_dst = (int32_t*)(sb + s.o_page_dst);
-    h->X.cosv = (float*)(sb + s.o_cosv);
+    h->X.ready = (int32_t*)(sb + s.o_ready);
 
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
     {
-        // leaves of the select tree: page ids [0, n_off); n_off never exceeds
-        // max(S/p, max_ctx/p - W/p), so the tree (zero-padded, CFR-6) needs next_pow2 of that
+        // leaves of the select tree: page ids [0, n_off); n_off never exceeds max(S/p, max_ctx/p - W/p),
+        // so the tree (zero-padded, CFR-6) needs next_pow2 of that.  CTAs per unit: the widest cluster
+        // (<= 8) that keeps one CTA per SM and >= 512 leaves per CTA; leaves per thread fill the tree
         const int n_off_max = std::max(D.n_sink, D.max_ctx / D.p - D.n_win);
-        int P2 = 1;
+        int P2 = 256;
         while (P2 < n_off_max) P2 <<= 1;
-        h->lpt = P2 <= 512 ? 1 : P2 / 512;      // 512-thread select (overlapped step)
-        h->lpt1k = P2 <= 1024 ? 1 : P2 / 1024;  // 1024-thread select (every unit at once)
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-        h->sel_cluster = (P2 >= 2048 && D.U * 8 < 2 * sms) ? 16 : 8;  // few units: wider clusters
-        h->sel_lptm = std::max(1, P2 / (h->sel_cluster * 128));
-        const char* fs = getenv("FREEKV_SELECT");
-        h->fused_select = fs && fs[0] == 'f' && h->D.pool == 0 && h->D.corr_pool == 0;
-        if (h->fused_select) h->D.direct = 0;  // the cluster select writes slot rows only
-        {
-            const char* ft = getenv("FREEKV_FIN_THREADS");
-            // 1024 (default): r1_v8 A/B -1.4 us/layer on c2, -5.9 on c3 (profiles/r1_v8_fin_ab.txt)
-            h->fin_nt = (ft && atoi(ft) == 512) ? 512 : 1024;
+        int nc = 8;
+        while (nc > 1 && (D.U * nc > sms || nc * 256 > P2)) nc >>= 1;
+        const char* ne = getenv("FREEKV_SELECT_NC");  // A/B: force the cluster width (1, 2, 4, 8)
+        if (ne && (atoi(ne) == 1 || atoi(ne) == 2 || atoi(ne) == 4 || atoi(ne) == 8)) nc = atoi(ne);
+        int lpt = std::max(1, P2 / (nc * 256));
+        if (nc > 1 && lpt > 4) {  // cluster instances are built for <= 4 leaves per thread
+            nc = 1;
+            lpt = P2 / 256;
         }
-        {
-            const char* ne = getenv("FREEKV_SELECT_THREADS");  // 256, 512 (default) or 1024
-            h->c2_nt = ne ? atoi(ne) : 1024;
-            if (h->c2_nt != 256 && h->c2_nt != 512) h->c2_nt = 1024;
-            h->c2_lpt = P2 <= h->c2_nt ? 1 : P2 / h->c2_nt;
-            if (h->c2_nt == 256 && h->c2_lpt < 2) h->c2_lpt = 2;  // (instantiated: 2..8)
+        if (lpt > 32) {
+            delete h;
+            return fail(FREEKV_EUNSUPPORTED, "max_ctx_tokens / page_size > 8192 pages");
         }
-        // the fused 2-CTA select is opt-in (FREEKV_SELECT=c2): its scoring is ALU-bound on two SMs per
-        // unit, while the score kernel spreads it over all SMs -- measured faster end to end
-        h->c2_select = fs && fs[0] == 'c' && h->D.pool == 0 && select_c2_fits(h->D, h->c2_lpt, h->c2_nt);
-        const char* pp = getenv("FREEKV_PIPELINE");
-        h->pipelined = h->D.direct && pp && pp[0] == '1';
+        h->sel_nc = nc;
+        h->sel_lpt = lpt;
+        // speculative step: the corrected units' select (few units, critical path) as wide as the tree
+        // allows (<= 8 CTAs, >= 256 leaves each); the side chain's select one CTA per unit (clusters
+        // would constrain the placement of the attention's clusters it runs beside)
+        int fnc = 8;
+        while (fnc > 1 && fnc * 256 > P2) fnc >>= 1;
+        h->fsel_nc = fnc;
+        h->fsel_lpt = std::max(1, P2 / (fnc * 256));
+        if (h->fsel_lpt > 4) {
+            h->fsel_nc = 1;
+            h->fsel_lpt = P2 / 256;
+        }
+        h->bsel_nc = 1;
+        h->bsel_lpt = P2 / 256;
+        const char* fe = getenv("FREEKV_FSELECT_NC");  // A/B of the critical select's width
+        if (fe && (atoi(fe) == 1 || atoi(fe) == 2 || atoi(fe) == 4 || atoi(fe) == 8)) {
+            h->fsel_nc = atoi(fe);
+            h->fsel_lpt = std::max(1, P2 / (h->fsel_nc * 256));
+        }
         h->one_graph = h->D.direct;  // recalls are forked branches of the one step graph
         const char* pd = getenv("FREEKV_PDL");
         h->pdl = !(pd && pd[0] == '0');
-        if (h->lpt > 16) {
-            delete h;
-            return fail(FREEKV_EUNSUPPORTED, "max_ctx_tokens / page_size > 8192 pages");
+        // step mode (FREEKV_STEP): fused (default: one kernel per layer, layer.cu), spec (pre kernel,
+        // attention beside the scoring/selection streams), serial (pre, score, select, attention)
+        const char* ov = getenv("FREEKV_STEP");
+        const std::string mode = ov ? ov : "fused";
+        h->spec = h->D.direct && mode == "spec";
+        if (h->D.direct && mode == "fused") {
+            int c = 8;
+            while (c > 2 && D.U * c > 2 * sms) c >>= 1;
+            int lpt = 1;
+            while (c * 128 * lpt < P2) lpt <<= 1;
+            if (layer_supported(h->D, c, lpt)) {
+                h->fused = true;
+                h->ly_c = c;
+                h->ly_lpt = lpt;
+            }
         }
     }
     {
@@ -641,38 +688,18 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
             freekv_destroy(h);
             return fail(FREEKV_ECUDA, std::string("occupancy query: ") + cudaGetErrorString(oe));
         }
-        // T <= V (every warp owns >= 1 page), T * V < 2^31 (32-bit range math), and at most
-        // ~254 records per unit (combine kernel capacity)
+        // split kernel (recall mode): T <= V (every warp owns >= 1 page), T * V < 2^31 (32-bit range
+        // math), and at most ~254 records per unit (combine kernel capacity)
         const long long V = (long long)D.U * D.P_max;
-        const char* mp = getenv("FREEKV_ATTN_MIN_PAGES");  // pages per warp (>= 1): fewer, longer warps
-        const long long minp = std::max(1, mp ? atoi(mp) : 1);
-        long long T = std::min<long long>({(long long)warps, (long long)kMaxAttnWarps, V / minp, 254LL * D.U});
+        long long T = std::min<long long>({(long long)warps, (long long)kMaxAttnWarps, V, 254LL * D.U});
         while (T > 1 && T * V >= (1LL << 31)) T /= 2;
         h->D.attn_warps = (int)std::max(1LL, T);
         h->D.attn_warps_p1 = h->D.attn_warps;
-        {
-            // clustered attention (direct mode): C CTAs per unit, the largest power of two <= 8
-            // with U * C within one wave of 2 CTAs per SM (FREEKV_ATTN=split: two kernels)
-            int sms = 148;
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-            const char* ae = getenv("FREEKV_ATTN");
-            int c = 8;
-            while (c > 1 && D.U * c > 2 * sms) c >>= 1;
-            h->attn_cluster = (h->D.direct && !(ae && ae[0] == 's')) ? c : 0;
-        }
-        if (h->pipelined) {
-            // phase 1 runs on the SMs the one-CTA-per-unit select leaves free
-            int sms = 148;
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-            const int free_sms = sms - D.U;
-            if (free_sms < 16 || !select_c2_fits(h->D, h->lpt, 512)) {
-                h->pipelined = false;  // not enough room beside the select: sequential step
-            } else {
-                const long long T1 = std::min<long long>({(long long)free_sms * 8, (long long)kMaxAttnWarps, V,
-                                                          254LL * D.U});
-                h->D.attn_warps_p1 = (int)std::max(1LL, T1);
-            }
-        }
+        // clustered attention (direct mode): C CTAs per unit, the largest power of two <= 8 with
+        // U * C within one wave of 2 CTAs per SM
+        int c = 8;
+        while (c > 1 && D.U * c > 2 * sms) c >>= 1;
+        h->attn_cluster = c;
     }
     h->X.trace = nullptr;
     {
@@ -684,14 +711,13 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
                 return fail(FREEKV_ECUDA, "trace buffer");
             }
         }
+        for (auto& L : h->layers) L.trace = h->X.trace;
     }
     {
         const char* fr = getenv("FREEKV_DEBUG_FULL_REFRESH");
         h->D.full_refresh = (fr && fr[0] == '1') ? 1 : 0;
-        const char* dx = getenv("FREEKV_DEBUG_EXP");
-        h->D.dbg = dx ? atoi(dx) : 0;
-        const char* sp = getenv("FREEKV_ATTN_SPEC");
-        h->D.attn_spec = (sp && sp[0] == '1') ? 1 : 0;
+        const char* lo2 = getenv("FREEKV_LAYER_ORDER");
+        h->D.dbg_order = lo2 ? atoi(lo2) : 0;
     }
     {
         const char* sr = getenv("FREEKV_SERIAL_RECALL");
@@ -704,22 +730,33 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
     h->ev_sync.resize(cfg->n_layers);
     h->ev_sync_x.resize(cfg->n_layers);
     h->ev_pre.resize(cfg->n_layers);
-    h->ev_fl.resize(cfg->n_layers);
     {
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        h->prio_hi = hi;  // the critical path's kernels outrank the side chains' (graph node priority)
         if (cudaStreamCreateWithPriority(&h->ss, cudaStreamNonBlocking, hi) != cudaSuccess) {
             freekv_destroy(h);
             return fail(FREEKV_ECUDA, "cudaStreamCreateWithPriority failed");
         }
+        // side streams of the speculative step (lowest priority), one per layer in rotation so the
+        // side chains of consecutive layers may run concurrently
+        const char* ns = getenv("FREEKV_SIDE_STREAMS");
+        const int n_side = std::max(1, std::min(8, ns ? atoi(ns) : 4));
+        for (int i = 0; i < n_side; ++i) {
+            cudaStream_t st2;
+            if (cudaStreamCreateWithPriority(&st2, cudaStreamNonBlocking, lo) != cudaSuccess) {
+                freekv_destroy(h);
+                return fail(FREEKV_ECUDA, "cudaStreamCreateWithPriority failed");
+            }
+            h->side.push_back(st2);
+        }
     }
     for (int l = 0; l < cfg->n_layers; ++l) {
-        if (cudaEventCreateWithFlags(&h->ev_select[l], cudaEventDisableTiming) != cudaSuccess ||
+        if (cudaEventCreateWithFlags(&h->ev_pre[l], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->ev_select[l], cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&h->ev_recall[l], cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&h->ev_sync[l], cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&h->ev_sync_x[l], cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&h->ev_pre[l], cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&h->ev_fl[l], cudaEventDisableTiming) != cudaSuccess) {
+            cudaEventCreateWithFlags(&h->ev_sync_x[l], cudaEventDisableTiming) != cudaSuccess) {
             freekv_destroy(h);
             return fail(FREEKV_ECUDA, "cudaEventCreate failed");
         }
@@ -759,7 +796,7 @@ freekv_status freekv_select_pages(freekv_handle* h, int32_t layer, const void* q
                                   uint8_t* corrected_out, void* stream) {
     freekv_status st = check_layer(h, layer);
     if (st != FREEKV_OK) return st;
-    return do_select(h, layer, q, pages_out, corrected_out, pick(h, stream));
+    return do_select(h, layer, q, pages_out, corrected_out, pick(h, stream), 0, 1);
 }
 
 freekv_status freekv_recall_pages(freekv_handle* h, int32_t layer, const uint8_t* sync_mask, void* stream) {
@@ -779,17 +816,9 @@ freekv_status freekv_decode_step(freekv_handle* h, int32_t layer, const void* q,
                                  const void* v_new, float* out) {
     freekv_status st = check_layer(h, layer);
     if (st != FREEKV_OK) return st;
-    cudaStream_t s = h->cs;
     if (!k_new || !v_new) return fail(FREEKV_EINVAL, "k_new/v_new is NULL");
     if (h->ctx_host[layer] + 1 > h->D.max_ctx) return fail(FREEKV_ERANGE, "context would exceed max_ctx_tokens");
-    if (h->pipelined) return do_step_pipelined(h, layer, q, k_new, v_new, out);
-    if (h->D.n_win >= 1) {
-        if ((st = do_select(h, layer, q, nullptr, nullptr, s, k_new, v_new)) != FREEKV_OK) return st;
-    } else {  // W = 0: the page completed by this token is a candidate now -> append first
-        if ((st = do_append(h, layer, k_new, v_new, 1, s)) != FREEKV_OK) return st;
-        if ((st = do_select(h, layer, q, nullptr, nullptr, s)) != FREEKV_OK) return st;
-    }
-    return do_step_tail(h, layer, q, out);
+    return do_layer_step(h, layer, q, k_new, v_new, out);
 }
 
 
@@ -844,8 +873,7 @@ freekv_status freekv_get_summaries(freekv_handle* h, int32_t layer, int32_t unit
     for (int j = page_begin; j < page_end; ++j)
         for (int which = 0; which < 2; ++which)
             for (int c = 0; c < D.d; ++c) {
-                const size_t blk = (size_t)(j >> 5) * (D.d / 8) + (c >> 3);
-                const size_t off = ((blk * 2 + which) * 32 + (j & 31)) * 8 + (c & 7);
+                const size_t off = (((size_t)(c >> 3) * 2 + which) * D.n_page_max + j) * 8 + (c & 7);
                 out[((size_t)(j - page_begin) * 2 + which) * D.d + c] = buf[off];
             }
     return FREEKV_OK;
@@ -950,21 +978,16 @@ freekv_status freekv_step_graph_capture(freekv_handle* h, const void* q_all, con
         const uint8_t* q = (const uint8_t*)q_all + q_stride * l;
         const uint8_t* k = (const uint8_t*)k_all + kv_stride * l;
         const uint8_t* v = (const uint8_t*)v_all + kv_stride * l;
-        if (h->pipelined) {
-            st = do_step_pipelined(h, l, q, k, v, out_all + o_stride * l);
-            continue;
-        }
-        if (D.n_win >= 1) {
-            st = do_select(h, l, q, nullptr, nullptr, h->cs, k, v);
-        } else {
-            e = launch_append(D, h->layers[l], (const uint16_t*)k, (const uint16_t*)v, 1, h->cs);
-            if (e == cudaSuccess) st = do_select(h, l, q, nullptr, nullptr, h->cs);
-        }
-        if (st == FREEKV_OK) st = do_step_tail(h, l, q, out_all + o_stride * l);
+        st = do_layer_step(h, l, q, k, v, out_all + o_stride * l);
     }
-    if (h->one_graph)  // join every layer's recall branch
+    if (h->one_graph) {  // join every layer's recall branch (and the corrected units' chain)
         for (int l = 0; l < h->cfg.n_layers && e == cudaSuccess && st == FREEKV_OK; ++l)
             e = cudaStreamWaitEvent(h->cs, h->ev_recall[l], 0);
+        if (h->spec && e == cudaSuccess && st == FREEKV_OK) {
+            e = cudaEventRecord(h->ev_sync_x[0], h->ss);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(h->cs, h->ev_sync_x[0], 0);
+        }
+    }
     cudaError_t e2 = cudaStreamEndCapture(h->cs, &gc);
     if (e == cudaSuccess) e = e2;
     if (e == cudaSuccess && st == FREEKV_OK && !h->one_graph) {
@@ -986,7 +1009,9 @@ freekv_status freekv_step_graph_capture(freekv_handle* h, const void* q_all, con
         h->graph_recs = h->prof_recs;
         h->prof_recs.clear();
     }
-    if (e == cudaSuccess && st == FREEKV_OK) e = cudaGraphInstantiate(&h->g_compute, gc, 0);
+    // per-node priorities: the critical path's kernels (pre, attention) outrank the side chains'
+    if (e == cudaSuccess && st == FREEKV_OK)
+        e = cudaGraphInstantiate(&h->g_compute, gc, cudaGraphInstantiateFlagUseNodePriority);
     if (e == cudaSuccess && st == FREEKV_OK && gr) e = cudaGraphInstantiate(&h->g_recall, gr, 0);
     if (gc) cudaGraphDestroy(gc);
     if (gr) cudaGraphDestroy(gr);
@@ -1054,9 +1079,11 @@ void freekv_destroy(freekv_handle* h) {
         if (e) cudaEventDestroy(e);
     for (auto e : h->ev_pre)
         if (e) cudaEventDestroy(e);
-    for (auto e : h->ev_fl)
-        if (e) cudaEventDestroy(e);
     for (auto e : h->prof_pool) cudaEventDestroy(e);
+    for (cudaStream_t s2 : h->side) {
+        cudaStreamSynchronize(s2);
+        cudaStreamDestroy(s2);
+    }
     if (h->ss) cudaStreamDestroy(h->ss);
     if (h->X.trace) cudaFree(h->X.trace);
     delete h;

@@ -34,12 +34,8 @@ __global__ void __launch_bounds__(128) fkv_summarize_kernel(FkvDims D, FkvLayer 
 cudaError_t launch_append(const FkvDims& D, const FkvLayer& L, const uint16_t* k, const uint16_t* v,
                           int n_new, cudaStream_t s) {
     const size_t smem = page_elems(D) * sizeof(uint16_t);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(fkv_append_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             cudaSharedmemCarveoutMaxShared);
-        configured = true;
-    }
+    cudaError_t e = func_smem((const void*)fkv_append_kernel, smem);
+    if (e != cudaSuccess) return e;
     fkv_append_kernel<<<D.U, 256, smem, s>>>(D, L, k, v, n_new);
     return cudaGetLastError();
 }
@@ -47,6 +43,8 @@ cudaError_t launch_append(const FkvDims& D, const FkvLayer& L, const uint16_t* k
 cudaError_t launch_summarize(const FkvDims& D, const FkvLayer& L, int page_begin, int page_end, cudaStream_t s) {
     if (page_end <= page_begin) return cudaSuccess;
     const size_t smem = (size_t)D.p * D.d * sizeof(uint16_t);
+    cudaError_t e = func_smem((const void*)fkv_summarize_kernel, smem);
+    if (e != cudaSuccess) return e;
     fkv_summarize_kernel<<<dim3(D.U, page_end - page_begin), 128, smem, s>>>(D, L, page_begin);
     return cudaGetLastError();
 }

@@ -32,8 +32,8 @@ __device__ __forceinline__ void summarize_smem_page(const FkvDims& D, const FkvL
             lo = kk < lo ? kk : lo;
             hi = kk > hi ? kk : hi;
         }
-        L.summ[summ_chunk_offset(D, u, j, c >> 3, 0) + (c & 7)] = from_key(lo);
-        L.summ[summ_chunk_offset(D, u, j, c >> 3, 1) + (c & 7)] = from_key(hi);
+        L.summ[summ_off(D, u, c >> 3, 0, j) + (c & 7)] = from_key(lo);
+        L.summ[summ_off(D, u, c >> 3, 1, j) + (c & 7)] = from_key(hi);
     }
 }
 

@@ -12,6 +12,11 @@ namespace fkv {
 
 constexpr int kHeadDim = 128;   // d (P:557 models: 128)
 constexpr int kMaxG = 8;        // GQA group size supported (Llama 4, Qwen 7, 70B 8)
+// pages scored by one score CTA (score.cu): the throughput variant (4 pages per thread) of the
+// serial step and the side chain, and the latency variant (1 page per thread, 4x more CTAs) that
+// scores the corrected units on the critical path
+constexpr int kScoreCtaPages = 512;
+constexpr int kScoreCtaPagesFast = 128;
 
 struct FkvDims {
     int nb, n_qo, n_kv, G, d, p;
@@ -26,8 +31,7 @@ struct FkvDims {
     int U;            // nb * n_kv
     int mode;
     int full_refresh; // diagnostics (env FREEKV_DEBUG_FULL_REFRESH=1): no slot reuse, all pages re-fetched
-    int dbg;          // timing experiments only (env FREEKV_DEBUG_EXP, bit flags; results not valid)
-    int attn_spec;    // speculative attention over R before the PDL wait (env FREEKV_ATTN_SPEC=1)
+    int dbg_order;    // A/B (env FREEKV_LAYER_ORDER): bit 0 = every uncorrected unit attends first
     int pool;         // FREEKV_POOL_* group pooling of the selection (f3); 0 = MeanS
     int corr_pool;    // 0 = mean of the cosines, 1 = corrected when the least similar head is below tau
     float tau;
@@ -35,15 +39,14 @@ struct FkvDims {
     float attn_c;     // log2(e)/sqrt(d) for attention softmax (not CFR)
     int P_max;        // upper bound of attention pages per unit: n_sink + K + R_loc
     int attn_warps;   // T: warps of the balanced split-KV attention grid (<= resident warps)
-    int attn_warps_p1;  // T of attention phase 1 (units attending R) -- smaller in the overlapped
-                        // step, where it runs beside the select on the SMs the select leaves free
+    int attn_warps_p1;  // T of attention phase 1 (recall mode: units attending R)
     int direct;       // 1: corrected units' fetched pages are read by the attention kernel straight
                       // from the host pool (and written back to their slots); 0: synchronous recall
                       // before a second attention phase
 };
 
 struct FkvLayer {
-    uint16_t* summ;       // [U][n_page_max/32][d/8][2][32][8]
+    uint16_t* summ;       // [U][d/8][2][n_page_max][8]: channel group c8, {min, max}, page, 8 channels
     uint16_t* sink;       // [U][n_sink][2][p][d]
     uint16_t* slots;      // [U][2K][2][p][d]
     uint16_t* ring;       // [U][R_loc][2][p][d]
@@ -64,13 +67,20 @@ struct FkvLayer {
     int32_t* n_fetch;     // [U]
     int32_t* ctx;         // [U]     context length Lc (tokens)
     int32_t* n_off;       // [U]     pages [0, n_off) are offloaded; candidates [n_sink, n_off)
+    uint16_t* q_cur;      // [nb][n_qo][d] this step's q, copied by the pre kernel (read by the side chain)
+    float* scores;        // [U][G][n_page_max] page scores of this step (CFR-3 base-2 logits)
+    int32_t* pend_valid;  // [U]     1: pend_* holds a selection not yet committed to R
+    int32_t* order;       // [U]     units in scoring/selection priority order (corrected units first)
+    int32_t* ord_cnt;     // [2][2]  per step parity (ctx & 1): fill counters of `order` (corrected from the
+                          //         front, the others from the back)
+    int32_t* score_done;  // [U]     score items of the unit finished this step (release/acquire hand-off)
+    unsigned long long* trace;  // diagnostics (FREEKV_TRACE=1): %globaltimer stamps, else NULL
     uint16_t* host;       // device-mapped host pool of this layer: [nb][n_page_host][n_kv][2][p][d]
     const uint16_t* arena;  // base of the device arena (row 0 of the attention TMA tensor)
     int host_row0;        // first row of this layer's host pool in the host TMA tensor (256-byte rows)
 };
 
 struct FkvScratch {
-    float* scores;        // [U][G][n_page_max]
     int32_t* page_rows;   // [U][P_max] attention page list of this step: arena row of the page's K block
     uint8_t* page_valid;  // [U][P_max] valid tokens of each listed page; bit 7: the row is a host
                           // pool row (direct mode), to be written back to arena row page_dst
@@ -80,15 +90,18 @@ struct FkvScratch {
     float* part_o;        // [2 phases][attn_warps][2 segments][G][d] per-warp, per-unit-segment partial outputs
     float* part_ml;       // [2 phases][attn_warps][2 segments][G][2] (running max, running sum)
     float* cosv;          // [U][kMaxG] per-head correction cosines from the score kernel
+    int32_t* ready;       // [U] 1 once the select kernel has published unit u's selection (S_i, pend_*,
+                          // fetch list, corrected units' page list); reset by the attention's commit
 };
 
 __host__ __device__ inline size_t page_elems(const FkvDims& D) { return (size_t)2 * D.p * D.d; }
 
-// summary element offset (in uint16) of page j, channel c, which (0 = min, 1 = max)
-__device__ __forceinline__ size_t summ_chunk_offset(const FkvDims& D, int u, int j, int c8, int which) {
-    size_t unit_base = (size_t)u * D.n_page_max * 2 * D.d;
-    size_t blk = (size_t)(j >> 5) * (D.d / 8) + c8;
-    return unit_base + ((blk * 2 + which) * 32 + (j & 31)) * 8;
+// summary element offset (in uint16) of the 8 channels [8 c8, 8 c8 + 8) of page j, which (0 = min,
+// 1 = max).  Channel-group-major: the c8 slice of consecutive pages is contiguous, so a scoring
+// warp streams {8 channels x 128 pages} as two 2 KiB bulk copies and lane l reads page l with
+// conflict-free 16-byte shared loads.
+__host__ __device__ __forceinline__ size_t summ_off(const FkvDims& D, int u, int c8, int which, int j) {
+    return ((((size_t)u * (kHeadDim / 8) + c8) * 2 + which) * D.n_page_max + j) * 8;
 }
 
 __device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
@@ -184,59 +197,122 @@ __device__ __forceinline__ float cos_cfr10(const uint16_t* qa, const uint16_t* q
     return (n1 == 0.0f || n2 == 0.0f) ? 0.0f : __fdiv_rn(dot, __fmul_rn(__fsqrt_rn(n1), __fsqrt_rn(n2)));
 }
 
+// Group pooling of the heads' cosines (CFR-10): 0 = mean (sequential sum / G, FreeKV);
+// 1 = minimum, the "max pooling over group C_i" of tab:abl-g-corr (reading R-11)
+__device__ __forceinline__ float pool_cos(const float* c, int G, int corr_pool) {
+    float acc = c[0];
+    for (int g = 1; g < G; ++g) acc = corr_pool ? (c[g] < acc ? c[g] : acc) : __fadd_rn(acc, c[g]);
+    return corr_pool ? acc : __fdiv_rn(acc, (float)G);
+}
+
+// Correction decision of one unit (readings A-12, A-13): step 0 (no resident set) is
+// always corrected; ALWAYS / tau >= 1 always, NEVER / tau <= 0 never; else pooled cosine < tau.
+__device__ __forceinline__ int correction_flag(const FkvDims& D, float pooled, int res_valid) {
+    int flag;
+    if (D.mode == 1 || D.tau >= 1.0f) flag = 1;
+    else if (D.mode == 2 || D.tau <= 0.0f) flag = 0;
+    else flag = pooled < D.tau;
+    return res_valid ? flag : 1;
+}
+
+// Unit at index i of a part of the speculative step (-1 if none): part 0 = the corrected units
+// L.order[0, n0), part 1 = the others L.order[n0, U); the counters of this step's parity (ctx & 1,
+// the batch shares one context length) were filled by the pre kernel.  part < 0: unit i.
+__device__ __forceinline__ int part_unit(const FkvDims& D, const FkvLayer& L, int part, int i) {
+    if (part < 0) return i;
+    const int n0 = L.ord_cnt[(L.ctx[0] & 1) * 2];
+    const int base = part == 0 ? 0 : n0, n = part == 0 ? n0 : D.U - n0;
+    return i < n ? L.order[base + i] : -1;
+}
+
+__device__ __forceinline__ int ld_acquire(const int32_t* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// Spin until *p >= v (acquire).  Bounded: a hand-off that never comes (a bug) traps -- the launch
+// fails with an error instead of hanging the GPU (~4 s at 64 ns per poll).
+__device__ __forceinline__ void spin_until_ge(const int32_t* p, int v) {
+    for (long long i = 0; ld_acquire(p) < v; ++i) {
+        if (i > (1ll << 26)) __trap();
+        __nanosleep(64);
+    }
+}
+
+__device__ __forceinline__ void st_release(int32_t* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Kernel attribute set-up, once per (kernel, device): dynamic shared memory opt-in and the
+// max-shared carveout (every kernel of the path prefers it, so consecutive kernels never force
+// an L1/shared reconfiguration).  Thread-safe; defined in api.cu.
+cudaError_t func_smem(const void* kern, size_t dyn_smem);
+
+// prio: 0 = the stream's, else a CUDA priority value (kernel-node priority inside captured graphs)
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
-                             Args... args) {
+                             int prio, Args... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = pdl ? attr : nullptr;
-    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (prio) {
+        attr[na].id = cudaLaunchAttributePriority;
+        attr[na].val.priority = prio;
+        ++na;
+    }
+    cfg.attrs = na ? attr : nullptr;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 }  // namespace fkv
 
-// kernel launchers (defined in the .cu files), return cudaGetLastError()
+// kernel launchers (defined in the .cu files), return the launch status
 namespace fkv {
 cudaError_t launch_append(const FkvDims& D, const FkvLayer& L, const uint16_t* k, const uint16_t* v,
                           int n_new, cudaStream_t s);
 cudaError_t launch_summarize(const FkvDims& D, const FkvLayer& L, int page_begin, int page_end,
                              cudaStream_t s);
-// which (score / finalize): 0 every unit, 1 unflagged units only, 2 corrected units only
+// decode-step prologue of one layer (one CTA per unit): deferred commit R := pend, q_cur := q,
+// correction flag (CFR-10), append of this step's token, ctx / n_off publish; ordered: also the
+// order of the units (corrected first) that the two parts of the speculative step use
+cudaError_t launch_pre(const FkvDims& D, const FkvLayer& L, const uint16_t* q, const uint16_t* k_new,
+                       const uint16_t* v_new, int ordered, bool pdl, int prio, cudaStream_t s);
+// page scoring.  part -1: every unit; 0: the corrected units (latency variant, critical path);
+// 1: the others (throughput variant, side chain); parts 0/1 count finished items per unit
 cudaError_t launch_score(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                         int max_n_off, int pending, int which, bool pdl, cudaStream_t s,
-                         const uint16_t* k_new = nullptr, const uint16_t* v_new = nullptr);
-cudaError_t launch_prep(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                        const uint16_t* k_new, const uint16_t* v_new, uint8_t* corrected_out, bool pdl,
-                        cudaStream_t s);
-cudaError_t launch_select_fused(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                                const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
-                                uint8_t* corrected_out, int cluster, int lptm, cudaStream_t s);
-cudaError_t launch_finalize(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                            const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
-                            uint8_t* corrected_out, int lpt, int nt, bool pdl, int which, cudaStream_t s,
-                            int appended = 0);
-bool select_c2_fits(const FkvDims& D, int lpt, int nt);
-cudaError_t launch_select_c2(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                             const uint16_t* k_new, const uint16_t* v_new, int32_t* pages_out,
-                             uint8_t* corrected_out, int lpt, int nt, int cl, bool pdl, int which, cudaStream_t s);
+                         int max_n_off, int part, bool pdl, int prio, cudaStream_t s);
+// softmax + pooling + top-K + delta (nc CTAs per unit, lpt leaves per thread); flag_src 1: flags from
+// the score kernel; list_all: attention page lists of every unit (else of the corrected ones)
+// part as for the score kernel; parts 0/1 wait per unit for its score items (no PDL wait)
+cudaError_t launch_select(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
+                          int32_t* pages_out, uint8_t* corrected_out, int flag_src, int list_all, int part,
+                          int nc, int lpt, bool pdl, int prio, cudaStream_t s);
 cudaError_t launch_recall(const FkvDims& D, const FkvLayer& L, int sync_mode, cudaStream_t s,
                           unsigned long long* trace = nullptr);
 cudaError_t attn_resident_warps(int cps, int* warps);  // warps of the split kernel's grid (cps CTAs per SM)
 cudaError_t launch_attn_split(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                               int phase, const CUtensorMap& tmap, const CUtensorMap& tmap_host,
-                              const uint16_t* arena, bool pdl, cudaStream_t s, int wpc = 4);
+                              const uint16_t* arena, bool pdl, cudaStream_t s);
+// mode 0: page lists of every unit from the select kernel (waits for it), commits every unit;
+// mode 1: speculative decode step (see attn.cu)
 cudaError_t launch_attn_cluster(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                                float* out, int phase, const CUtensorMap& tmap, const CUtensorMap& tmap_h,
-                                int commit, int c, bool pdl, cudaStream_t s);
-// commit: 0 = every unit (R := S_i, q_prev := q_i), 2 = corrected units only (pipelined step:
-// the background select kernel commits the others)
+                                float* out, const CUtensorMap& tmap, const CUtensorMap& tmap_h, int mode, int c,
+                                bool pdl, int prio, cudaStream_t s);
 cudaError_t launch_attn_combine(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                                 float* out, int split, int commit, bool pdl, cudaStream_t s);
+// the fused decode step of one layer (layer.cu): c CTAs per unit, lpt pages per thread
+bool layer_supported(const FkvDims& D, int c, int lpt);
+cudaError_t launch_layer(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
+                         const uint16_t* k_new, const uint16_t* v_new, float* out, const CUtensorMap& tmap,
+                         const CUtensorMap& tmap_h, int c, int lpt, bool pdl, cudaStream_t s);
 }  // namespace fkv

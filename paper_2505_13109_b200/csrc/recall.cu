@@ -6,10 +6,10 @@
 // step's attention, the others in the background for reuse at step i+1.
 //
 // B200 design: the fetch list is produced on the GPU by the
-// select kernel, so the copy is a zero-copy gather: one CTA per fetched page
-// reads the device-mapped pinned host page over PCIe with 128-bit loads and
-// writes it into its free cache slot (slot double-buffering: the slot is not
-// read by any attention until the next commit).  Synchronous mode runs on the
+// select kernel, so the copy is a kernel: each fetched page moves from the
+// device-mapped pinned host pool into its free cache slot with TMA bulk copies
+// (slot double-buffering: the slot is not read by any attention until the next
+// commit).  Synchronous mode runs on the
 // compute stream for flagged units; background mode runs on the dedicated
 // recall stream for the others.
 #include <algorithm>
@@ -18,14 +18,6 @@
 #include "fkv_internal.cuh"
 
 namespace fkv {
-
-__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
-    uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
-}
 
 // The fetch lists of the units of this mode (sync: corrected units, background: the
 // others) are concatenated: every CTA loads all units' counts in one batch, builds the
@@ -39,7 +31,7 @@ constexpr int kRecallMaxU = 4096;
 
 __global__ void __launch_bounds__(kRecallThreads) fkv_recall_kernel(FkvDims D, FkvLayer L, int sync_mode,
                                                                     unsigned long long* __restrict__ trace,
-                                                                    int use_tma, int frag) {
+                                                                    int frag) {
     __shared__ int s_off[kRecallMaxU + 1];  // exclusive prefix of the eligible units' fetch counts
     __shared__ int s_wsum[kRecallThreads / 32];
     if (threadIdx.x == 0) trace_stamp(trace, 2 + (sync_mode ? 0 : 1), blockIdx.x, 0);
@@ -82,80 +74,45 @@ __global__ void __launch_bounds__(kRecallThreads) fkv_recall_kernel(FkvDims D, F
     __syncthreads();
     const int total = s_off[D.U];
     const size_t pe = page_elems(D);
-    const int n = (int)(pe / 8);  // uint4 per page
-    if (use_tma) {
-        // one elected thread moves each page with two bulk copies through shared memory
-        // (host pool -> smem over the link, smem -> slot in HBM): the copy engine of the TMA
-        // unit carries the PCIe reads, not the SM's load/store pipeline
-        extern __shared__ __align__(128) uint8_t s_page[];
-        __shared__ __align__(8) uint64_t bar;
-        if (tid == 0) {
-            mbar_init(&bar, 1);
-            fence_mbar_init();
-            uint32_t ph = 0;
-            const uint32_t bytes = (uint32_t)(pe * sizeof(uint16_t));
-            for (int f = blockIdx.x; f < total; f += gridDim.x) {
-                int lo = 0, hi = D.U - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (s_off[mid] <= f) lo = mid;
-                    else hi = mid - 1;
-                }
-                const int u = lo, k = f - s_off[u];
-                const int b = u / D.n_kv, m = u % D.n_kv;
-                const int j = L.fetch_page[(size_t)u * D.K + k];
-                const int slot = L.fetch_slot[(size_t)u * D.K + k];
-                const uint16_t* src = L.host + (((size_t)b * D.n_page_host + j) * D.n_kv + m) * pe;
-                uint16_t* dst = L.slots + ((size_t)u * 2 * D.K + slot) * pe;
-                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // s_page free again
-                mbar_expect_tx(&bar, bytes);
-                if (frag > 0 && frag < (int)bytes) {  // ablation: many small transfers per page
-                    for (uint32_t off = 0; off < bytes; off += (uint32_t)frag)
-                        bulk_g2s(s_page + off, reinterpret_cast<const uint8_t*>(src) + off, (uint32_t)frag, &bar);
-                } else {
-                    bulk_g2s(s_page, src, bytes, &bar);
-                }
-                mbar_wait(&bar, ph);
-                ph ^= 1u;
-                asm volatile(
-                    "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(s_page)),
-                    "r"(bytes)
-                    : "memory");
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    // one elected thread moves each page with two bulk copies through shared memory (host pool ->
+    // smem over the link, smem -> slot in HBM): the TMA engine carries the PCIe reads, not the SM's
+    // load/store pipeline
+    extern __shared__ __align__(128) uint8_t s_page[];
+    __shared__ __align__(8) uint64_t bar;
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+        uint32_t ph = 0;
+        const uint32_t bytes = (uint32_t)(pe * sizeof(uint16_t));
+        for (int f = blockIdx.x; f < total; f += gridDim.x) {
+            int lo = 0, hi = D.U - 1;  // unit of the f-th fetched page: the last u with s_off[u] <= f
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (s_off[mid] <= f) lo = mid;
+                else hi = mid - 1;
             }
-            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        }
-        if (threadIdx.x == 0) trace_stamp(trace, 2 + (sync_mode ? 0 : 1), blockIdx.x, 1);
-        return;
-    }
-    for (int f = blockIdx.x; f < total; f += gridDim.x) {
-        // unit of the f-th fetched page: the last u with s_off[u] <= f
-        int lo = 0, hi = D.U - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (s_off[mid] <= f) lo = mid;
-            else hi = mid - 1;
-        }
-        const int u = lo, k = f - s_off[u];
-        const int b = u / D.n_kv, m = u % D.n_kv;
-        const int j = L.fetch_page[(size_t)u * D.K + k];
-        const int slot = L.fetch_slot[(size_t)u * D.K + k];
-        const uint4* src =
-            reinterpret_cast<const uint4*>(L.host + (((size_t)b * D.n_page_host + j) * D.n_kv + m) * pe);
-        uint4* dst = reinterpret_cast<uint4*>(L.slots + ((size_t)u * 2 * D.K + slot) * pe);
-        for (int base2 = 0; base2 < n; base2 += 8 * kRecallThreads) {
-            uint4 r[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int idx = base2 + i * kRecallThreads + tid;
-                if (idx < n) r[i] = ld_stream(src + idx);
+            const int u = lo, k = f - s_off[u];
+            const int b = u / D.n_kv, m = u % D.n_kv;
+            const int j = L.fetch_page[(size_t)u * D.K + k];
+            const int slot = L.fetch_slot[(size_t)u * D.K + k];
+            const uint16_t* src = L.host + (((size_t)b * D.n_page_host + j) * D.n_kv + m) * pe;
+            uint16_t* dst = L.slots + ((size_t)u * 2 * D.K + slot) * pe;
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // s_page free again
+            mbar_expect_tx(&bar, bytes);
+            if (frag > 0 && frag < (int)bytes) {  // ablation (f2): many small transfers per page
+                for (uint32_t off = 0; off < bytes; off += (uint32_t)frag)
+                    bulk_g2s(s_page + off, reinterpret_cast<const uint8_t*>(src) + off, (uint32_t)frag, &bar);
+            } else {
+                bulk_g2s(s_page, src, bytes, &bar);
             }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int idx = base2 + i * kRecallThreads + tid;
-                if (idx < n) dst[idx] = r[i];
-            }
+            mbar_wait(&bar, ph);
+            ph ^= 1u;
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(s_page)),
+                         "r"(bytes)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     if (threadIdx.x == 0) trace_stamp(trace, 2 + (sync_mode ? 0 : 1), blockIdx.x, 1);
 }
@@ -175,41 +132,23 @@ static int recall_ctas(int sync_mode) {
 
 cudaError_t launch_recall(const FkvDims& D, const FkvLayer& L, int sync_mode, cudaStream_t s,
                           unsigned long long* trace) {
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(fkv_recall_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             cudaSharedmemCarveoutMaxShared);
-        configured = true;
-    }
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int want = recall_ctas(sync_mode ? 1 : 0);
     const int grid = std::min(want == 148 ? sms : want, D.U * D.K);
-    static int mode = -1;  // FREEKV_RECALL_MODE=ld: SM loads/stores instead of bulk copies
-    if (mode < 0) {
-        const char* e = getenv("FREEKV_RECALL_MODE");
-        mode = (e && e[0] == 'l') ? 0 : 1;
-    }
-    const size_t smem = mode ? page_elems(D) * sizeof(uint16_t) : 0;
-    static size_t smem_set = 0;
-    if (smem > smem_set) {
-        cudaError_t e = cudaFuncSetAttribute(fkv_recall_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        smem_set = smem;
-    }
+    const size_t smem = page_elems(D) * sizeof(uint16_t);
+    cudaError_t e = func_smem((const void*)fkv_recall_kernel, smem);
+    if (e != cudaSuccess) return e;
     // FREEKV_RECALL_FRAG=<bytes> (ablation): move each page as <bytes>-sized
     // transfers, e.g. 256 = one (token, head) row of an NHD host layout, instead of one 16 KiB page
     static int frag = -1;
     if (frag < 0) {
-        const char* e = getenv("FREEKV_RECALL_FRAG");
-        frag = e ? std::max(0, atoi(e)) : 0;
-        if (frag % 16) frag = 0;  // bulk copies move multiples of 16 bytes
+        const char* fe = getenv("FREEKV_RECALL_FRAG");
+        int v = fe ? std::max(0, atoi(fe)) : 0;
+        frag = (v % 16) ? 0 : v;  // bulk copies move multiples of 16 bytes
     }
-    fkv_recall_kernel<<<grid, kRecallThreads, smem, s>>>(D, L, sync_mode, trace, mode, frag);
+    fkv_recall_kernel<<<grid, kRecallThreads, smem, s>>>(D, L, sync_mode, trace, frag);
     return cudaGetLastError();
 }
 

@@ -149,13 +149,13 @@ def test_parity_long_context_many_tiles():
     run_parity(G=4, n_kv=1, batch=1, page=16, sink=64, window=64, budget=640, L0=20000, steps=3, n_layers=1)
 
 
-@pytest.mark.parametrize("pipeline", ["0", "1"])
-def test_step_graph_matches_eager(pipeline, monkeypatch):
-    """Whole-step CUDA graphs (one graph with forked recall branches; pipelined: two graphs
-    joined by external event nodes) give the same selections and bit-identical outputs as
-    the eager per-layer calls."""
+@pytest.mark.parametrize("overlap", ["0", "1"])
+def test_step_graph_matches_eager(overlap, monkeypatch):
+    """Whole-step CUDA graphs (one graph with forked recall branches) give the same selections and
+    bit-identical outputs as the eager per-layer calls, with the attention overlapping the select
+    (default) and waiting for it (FREEKV_OVERLAP=0)."""
     _need_gpu()
-    monkeypatch.setenv("FREEKV_PIPELINE", pipeline)
+    monkeypatch.setenv("FREEKV_OVERLAP", overlap)
     import paper_2505_13109_b200 as P
     nb, n_kv, G, d, p, L0, steps, n_layers = 2, 2, 4, 128, 32, 1200, 6, 3
     n_qo = G * n_kv
@@ -201,14 +201,6 @@ def test_step_graph_matches_eager(pipeline, monkeypatch):
     b.close()
 
 
-@pytest.mark.parametrize("select_impl", ["fused"])
-def test_parity_fused_cluster_select(select_impl, monkeypatch):
-    """The one-launch cluster select path (FREEKV_SELECT=fused) gives the same bits."""
-    monkeypatch.setenv("FREEKV_SELECT", select_impl)
-    run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=4)
-    run_parity(G=7, n_kv=1, batch=1, page=16, sink=64, window=64, budget=640, L0=9000, steps=3, n_layers=1)
-
-
 def test_parity_without_pdl(monkeypatch):
     monkeypatch.setenv("FREEKV_PDL", "0")
     run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=4)
@@ -229,59 +221,36 @@ def test_parity_full_refresh_direct(monkeypatch):
     run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=4, mode=O.MODE_ALWAYS, check_fetch=False)
 
 
-def test_parity_pipelined(monkeypatch):
-    """FREEKV_PIPELINE=1: speculative units attend R while the selection of step i runs in the
-    background; corrected units run score + select + attention on a second stream."""
-    monkeypatch.setenv("FREEKV_PIPELINE", "1")
+@pytest.mark.parametrize("nc", ["1", "2", "4", "8"])
+def test_parity_select_cluster_widths(nc, monkeypatch):
+    """The select kernel at every cluster width (CTAs per unit; CFR-6 power-of-two partition of the
+    pairwise tree, DSMEM exchange of maxima, subtree sums, histograms, boundary keys and ranks):
+    bit-identical pages to the oracle, |J| from 1 to 4 leaves per thread, G = 4 and G = 7."""
+    monkeypatch.setenv("FREEKV_SELECT_NC", nc)
+    run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=4)
+    run_parity(G=7, n_kv=1, batch=2, page=16, sink=64, window=64, budget=640, L0=20000, steps=3, n_layers=1)
+    run_parity(G=4, n_kv=1, batch=1, page=16, sink=64, window=64, budget=640, L0=60000, steps=2, n_layers=1,
+               tie_pages=True, event_rate=0.0)
+
+
+def test_parity_overlap_off(monkeypatch):
+    """FREEKV_OVERLAP=0: the attention waits for the whole select (page lists of every unit)."""
+    monkeypatch.setenv("FREEKV_OVERLAP", "0")
     run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=5)
-    run_parity(G=7, n_kv=1, batch=2, page=16, sink=64, window=64, budget=640, L0=3000, steps=4, n_layers=1)
-    run_parity(G=4, n_kv=2, batch=1, page=32, sink=64, window=0, budget=256, L0=1000, steps=40, n_layers=1)
+
+
+@pytest.mark.parametrize("env", [("FREEKV_RECALL_FRAG", "256"), ("FREEKV_RECALL_FRAG", "4096"),
+                                 ("FREEKV_SERIAL_RECALL", "1")])
+def test_parity_recall_ablation_modes(env, monkeypatch):
+    """The f2 ablation's recall variants (256-byte / 4 KiB transfers per page, background recall on
+    the compute stream) recall the same bytes: same selections and outputs as the oracle."""
+    monkeypatch.setenv(*env)
+    run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=6, event_rate=0.3)
 
 
 def test_parity_window_zero():
     """W = 0: the page completed by this step's token is a candidate at once (append first)."""
     run_parity(G=4, n_kv=2, batch=1, page=32, sink=64, window=0, budget=256, L0=1000, steps=40, n_layers=1)
-
-
-def test_parity_fused_c2_select(monkeypatch):
-    """FREEKV_SELECT=c2: score + select fused in 2-CTA clusters (helper CTA scores half of the
-    pages over DSMEM and does the append and correction check); default is two kernels."""
-    monkeypatch.setenv("FREEKV_SELECT", "c2")
-    run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=5)
-    run_parity(G=4, n_kv=1, batch=1, page=16, sink=64, window=64, budget=640, L0=20000, steps=3, n_layers=1)
-
-
-@pytest.mark.parametrize("threads", ["512", "1024"])
-def test_parity_select_finalize_threads(threads, monkeypatch):
-    """The default (unfused) select kernel at 512 and 1024 threads: leaves per thread change,
-    the pairwise tree of CFR-6 does not; |J| above 1024 too."""
-    monkeypatch.setenv("FREEKV_FIN_THREADS", threads)
-    run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=4)
-    run_parity(G=7, n_kv=1, batch=2, page=16, sink=64, window=64, budget=640, L0=20000, steps=3, n_layers=1)
-
-
-@pytest.mark.parametrize("threads", ["256", "512", "1024"])
-def test_parity_select_threads(threads, monkeypatch):
-    """The fused select at other CTA sizes (leaves per thread change; the tree does not)."""
-    monkeypatch.setenv("FREEKV_SELECT", "c2")
-    monkeypatch.setenv("FREEKV_SELECT_THREADS", threads)
-    run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=4)
-    run_parity(G=8, n_kv=1, batch=1, page=16, sink=64, window=64, budget=640, L0=9000, steps=3, n_layers=1)
-
-
-def test_parity_split_attention(monkeypatch):
-    """FREEKV_ATTN=split: balanced split-KV attention + combine kernels (the default attends
-    each unit with a cluster of CTAs and merges the partial records over DSMEM)."""
-    monkeypatch.setenv("FREEKV_ATTN", "split")
-    run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=5)
-    run_parity(G=4, n_kv=2, batch=1, page=32, L0=900, steps=4, use_primitives=True)
-
-
-def test_parity_speculative_attention(monkeypatch):
-    """FREEKV_ATTN_SPEC=1: units attend their resident set before the select finishes; corrected
-    units discard that work (results identical)."""
-    monkeypatch.setenv("FREEKV_ATTN_SPEC", "1")
-    run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=6)
 
 
 @pytest.mark.parametrize("pool", [1, 2, 3, 4, 5])
@@ -293,11 +262,11 @@ def test_parity_pooling_variants(pool):
                pool=pool)
 
 
-@pytest.mark.parametrize("pipeline", ["0", "1"])
-def test_parity_max_pooled_correction(pipeline, monkeypatch):
+@pytest.mark.parametrize("overlap", ["0", "1"])
+def test_parity_max_pooled_correction(overlap, monkeypatch):
     """Max-pooled correction (tab:abl-g-corr, reading R-11): corrected when any head's similarity
     is below tau; more units corrected than with mean pooling on the same inputs."""
-    monkeypatch.setenv("FREEKV_PIPELINE", pipeline)
+    monkeypatch.setenv("FREEKV_OVERLAP", overlap)
     nf_max, _, _ = run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=5, corr_pool=1, event_rate=0.3)
     nf_mean, _, _ = run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=5, corr_pool=0, event_rate=0.3)
     assert nf_max >= nf_mean

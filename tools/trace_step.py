@@ -7,7 +7,8 @@ import numpy as np, torch
 import paper_2505_13109_b200 as P
 import synth
 
-nb, nq, nk, d, p, ctx, L = 8, 32, 8, 128, 32, 32768, 2
+nb, nq, nk, d, p, ctx = 8, 32, 8, 128, 32, 32768
+L = int(os.environ.get("FKV_TRACE_LAYERS", "2"))
 cfg = P.FreeKVConfig(n_layers=L, batch=nb, n_qo=nq, n_kv=nk, max_ctx_tokens=ctx + 64)
 fkv = P.FreeKV(cfg)
 dev = fkv.device
@@ -26,8 +27,8 @@ if GRAPH:
     kb = torch.empty(L, nb, 1, nk, d, dtype=torch.bfloat16, device=dev)
     vb = torch.empty_like(kb)
     ob = torch.empty(L, nb, nq, d, dtype=torch.float32, device=dev)
-names = {0: "score", 1: "finalize", 2: "recall_sync", 3: "recall_bg", 4: "attn", 5: "attn_phase1", 6: "attn_phase2",
-         7: "combine", 8: "prep", 9: "score_bg", 10: "finalize_bg", 11: "radix_passes"}
+names = {0: "score", 1: "select", 2: "recall_sync", 3: "recall_bg", 4: "attn", 5: "attn_phase1", 6: "attn_phase2",
+         7: "merge", 8: "pre", 9: "score_bg", 10: "finalize_bg", 11: "radix_passes"}
 res = {}
 def steps():
     for i in range(12):
