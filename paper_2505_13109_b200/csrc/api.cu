@@ -83,6 +83,7 @@ struct freekv_handle {
     int prio_hi = 0;             // kernel priority of the critical path (pre, attention)
     int attn_cluster = 1;        // CTAs per unit of the clustered attention
     int sel_nc = 1, sel_lpt = 1; // select: CTAs per unit (cluster), leaves per thread (CFR-6 tree)
+    int sel_nt = 256;            // select: threads per CTA (256, or 1024 for one CTA per unit)
     int fsel_nc = 1, fsel_lpt = 1;  // the corrected units' select on the critical path (speculative step)
     int bsel_nc = 1, bsel_lpt = 1;  // the other units' select in the side chain (speculative step)
     std::vector<int> ctx_host;
@@ -271,7 +272,11 @@ freekv_status do_append(freekv_handle* h, int layer, const void* k, const void* 
 // select kernel.  flag_src 1: the pre kernel decided the correction flags; list_all: page lists of
 // every unit for the attention.
 freekv_status do_select(freekv_handle* h, int layer, const void* q, int32_t* pages_out, uint8_t* corr_out,
-                        cudaStream_t s, int flag_src, int list_all) {
+                        cudaStream_t s, int flag_src, int list_all, const void* k_new = nullptr,
+                        const void* v_new = nullptr) {
+    // k_new/v_new given (serial step, W >= 1 page): the score grid also runs the correction check
+    // and the append of every unit (its first U CTAs); the token stays pending until the attention
+    const int pending = k_new ? 1 : 0;
     if (!q) return fail(FREEKV_EINVAL, "q is NULL");
     if (h->ctx_host[layer] <= 0) return fail(FREEKV_ESTATE, "select before any token was appended");
     // the background recall of the previous step reads this layer's fetch list (one-graph
@@ -283,13 +288,15 @@ freekv_status do_select(freekv_handle* h, int layer, const void* q, int32_t* pag
         FKV_CUDA(cudaStreamWaitEvent(s, h->ev_recall[layer], 0));
     const int mno = h->capturing ? max_n_off(h->D, h->D.max_ctx) : max_n_off(h->D, h->ctx_host[layer]);
     FkvLayer& L = h->layers[layer];
-    if (h->capturing || mno - h->D.n_sink > h->D.K)
+    const bool scoring = h->capturing || mno - h->D.n_sink > h->D.K;
+    if (scoring || pending)
         FKV_CUDA(timed(h, K_SCORE, s, [&] {
-            return launch_score(h->D, L, h->X, (const uint16_t*)q, mno, -1, h->pdl, 0, s);
+            return launch_score(h->D, L, h->X, (const uint16_t*)q, scoring ? mno : 0, pending ? -2 : -1, h->pdl,
+                                0, s, (const uint16_t*)k_new, (const uint16_t*)v_new);
         }));
     FKV_CUDA(timed(h, K_FINALIZE, s, [&] {
         return launch_select(h->D, L, h->X, (const uint16_t*)q, pages_out, corr_out, flag_src, list_all, -1,
-                             h->sel_nc, h->sel_lpt, h->pdl, 0, s);
+                             h->sel_nc, h->sel_lpt, h->pdl, 0, s, pending, h->sel_nt);
     }));
     return FREEKV_OK;
 }
@@ -340,14 +347,14 @@ freekv_status do_attn(freekv_handle* h, int layer, const void* q, float* out, cu
 // runs on the high-priority stream ss while the attention of every other unit (whose pages are
 // resident) runs on the compute stream; the corrected units are attended once their pages have
 // landed.  The background recall follows the synchronous one.
-freekv_status do_step_tail(freekv_handle* h, int layer, const void* q, float* out) {
+freekv_status do_step_tail(freekv_handle* h, int layer, const void* q, float* out, int pending = 0) {
     cudaStream_t cs = h->cs;
     const FkvDims& D = h->D;
     FkvLayer& L = h->layers[layer];
     if (D.direct) {
         FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] {
-            return launch_attn_cluster(D, L, h->X, (const uint16_t*)q, out, h->tmap_kv, h->tmap_host, 0,
-                                       h->attn_cluster, h->pdl, h->prio_hi, cs);
+            return launch_attn_cluster(D, L, h->X, (const uint16_t*)q, out, h->tmap_kv, h->tmap_host, 2,
+                                       h->attn_cluster, h->pdl, h->prio_hi, cs, pending);
         }));
         // the background recall of this layer starts after its attention (which completes only after
         // the select); it overlaps the next layers
@@ -435,6 +442,16 @@ freekv_status do_layer_step(freekv_handle* h, int layer, const void* q, const vo
         }
         if (!h->capturing) h->recall_pending[layer] = 1;
         return FREEKV_OK;
+    }
+    if (!h->spec && D.direct && D.n_win >= 1) {
+        // serial step, three launches: score grid (+ correction check and append per unit, the token
+        // pending) -> select (every unit's page list) -> attention (mode 2; its commit publishes the
+        // new context length).  A window of >= 1 page keeps the page the append completes out of
+        // this step's candidates, so the append may run beside the scoring.
+        if (!h->capturing) h->ctx_host[layer] += 1;
+        freekv_status st = do_select(h, layer, q, nullptr, nullptr, cs, 1, 1, k_new, v_new);
+        if (st != FREEKV_OK) return st;
+        return do_step_tail(h, layer, q, out, 1);
     }
     FKV_CUDA(timed(h, K_PRE, cs, [&] {
         return launch_pre(D, L, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new, h->spec ? 1 : 0,
@@ -618,6 +635,7 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
     h->X.page_valid = (uint8_t*)(sb + s.o_page_valid);
     h->X.page_dst = (int32_t*)(sb + s.o_page_dst);
     h->X.ready = (int32_t*)(sb + s.o_ready);
+    h->X.arena = h->layers[0].arena;
 
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
@@ -630,6 +648,9 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         while (P2 < n_off_max) P2 <<= 1;
         int nc = 8;
         while (nc > 1 && (D.U * nc > sms || nc * 256 > P2)) nc >>= 1;
+        // many units (<= 2 CTAs each would fit): one wide 1024-thread CTA per unit instead
+        // (A/B on B200 at c2: 42.3 us/layer vs 50.3 with 2-CTA clusters of 256 threads)
+        if (nc <= 2 && P2 >= 1024 && P2 / 1024 <= 8) nc = 1;
         const char* ne = getenv("FREEKV_SELECT_NC");  // A/B: force the cluster width (1, 2, 4, 8)
         if (ne && (atoi(ne) == 1 || atoi(ne) == 2 || atoi(ne) == 4 || atoi(ne) == 8)) nc = atoi(ne);
         int lpt = std::max(1, P2 / (nc * 256));
@@ -643,6 +664,15 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         }
         h->sel_nc = nc;
         h->sel_lpt = lpt;
+        // one 1024-thread CTA per unit when there are enough units to fill the GPU with clusters
+        // of one (A/B on B200: the wide CTA's short per-thread chains beat both the 256-thread CTA
+        // and a 2-CTA cluster at c2); FREEKV_SELECT_NT=256|1024 overrides
+        const char* nte = getenv("FREEKV_SELECT_NT");
+        int nt = (nc == 1 && P2 >= 1024 && P2 / 1024 <= 8) ? 1024 : 256;
+        if (nte && (atoi(nte) == 256 || atoi(nte) == 1024)) nt = atoi(nte);
+        if (nt == 1024 && (nc != 1 || P2 < 1024 || P2 / 1024 > 8)) nt = 256;
+        if (nt == 1024) h->sel_lpt = P2 / 1024;
+        h->sel_nt = nt;
         // speculative step: the corrected units' select (few units, critical path) as wide as the tree
         // allows (<= 8 CTAs, >= 256 leaves each); the side chain's select one CTA per unit (clusters
         // would constrain the placement of the attention's clusters it runs beside)
@@ -667,7 +697,7 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         // step mode (FREEKV_STEP): fused (default: one kernel per layer, layer.cu), spec (pre kernel,
         // attention beside the scoring/selection streams), serial (pre, score, select, attention)
         const char* ov = getenv("FREEKV_STEP");
-        const std::string mode = ov ? ov : "fused";
+        const std::string mode = ov ? ov : "serial";
         h->spec = h->D.direct && mode == "spec";
         if (h->D.direct && mode == "fused") {
             int c = 8;
@@ -718,6 +748,10 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         h->D.full_refresh = (fr && fr[0] == '1') ? 1 : 0;
         const char* lo2 = getenv("FREEKV_LAYER_ORDER");
         h->D.dbg_order = lo2 ? atoi(lo2) : 0;
+        const char* st = getenv("FREEKV_SEL_TRIGGER");
+        h->D.sel_trig = st ? atoi(st) : 0;
+        const char* sp = getenv("FREEKV_SCORE_PPT");
+        h->D.score_ppt = sp ? atoi(sp) : 4;
     }
     {
         const char* sr = getenv("FREEKV_SERIAL_RECALL");

@@ -100,6 +100,5 @@ __device__ __forceinline__ void append_unit(const FkvDims& D, const FkvLayer& L,
     }
 }
 
-__device__ __forceinline__ int frontier_for(const FkvDims& D, int ctx) { return max(D.n_sink, ctx / D.p - D.n_win); }
 
 }  // namespace fkv

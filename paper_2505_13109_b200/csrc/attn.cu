@@ -195,7 +195,7 @@ template <int NST, int C>
 __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 3)
     fkv_attn_cluster_kernel(FkvDims D, FkvLayer L, FkvScratch X, const uint16_t* __restrict__ q,
                             float* __restrict__ out, const __grid_constant__ CUtensorMap tmap,
-                            const __grid_constant__ CUtensorMap tmap_h, int mode) {
+                            const __grid_constant__ CUtensorMap tmap_h, int mode, int pending) {
     constexpr int kStages = NST, W = kAttnWarpsPerCta, NW = W * C;
     extern __shared__ __align__(1024) uint8_t s_stage[];  // [W][kStages][8 KiB]; then the records
     __shared__ __align__(8) uint64_t bar[W][kStages];
@@ -207,7 +207,14 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 3)
     const int G = D.G;
     pdl_trigger();
     const int w = u * NW + crank * W + warp;  // trace entity
-    if (lane == 0) trace_stamp(X.trace, 4, w, 0);
+    if (lane == 0) {
+        trace_stamp(X.trace, 4, w, 0);
+        if (X.trace && w < kTraceEnt) {  // diagnostics: the SM of this warp
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            X.trace[((size_t)4 * kTraceEnt + w) * kTraceStamps + 7] = smid;
+        }
+    }
     uint8_t* ring = s_stage + warp * (kStages * kSlabBytes);
     if (lane == 0) {
 #pragma unroll
@@ -230,9 +237,37 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 3)
         for (int j = 0; j < 4; ++j) oacc[i][j] = 0.0f;
     float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.0f, 0.0f};
     uint4 qa[2][2];
-    pdl_wait();  // mode 0: every page list is written by the select kernel; mode 1: the pre kernel is done
-    const int flag = L.flags[u];
-    const int Lc = L.ctx[u];
+    // mode 2 (serial decode step): the pre kernel has completed when this grid launches (the select
+    // before it triggers after its own wait, the score before that after its own), so the flags,
+    // the context length and R are final.  A unit that is not corrected attends the same list the
+    // select would write for it -- sink pages, R, local pages -- built from R here, and its first
+    // slabs are in flight before the wait for the select
+    int flag = 0, Lc = 0, pre = 0;
+    if (mode == 2) {
+        flag = L.flags[u];
+        Lc = L.ctx[u] + pending;
+        if (!flag) {
+            const ResSrc rsrc = res_src(D, L, u, Lc);
+            const int n_pages = rsrc.count();
+#pragma unroll
+            for (int i = 0; i < kStages; ++i) {
+                const int x = sa + i;
+                if (x >= sb) break;
+                const int pi = x / spp, sl = x - pi * spp;
+                if (pi >= n_pages) break;
+                int row, valid, dst;
+                rsrc.load(pi, row, valid, dst);
+                if (valid - sl * 16 <= 0) break;
+                if (lane == 0) issue_slab(&tmap, ring + i * kSlabBytes, &bar[warp][i], row + sl * 16, D.p, X.arena);
+                pre = i + 1;
+            }
+        }
+    }
+    pdl_wait();  // mode 0/2: the select kernel's page lists are complete; mode 1: the pre kernel is done
+    if (mode != 2) {
+        flag = L.flags[u];
+        Lc = L.ctx[u];
+    }
     load_q_frags(D, q, u, qa);
     if (mode == 1 && flag) {  // corrected unit: its S_i page list comes from the select kernel
         if (lane == 0)
@@ -249,7 +284,7 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 3)
         const ResSrc rsrc = res_src(D, L, u, Lc);
         const int pe = min(pbc, rsrc.count());
         attend_pages<NST>(D, X, qa, &tmap, &tmap_h, rsrc, pa, pe, ring, bar[warp], phase_bits, m_run, l_run, oacc, 4,
-                          w, 0, skip, pe == pbc ? trim : 0);
+                          w, pre, skip, pe == pbc ? trim : 0);
     }
     if (lane == 0) trace_stamp(X.trace, 4, w, 3);
     // ---- this warp's record, in its own (now idle) ring: o [G][128], then m [G], l [G]
@@ -269,25 +304,54 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 3)
             }
         }
     }
-    cl.sync();  // every record of the unit is in its CTA's shared memory
+    // CTA-level merge of the W warp records into one CTA record (warp 0's second stage), then the
+    // leader merges the C CTA records over DSMEM: C remote records per output instead of W * C
+    __syncthreads();
+    float* crec = reinterpret_cast<float*>(s_stage + kSlabBytes);
+    for (int e = tid; e < G * (kHeadDim / 4); e += blockDim.x) {
+        const int h = e / (kHeadDim / 4), c4 = e % (kHeadDim / 4);
+        float M = -INFINITY;
+#pragma unroll
+        for (int r = 0; r < W; ++r)
+            M = fmaxf(M, reinterpret_cast<const float*>(s_stage + r * (kStages * kSlabBytes))[G * kHeadDim + h]);
+        float Ls = 0.0f;
+        float4 O = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+        for (int r = 0; r < W; ++r) {
+            const float* rr = reinterpret_cast<const float*>(s_stage + r * (kStages * kSlabBytes));
+            const float mr = rr[G * kHeadDim + h];
+            const float wgt = mr == -INFINITY ? 0.0f : exp2f(mr - M);
+            const float4 o = reinterpret_cast<const float4*>(rr + h * kHeadDim)[c4];
+            Ls += wgt * rr[G * kHeadDim + G + h];
+            O.x += wgt * o.x;
+            O.y += wgt * o.y;
+            O.z += wgt * o.z;
+            O.w += wgt * o.w;
+        }
+        reinterpret_cast<float4*>(crec + h * kHeadDim)[c4] = O;
+        if (c4 == 0) {
+            crec[G * kHeadDim + h] = M;
+            crec[G * kHeadDim + G + h] = Ls;
+        }
+    }
+    cl.sync();  // every CTA record of the unit is in its CTA's shared memory
     if (crank == 0) {
         if (tid == 0) trace_stamp(X.trace, 7, u, 0);
-        // thread -> (head h, 4 channels); records read over DSMEM, merged with an online max
+        // thread -> (head h, 4 channels); CTA records read over DSMEM, merged with an online max
 #pragma unroll
         for (int qi = 0; qi < kQv; ++qi) {
             const int e = tid + qi * (int)blockDim.x;
             if (e >= G * (kHeadDim / 4)) break;
-            const float4 o4 = merge_records<NW>(G, e, [&](int r) {
-                return cl.map_shared_rank(reinterpret_cast<const float*>(s_stage + (r % W) * (kStages * kSlabBytes)),
-                                          r / W);
+            const float4 o4 = merge_records<C>(G, e, [&](int r) {
+                return cl.map_shared_rank(reinterpret_cast<const float*>(s_stage + kSlabBytes), r);
             });
             const size_t row = (size_t)b * D.n_qo + m * G + e / (kHeadDim / 4);
             reinterpret_cast<float4*>(out + row * kHeadDim)[e % (kHeadDim / 4)] = o4;
             reinterpret_cast<uint2*>(L.q_prev + row * kHeadDim)[e % (kHeadDim / 4)] = qv[qi];  // q_prev := q_i
         }
-        // commit R := S_i: every unit in mode 0; in mode 1 the corrected units (the others'
-        // S_i is committed by the next step's pre kernel, after their background recall)
-        if (mode == 0 || flag) {
+        // commit R := S_i: every unit in modes 0 and 2; in mode 1 the corrected units (the
+        // others' S_i is committed by the next step's pre kernel, after their background recall)
+        if (mode != 1 || flag) {
             for (int i = tid; i < D.K; i += blockDim.x) {
                 L.res_pages[(size_t)u * D.K + i] = __ldcg(L.pend_pages + (size_t)u * D.K + i);
                 L.res_slot[(size_t)u * D.K + i] = __ldcg(L.pend_slot + (size_t)u * D.K + i);
@@ -298,6 +362,10 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 3)
                 L.res_valid[u] = 1;
                 L.pend_valid[u] = 0;
                 X.ready[u] = 0;
+                if (pending) {  // the token the score grid appended is now part of the context
+                    L.ctx[u] = Lc;
+                    L.n_off[u] = max(L.n_off[u], frontier_for(D, Lc));
+                }
             }
         }
         if (tid == 0) trace_stamp(X.trace, 7, u, 1);
@@ -308,7 +376,7 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 3)
 template <int NST, int C>
 static cudaError_t launch_cluster_c(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                                     float* out, const CUtensorMap& tmap, const CUtensorMap& tmap_h, int mode, bool pdl,
-                                    int prio, cudaStream_t s) {
+                                    int prio, cudaStream_t s, int pending) {
     auto kern = fkv_attn_cluster_kernel<NST, C>;
     const int smem = kAttnWarpsPerCta * NST * kSlabBytes;
     cudaError_t e = func_smem((const void*)kern, smem);
@@ -337,20 +405,20 @@ static cudaError_t launch_cluster_c(const FkvDims& D, const FkvLayer& L, const F
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, kern, D, L, X, q, out, tmap, tmap_h, mode);
+    return cudaLaunchKernelEx(&cfg, kern, D, L, X, q, out, tmap, tmap_h, mode, pending);
 }
 
 // Clustered attention + merge + commit; c = CTAs per unit (1, 2, 4, 8)
 cudaError_t launch_attn_cluster(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                                 float* out, const CUtensorMap& tmap, const CUtensorMap& tmap_h, int mode, int c,
-                                bool pdl, int prio, cudaStream_t s) {
+                                bool pdl, int prio, cudaStream_t s, int pending) {
     const int nst = attn_stages();
 #define FKV_CL(NS)                                                                                         \
     do {                                                                                                   \
-        if (c == 1) return launch_cluster_c<NS, 1>(D, L, X, q, out, tmap, tmap_h, mode, pdl, prio, s); \
-        if (c == 2) return launch_cluster_c<NS, 2>(D, L, X, q, out, tmap, tmap_h, mode, pdl, prio, s); \
-        if (c == 4) return launch_cluster_c<NS, 4>(D, L, X, q, out, tmap, tmap_h, mode, pdl, prio, s); \
-        return launch_cluster_c<NS, 8>(D, L, X, q, out, tmap, tmap_h, mode, pdl, prio, s);             \
+        if (c == 1) return launch_cluster_c<NS, 1>(D, L, X, q, out, tmap, tmap_h, mode, pdl, prio, s, pending); \
+        if (c == 2) return launch_cluster_c<NS, 2>(D, L, X, q, out, tmap, tmap_h, mode, pdl, prio, s, pending); \
+        if (c == 4) return launch_cluster_c<NS, 4>(D, L, X, q, out, tmap, tmap_h, mode, pdl, prio, s, pending); \
+        return launch_cluster_c<NS, 8>(D, L, X, q, out, tmap, tmap_h, mode, pdl, prio, s, pending);             \
     } while (0)
     if (nst == 2) FKV_CL(2);
     FKV_CL(3);

@@ -63,8 +63,16 @@ __device__ __forceinline__ void store_slab(const CUtensorMap* map, const uint8_t
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
-__device__ __forceinline__ void issue_slab(const CUtensorMap* map, uint8_t* st, uint64_t* bar, int row, int p) {
+__device__ __forceinline__ void issue_slab(const CUtensorMap* map, uint8_t* st, uint64_t* bar, int row, int p,
+                                           const uint16_t* arena = nullptr) {
     mbar_expect_tx(bar, kSlabBytes);
+#ifdef FKV_ATTN_BULK  // A/B timing experiment only (unswizzled, wrong results): two 1D 4 KB copies
+    if (arena) {
+        bulk_g2s(st, arena + (size_t)row * 128, 2 * kBoxBytes, bar);
+        bulk_g2s(st + 2 * kBoxBytes, arena + (size_t)(row + p) * 128, 2 * kBoxBytes, bar);
+        return;
+    }
+#endif
     tma_load_2d(st + 0 * kBoxBytes, map, 0, row, bar);
     tma_load_2d(st + 1 * kBoxBytes, map, 64, row, bar);
     tma_load_2d(st + 2 * kBoxBytes, map, 0, row + p, bar);
@@ -285,7 +293,8 @@ __device__ __forceinline__ void attend_pages(const FkvDims& D, const FkvScratch&
 #pragma unroll
             for (int i = 0; i < kStages; ++i)
                 if (valids[i] > 0 && !(cb == pa && i < pre))
-                    issue_slab(is_host(i0 + i) ? &tmap_h : &tmap, ring + i * kSlabBytes, &bars[i], rows[i], D.p);
+                    issue_slab(is_host(i0 + i) ? &tmap_h : &tmap, ring + i * kSlabBytes, &bars[i], rows[i], D.p,
+                               is_host(i0 + i) ? nullptr : X.arena);
         }
         for (int i = i0; i < nx; ++i) {
             const int stg = (i - i0) % kStages;
@@ -298,7 +307,11 @@ __device__ __forceinline__ void attend_pages(const FkvDims& D, const FkvScratch&
                 mbar_wait(&bars[stg], (phase_bits >> stg) & 1u);
                 phase_bits ^= 1u << stg;
                 if (i == 0 && lane == 0) trace_stamp(X.trace, tcls, w, 2);
+#ifndef FKV_ATTN_NOCOMPUTE
                 compute_slab(ring + stg * kSlabBytes, valid, qa, sc, g, t, m_run, l_run, oacc);
+#else
+                oacc[0][0] += (float)ring[stg * kSlabBytes + lane];
+#endif
             }
             __syncwarp();  // every lane is done with this stage before it is refilled
             if (lane == 0) {
@@ -309,7 +322,7 @@ __device__ __forceinline__ void attend_pages(const FkvDims& D, const FkvScratch&
                 if (valid2 > 0) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     issue_slab(is_host(i + kStages) ? &tmap_h : &tmap, ring + stg * kSlabBytes, &bars[stg],
-                               row2, D.p);
+                               row2, D.p, is_host(i + kStages) ? nullptr : X.arena);
                 }
             }
         }

@@ -32,6 +32,9 @@ struct FkvDims {
     int mode;
     int full_refresh; // diagnostics (env FREEKV_DEBUG_FULL_REFRESH=1): no slot reuse, all pages re-fetched
     int dbg_order;    // A/B (env FREEKV_LAYER_ORDER): bit 0 = every uncorrected unit attends first
+    int score_ppt;    // pages per thread of the score kernel (parts -1/-2): 1, 2 or 4 (env FREEKV_SCORE_PPT)
+    int sel_trig;     // serial step: where the select kernel lets the attention launch (PDL trigger):
+                      // 0 at its start, 1 after the ranking, 2 at its end (env FREEKV_SEL_TRIGGER)
     int pool;         // FREEKV_POOL_* group pooling of the selection (f3); 0 = MeanS
     int corr_pool;    // 0 = mean of the cosines, 1 = corrected when the least similar head is below tau
     float tau;
@@ -90,6 +93,7 @@ struct FkvScratch {
     float* part_o;        // [2 phases][attn_warps][2 segments][G][d] per-warp, per-unit-segment partial outputs
     float* part_ml;       // [2 phases][attn_warps][2 segments][G][2] (running max, running sum)
     float* cosv;          // [U][kMaxG] per-head correction cosines from the score kernel
+    const uint16_t* arena;  // base of the device arena (row 0 of the attention TMA tensor)
     int32_t* ready;       // [U] 1 once the select kernel has published unit u's selection (S_i, pend_*,
                           // fetch list, corrected units' page list); reset by the attention's commit
 };
@@ -218,6 +222,9 @@ __device__ __forceinline__ int correction_flag(const FkvDims& D, float pooled, i
 // Unit at index i of a part of the speculative step (-1 if none): part 0 = the corrected units
 // L.order[0, n0), part 1 = the others L.order[n0, U); the counters of this step's parity (ctx & 1,
 // the batch shares one context length) were filled by the pre kernel.  part < 0: unit i.
+// end of the candidate range [n_sink, n_off) once the context holds ctx tokens
+__device__ __forceinline__ int frontier_for(const FkvDims& D, int ctx) { return max(D.n_sink, ctx / D.p - D.n_win); }
+
 __device__ __forceinline__ int part_unit(const FkvDims& D, const FkvLayer& L, int part, int i) {
     if (part < 0) return i;
     const int n0 = L.ord_cnt[(L.ctx[0] & 1) * 2];
@@ -287,16 +294,20 @@ cudaError_t launch_summarize(const FkvDims& D, const FkvLayer& L, int page_begin
 // order of the units (corrected first) that the two parts of the speculative step use
 cudaError_t launch_pre(const FkvDims& D, const FkvLayer& L, const uint16_t* q, const uint16_t* k_new,
                        const uint16_t* v_new, int ordered, bool pdl, int prio, cudaStream_t s);
-// page scoring.  part -1: every unit; 0: the corrected units (latency variant, critical path);
-// 1: the others (throughput variant, side chain); parts 0/1 count finished items per unit
+// page scoring.  part -1: every unit; -2: every unit plus one CTA per unit for the correction check
+// and the append of k_new/v_new (serial step, the token pending); 0: the corrected units (latency
+// variant, critical path); 1: the others (throughput variant, side chain); parts 0/1 count
+// finished items per unit
 cudaError_t launch_score(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                         int max_n_off, int part, bool pdl, int prio, cudaStream_t s);
+                         int max_n_off, int part, bool pdl, int prio, cudaStream_t s,
+                         const uint16_t* k_new = nullptr, const uint16_t* v_new = nullptr);
 // softmax + pooling + top-K + delta (nc CTAs per unit, lpt leaves per thread); flag_src 1: flags from
 // the score kernel; list_all: attention page lists of every unit (else of the corrected ones)
-// part as for the score kernel; parts 0/1 wait per unit for its score items (no PDL wait)
+// part as for the score kernel; parts 0/1 wait per unit for its score items (no PDL wait).
+// pending: this step's token was appended by the score grid but not yet published (serial step)
 cudaError_t launch_select(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                           int32_t* pages_out, uint8_t* corrected_out, int flag_src, int list_all, int part,
-                          int nc, int lpt, bool pdl, int prio, cudaStream_t s);
+                          int nc, int lpt, bool pdl, int prio, cudaStream_t s, int pending = 0, int nt = 256);
 cudaError_t launch_recall(const FkvDims& D, const FkvLayer& L, int sync_mode, cudaStream_t s,
                           unsigned long long* trace = nullptr);
 cudaError_t attn_resident_warps(int cps, int* warps);  // warps of the split kernel's grid (cps CTAs per SM)
@@ -307,7 +318,7 @@ cudaError_t launch_attn_split(const FkvDims& D, const FkvLayer& L, const FkvScra
 // mode 1: speculative decode step (see attn.cu)
 cudaError_t launch_attn_cluster(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                                 float* out, const CUtensorMap& tmap, const CUtensorMap& tmap_h, int mode, int c,
-                                bool pdl, int prio, cudaStream_t s);
+                                bool pdl, int prio, cudaStream_t s, int pending = 0);
 cudaError_t launch_attn_combine(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                                 float* out, int split, int commit, bool pdl, cudaStream_t s);
 // the fused decode step of one layer (layer.cu): c CTAs per unit, lpt pages per thread

@@ -67,16 +67,18 @@ __device__ __forceinline__ uint32_t u4w(const uint4& v, int i) {
 //    back) -- the side chain scores and selects the corrected units first.
 constexpr int kPreThreads = 128;
 
-__global__ void __launch_bounds__(kPreThreads) fkv_pre_kernel(FkvDims D, FkvLayer L, const uint16_t* __restrict__ q,
-                                                              const uint16_t* __restrict__ k_new,
-                                                              const uint16_t* __restrict__ v_new, int ordered) {
-    extern __shared__ __align__(16) uint4 s_page[];  // append staging: one (2, p, d) page
+// full = 1: the pre kernel (every duty above).  full = 0: the extra CTAs of the serial step's score
+// grid -- correction flag and append only; the context length stays unpublished until the
+// attention's commit (the scoring CTAs of the same grid read it: the token is "pending").
+__device__ __forceinline__ void pre_unit(const FkvDims& D, const FkvLayer& L, int u, const uint16_t* __restrict__ q,
+                                         const uint16_t* __restrict__ k_new, const uint16_t* __restrict__ v_new,
+                                         int ordered, int full, uint4* s_page) {
     __shared__ float s_cos[kMaxG];
-    const int u = blockIdx.x, b = u / D.n_kv, m = u % D.n_kv, G = D.G, tid = threadIdx.x;
+    const int b = u / D.n_kv, m = u % D.n_kv, G = D.G, tid = threadIdx.x, nt = blockDim.x;
     // state only before the PDL wait (the previous kernel is the previous layer's attention)
-    const int pv = L.pend_valid[u];
+    const int pv = full ? L.pend_valid[u] : 0;
     if (pv) {
-        for (int i = tid; i < D.K; i += kPreThreads) {
+        for (int i = tid; i < D.K; i += nt) {
             L.res_pages[(size_t)u * D.K + i] = L.pend_pages[(size_t)u * D.K + i];
             L.res_slot[(size_t)u * D.K + i] = L.pend_slot[(size_t)u * D.K + i];
         }
@@ -93,8 +95,9 @@ __global__ void __launch_bounds__(kPreThreads) fkv_pre_kernel(FkvDims D, FkvLaye
     pdl_wait();  // q_i and the new token are this layer's inputs
     pdl_trigger();
     const size_t row0 = ((size_t)b * D.n_qo + m * G) * kHeadDim;
-    for (int i = tid; i < G * (kHeadDim / 8); i += kPreThreads)
-        reinterpret_cast<uint4*>(L.q_cur + row0)[i] = reinterpret_cast<const uint4*>(q + row0)[i];
+    if (full)
+        for (int i = tid; i < G * (kHeadDim / 8); i += nt)
+            reinterpret_cast<uint4*>(L.q_cur + row0)[i] = reinterpret_cast<const uint4*>(q + row0)[i];
     if (tid < G) s_cos[tid] = cos_cfr10(q + row0 + (size_t)tid * kHeadDim, L.q_prev + row0 + (size_t)tid * kHeadDim);
     __syncthreads();
     if (tid == 0) {
@@ -115,11 +118,18 @@ __global__ void __launch_bounds__(kPreThreads) fkv_pre_kernel(FkvDims D, FkvLaye
         }
     }
     append_unit(D, L, u, ctx0, k_new, v_new, 1, s_page);
-    if (tid == 0) {
+    if (full && tid == 0) {
         L.ctx[u] = ctx0 + 1;
         L.n_off[u] = max(L.n_off[u], frontier_for(D, ctx0 + 1));
-        trace_stamp(L.trace, 8, u, 1);
     }
+    if (tid == 0) trace_stamp(L.trace, 8, u, 1);
+}
+
+__global__ void __launch_bounds__(kPreThreads) fkv_pre_kernel(FkvDims D, FkvLayer L, const uint16_t* __restrict__ q,
+                                                              const uint16_t* __restrict__ k_new,
+                                                              const uint16_t* __restrict__ v_new, int ordered) {
+    extern __shared__ __align__(16) uint4 s_page[];  // append staging: one (2, p, d) page
+    pre_unit(D, L, blockIdx.x, q, k_new, v_new, ordered, 1, s_page);
 }
 
 cudaError_t launch_pre(const FkvDims& D, const FkvLayer& L, const uint16_t* q, const uint16_t* k_new,
@@ -136,7 +146,9 @@ cudaError_t launch_pre(const FkvDims& D, const FkvLayer& L, const uint16_t* q, c
 // which the select kernel acquires per unit instead of waiting for the whole grid.
 template <int G, int PPT>
 __global__ void __launch_bounds__(kScThreads) fkv_score_kernel(FkvDims D, FkvLayer L, const uint16_t* __restrict__ q,
-                                                               int items_per_unit, int part) {
+                                                               int items_per_unit, int part,
+                                                               const uint16_t* __restrict__ k_new,
+                                                               const uint16_t* __restrict__ v_new) {
     constexpr int GP = (G + 1) / 2;  // head pairs
     constexpr int kScPPT = PPT, kScWarpPages = ScGeom<PPT>::WarpPages, kScCtaPages = ScGeom<PPT>::CtaPages;
     constexpr int kScStageBytes = ScGeom<PPT>::StageBytes;
@@ -146,18 +158,29 @@ __global__ void __launch_bounds__(kScThreads) fkv_score_kernel(FkvDims D, FkvLay
     __shared__ __align__(8) uint64_t bar[kScWarps][kScStages];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned long long* trace = L.trace;
-    const int item = blockIdx.x;
+    // part -2 (serial step): U extra CTAs first, each the correction check and append of one unit
+    // (the token is pending: the scoring CTAs take the frontier of ctx + 1)
+    const int n_pre = part == -2 ? D.U : 0;
+    if ((int)blockIdx.x < n_pre) {
+        pre_unit(D, L, blockIdx.x, q, k_new, v_new, 0, 0, reinterpret_cast<uint4*>(s_raw));
+        return;
+    }
+    const int item = blockIdx.x - n_pre;
     const int ui = item / items_per_unit, r = item - ui * items_per_unit;
     // part 0 runs on the critical path right after the pre kernel, which writes the unit order
     if (part == 0) pdl_wait();
-    const int u = part_unit(D, L, part, ui);
+    const int u = part_unit(D, L, part == -2 ? -1 : part, ui);
     if (u < 0) return;  // CTA-uniform: no unit at this index in this part
     const int b = u / D.n_kv, m = u % D.n_kv;
-    const int n_off = L.n_off[u];
-    if (r * kScCtaPages >= n_off) return;  // CTA-uniform: no candidate page in this item
+    // the frontier only grows; the pre kernel (possibly this grid's predecessor) may still raise it,
+    // so the summaries issued before the PDL wait are those of the pages below the state's value
+    const int pending = part == -2 ? 1 : 0;
+    const int n_lo = pending ? max(L.n_off[u], frontier_for(D, L.ctx[u] + 1)) : L.n_off[u];
     if (threadIdx.x == 0) trace_stamp(trace, 0, item, 0);
     const int j0 = r * kScCtaPages + warp * kScWarpPages;
-    const bool active = j0 < n_off && j0 + kScWarpPages > D.n_sink;
+    // (with W = 0 the pre kernel's append may complete a page that is a candidate at once: its
+    // summary is written by the predecessor, so nothing is issued before the wait)
+    const bool pre_active = D.n_win >= 1 && j0 < n_lo && j0 + kScWarpPages > D.n_sink;
     uint8_t* ring = s_raw + warp * (kScStages * kScStageBytes);
     auto issue = [&](int slot, int c8) {
         mbar_expect_tx(&bar[warp][slot], kScStageBytes);
@@ -165,16 +188,23 @@ __global__ void __launch_bounds__(kScThreads) fkv_score_kernel(FkvDims D, FkvLay
         bulk_g2s(ring + slot * kScStageBytes + kScStageBytes / 2, L.summ + summ_off(D, u, c8, 1, j0),
                  kScStageBytes / 2, &bar[warp][slot]);
     };
-    if (active && lane == 0) {
+    if (lane == 0) {
 #pragma unroll
         for (int s2 = 0; s2 < kScStages; ++s2) mbar_init(&bar[warp][s2], 1);
         fence_mbar_init();
+        if (pre_active)
 #pragma unroll
-        for (int s2 = 0; s2 < kScStages; ++s2) issue(s2, s2);  // state: before the PDL wait
+            for (int s2 = 0; s2 < kScStages; ++s2) issue(s2, s2);  // state: before the PDL wait
     }
     // q_i is this layer's input: read only after the previous kernel (the previous layer) is done
     pdl_wait();
     pdl_trigger();
+    const int n_off = pending ? n_lo : L.n_off[u];  // final for this step
+    if (r * kScCtaPages >= n_off) return;  // CTA-uniform: no candidate page (nothing was issued)
+    const bool active = j0 < n_off && j0 + kScWarpPages > D.n_sink;
+    if (active && !pre_active && lane == 0)
+#pragma unroll
+        for (int s2 = 0; s2 < kScStages; ++s2) issue(s2, s2);
     // staging: thread (pair hp, channel group c8) loads 16 bytes of each head of the pair
     for (int i = threadIdx.x; i < GP * (kHeadDim / 8); i += blockDim.x) {
         const int hp = i / (kHeadDim / 8), c8 = i % (kHeadDim / 8);
@@ -293,35 +323,39 @@ __global__ void __launch_bounds__(kScThreads) fkv_score_kernel(FkvDims D, FkvLay
 
 template <int G, int PPT>
 static cudaError_t launch_score_gp(const FkvDims& D, const FkvLayer& L, const uint16_t* q, int max_n_off, int part,
-                                   bool pdl, int prio, cudaStream_t s) {
-    constexpr int CP = ScGeom<PPT>::CtaPages, SM = ScGeom<PPT>::Smem;
+                                   bool pdl, int prio, cudaStream_t s, const uint16_t* k_new, const uint16_t* v_new) {
+    constexpr int CP = ScGeom<PPT>::CtaPages;
+    const int SM = std::max<int>(ScGeom<PPT>::Smem, (int)(page_elems(D) * sizeof(uint16_t)));
     const int ipu = std::max(0, (max_n_off + CP - 1) / CP);
-    if (ipu == 0) return cudaSuccess;
+    if (ipu == 0 && part != -2) return cudaSuccess;
     cudaError_t e = func_smem((const void*)fkv_score_kernel<G, PPT>, SM);
     if (e != cudaSuccess) return e;
-    return launch_ex(fkv_score_kernel<G, PPT>, dim3(D.U * ipu), dim3(kScThreads), SM, s, pdl, prio, D, L, q, ipu,
-                     part);
+    const int grid = (part == -2 ? D.U : 0) + D.U * ipu;
+    return launch_ex(fkv_score_kernel<G, PPT>, dim3(grid), dim3(kScThreads), SM, s, pdl, prio, D, L, q,
+                     std::max(ipu, 1), part, k_new, v_new);
 }
 
 template <int G>
 static cudaError_t launch_score_g(const FkvDims& D, const FkvLayer& L, const uint16_t* q, int max_n_off, int part,
-                                  bool pdl, int prio, cudaStream_t s) {
-    if (part == 0) return launch_score_gp<G, 1>(D, L, q, max_n_off, part, pdl, prio, s);
-    return launch_score_gp<G, 4>(D, L, q, max_n_off, part, pdl, prio, s);
+                                  bool pdl, int prio, cudaStream_t s, const uint16_t* k_new, const uint16_t* v_new) {
+    if (part == 0) return launch_score_gp<G, 1>(D, L, q, max_n_off, part, pdl, prio, s, k_new, v_new);
+    if (part < 0 && D.score_ppt == 1) return launch_score_gp<G, 1>(D, L, q, max_n_off, part, pdl, prio, s, k_new, v_new);
+    if (part < 0 && D.score_ppt == 2) return launch_score_gp<G, 2>(D, L, q, max_n_off, part, pdl, prio, s, k_new, v_new);
+    return launch_score_gp<G, 4>(D, L, q, max_n_off, part, pdl, prio, s, k_new, v_new);
 }
 
 cudaError_t launch_score(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q, int max_n_off,
-                         int part, bool pdl, int prio, cudaStream_t s) {
+                         int part, bool pdl, int prio, cudaStream_t s, const uint16_t* k_new, const uint16_t* v_new) {
     (void)X;
     switch (D.G) {
-        case 1: return launch_score_g<1>(D, L, q, max_n_off, part, pdl, prio, s);
-        case 2: return launch_score_g<2>(D, L, q, max_n_off, part, pdl, prio, s);
-        case 3: return launch_score_g<3>(D, L, q, max_n_off, part, pdl, prio, s);
-        case 4: return launch_score_g<4>(D, L, q, max_n_off, part, pdl, prio, s);
-        case 5: return launch_score_g<5>(D, L, q, max_n_off, part, pdl, prio, s);
-        case 6: return launch_score_g<6>(D, L, q, max_n_off, part, pdl, prio, s);
-        case 7: return launch_score_g<7>(D, L, q, max_n_off, part, pdl, prio, s);
-        case 8: return launch_score_g<8>(D, L, q, max_n_off, part, pdl, prio, s);
+        case 1: return launch_score_g<1>(D, L, q, max_n_off, part, pdl, prio, s, k_new, v_new);
+        case 2: return launch_score_g<2>(D, L, q, max_n_off, part, pdl, prio, s, k_new, v_new);
+        case 3: return launch_score_g<3>(D, L, q, max_n_off, part, pdl, prio, s, k_new, v_new);
+        case 4: return launch_score_g<4>(D, L, q, max_n_off, part, pdl, prio, s, k_new, v_new);
+        case 5: return launch_score_g<5>(D, L, q, max_n_off, part, pdl, prio, s, k_new, v_new);
+        case 6: return launch_score_g<6>(D, L, q, max_n_off, part, pdl, prio, s, k_new, v_new);
+        case 7: return launch_score_g<7>(D, L, q, max_n_off, part, pdl, prio, s, k_new, v_new);
+        case 8: return launch_score_g<8>(D, L, q, max_n_off, part, pdl, prio, s, k_new, v_new);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -44,12 +44,12 @@ constexpr int kSelWarps = kSelThreads / 32;
 // part >= 0 (speculative step): the unit of cluster i is part_unit(part, i) -- part 0 the corrected
 // units, part 1 the others; instead of waiting for the whole score grid (PDL), each unit waits for
 // its own score items.
-template <int LPT, int GM, int NC>
-__global__ void __launch_bounds__(kSelThreads, LPT * GM <= 16 ? 4 : 1)
+template <int LPT, int GM, int NC, int NT>
+__global__ void __launch_bounds__(NT, NT == kSelThreads && LPT * GM <= 16 ? 4 : 1)
     fkv_select_kernel(FkvDims D, FkvLayer L, FkvScratch X, const uint16_t* __restrict__ q,
                       int32_t* __restrict__ pages_out, uint8_t* __restrict__ corrected_out, int flag_src,
-                      int list_all, int part) {
-    constexpr int NT = kSelThreads, W = kSelWarps;
+                      int list_all, int part, int pending) {
+    constexpr int W = NT / 32;
     const int rank = NC > 1 ? (int)cg::this_cluster().block_rank() : 0;
     const int u = part_unit(D, L, part, (int)blockIdx.x / NC);
     if (u < 0) return;  // cluster-uniform: no unit at this index in this part
@@ -65,9 +65,12 @@ __global__ void __launch_bounds__(kSelThreads, LPT * GM <= 16 ? 4 : 1)
     int n_res = 0;
     if (leader) n_res = stage_resident<NT>(D, L, u, res_valid, U);
     rank_clear<NT>(S);
+    if (tid == 0) trace_stamp(X.trace, 1, blockIdx.x, 4);
     if constexpr (NC > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-    const int Lc = L.ctx[u];  // published before the scores (pre kernel / append kernel)
-    const int n_off = L.n_off[u];
+    // the context as published before the scores (pre kernel / append kernel), or with the token the
+    // score grid appended (pending)
+    const int Lc = L.ctx[u] + pending;
+    const int n_off = pending ? max(L.n_off[u], frontier_for(D, Lc)) : L.n_off[u];
     const int n_cand = n_off - D.n_sink;
     const bool rank_all = n_cand <= D.K;  // A-11: every candidate selected, no ranking (cluster-uniform)
     if (part >= 0) {  // this unit's score items are written (acquire)
@@ -78,10 +81,12 @@ __global__ void __launch_bounds__(kSelThreads, LPT * GM <= 16 ? 4 : 1)
         }
     } else {
         pdl_wait();  // the scores (previous kernel) are complete; q_i is ready
-        pdl_trigger();
+        if (D.sel_trig == 0) pdl_trigger();
     }
+    if (tid == 0) trace_stamp(X.trace, 1, blockIdx.x, 5);
     if constexpr (NC > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // every CTA started
     __syncthreads();
+    if (tid == 0) trace_stamp(X.trace, 1, blockIdx.x, 6);
     int cnt;
     if (rank_all) {
         if (!leader) return;
@@ -101,7 +106,8 @@ __global__ void __launch_bounds__(kSelThreads, LPT * GM <= 16 ? 4 : 1)
                                                                   : -INFINITY;
             }
         if (tid == 0) trace_stamp(X.trace, 1, blockIdx.x, 1);
-        rank_unit<LPT, GM, NC, NT>(D, rank, n_off, sv, S);
+        rank_unit<LPT, GM, NC, NT>(D, rank, n_off, sv, S, X.trace, blockIdx.x);
+        if (D.sel_trig == 1) pdl_trigger();
         if (!leader) return;
         cnt = D.K;
     }
@@ -138,17 +144,17 @@ __global__ void __launch_bounds__(kSelThreads, LPT * GM <= 16 ? 4 : 1)
     }
 }
 
-template <int LPT, int GM, int NC>
+template <int LPT, int GM, int NC, int NT>
 static cudaError_t launch_sel(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                               int32_t* pages_out, uint8_t* corrected_out, int flag_src, int list_all, int part,
-                              bool pdl, int prio, cudaStream_t s) {
-    auto kern = fkv_select_kernel<LPT, GM, NC>;
+                              bool pdl, int prio, cudaStream_t s, int pending) {
+    auto kern = fkv_select_kernel<LPT, GM, NC, NT>;
     const size_t smem = 0;
     cudaError_t e = func_smem((const void*)kern, smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(D.U * NC);
-    cfg.blockDim = dim3(kSelThreads);
+    cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[3];
@@ -172,26 +178,38 @@ static cudaError_t launch_sel(const FkvDims& D, const FkvLayer& L, const FkvScra
     }
     cfg.attrs = na ? attr : nullptr;
     cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, kern, D, L, X, q, pages_out, corrected_out, flag_src, list_all, part);
+    return cudaLaunchKernelEx(&cfg, kern, D, L, X, q, pages_out, corrected_out, flag_src, list_all, part, pending);
 }
 
-template <int LPT, int NC>
+template <int LPT, int NC, int NT = kSelThreads>
 static cudaError_t launch_sel_g(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                                 int32_t* pages_out, uint8_t* corrected_out, int flag_src, int list_all, int part,
-                                bool pdl, int prio, cudaStream_t s) {
-    if (D.G <= 1) return launch_sel<LPT, 1, NC>(D, L, X, q, pages_out, corrected_out, flag_src, list_all, part, pdl, prio, s);
-    if (D.G <= 2) return launch_sel<LPT, 2, NC>(D, L, X, q, pages_out, corrected_out, flag_src, list_all, part, pdl, prio, s);
-    if (D.G <= 4) return launch_sel<LPT, 4, NC>(D, L, X, q, pages_out, corrected_out, flag_src, list_all, part, pdl, prio, s);
-    return launch_sel<LPT, 8, NC>(D, L, X, q, pages_out, corrected_out, flag_src, list_all, part, pdl, prio, s);
+                                bool pdl, int prio, cudaStream_t s, int pending) {
+    if (D.G <= 1) return launch_sel<LPT, 1, NC, NT>(D, L, X, q, pages_out, corrected_out, flag_src, list_all, part, pdl, prio, s, pending);
+    if (D.G <= 2) return launch_sel<LPT, 2, NC, NT>(D, L, X, q, pages_out, corrected_out, flag_src, list_all, part, pdl, prio, s, pending);
+    if (D.G <= 4) return launch_sel<LPT, 4, NC, NT>(D, L, X, q, pages_out, corrected_out, flag_src, list_all, part, pdl, prio, s, pending);
+    return launch_sel<LPT, 8, NC, NT>(D, L, X, q, pages_out, corrected_out, flag_src, list_all, part, pdl, prio, s, pending);
 }
 
 // nc = CTAs per unit (1, 2, 4, 8), lpt = leaves per thread: nc * 256 * lpt >= next_pow2(n_off) for
 // every n_off the handle can reach (a larger zero-padded tree gives the same Z, CFR-6)
 cudaError_t launch_select(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                           int32_t* pages_out, uint8_t* corrected_out, int flag_src, int list_all, int part,
-                          int nc, int lpt, bool pdl, int prio, cudaStream_t s) {
+                          int nc, int lpt, bool pdl, int prio, cudaStream_t s, int pending, int nt) {
 #define FKV_SEL(LP, N) \
-    return launch_sel_g<LP, N>(D, L, X, q, pages_out, corrected_out, flag_src, list_all, part, pdl, prio, s)
+    return launch_sel_g<LP, N>(D, L, X, q, pages_out, corrected_out, flag_src, list_all, part, pdl, prio, s, pending)
+#define FKV_SELW(LP) \
+    return launch_sel_g<LP, 1, 1024>(D, L, X, q, pages_out, corrected_out, flag_src, list_all, part, pdl, prio, s, \
+                                     pending)
+    if (nc == 1 && nt == 1024) {  // one wide CTA per unit (few, short per-thread chains)
+        switch (lpt) {
+            case 1: FKV_SELW(1);
+            case 2: FKV_SELW(2);
+            case 4: FKV_SELW(4);
+            case 8: FKV_SELW(8);
+            default: return cudaErrorInvalidValue;
+        }
+    }
     if (nc == 1) {
         switch (lpt) {
             case 1: FKV_SEL(1, 1);
@@ -228,6 +246,7 @@ cudaError_t launch_select(const FkvDims& D, const FkvLayer& L, const FkvScratch&
         }
     }
 #undef FKV_SEL
+#undef FKV_SELW
     return cudaErrorInvalidValue;
 }
 

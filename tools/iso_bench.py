@@ -76,12 +76,12 @@ if a.trace:
             continue
         t0 = e[:, 0].min()
         ph = {"ctas": int(len(e)), "start_spread_us": round(float((e[:, 0].max() - t0) / 1e3), 2)}
-        for j in range(1, 5):
+        for j in range(1, 8):
             ok = e[:, j] > 0
             if ok.any():
                 ph[f"med_stamp{j}_us"] = round(float(np.median(e[ok, j] - e[ok, 0]) / 1e3), 2)
                 ph[f"max_stamp{j}_us"] = round(float(np.max(e[ok, j] - t0) / 1e3), 2)
-        if cls == 0 and (e[:, 5] > 0).any():  # FKV_SC_CLK builds: SM cycles between stamps 1 and 2
+        if cls == 0 and False:  # FKV_SC_CLK builds: SM cycles between stamps 1 and 2
             ok = (e[:, 5] > 0) & (e[:, 2] > e[:, 1])
             ph["sm_mhz_in_loop"] = round(float(np.median(e[ok, 5] / ((e[ok, 2] - e[ok, 1]) / 1e3))), 1)
         phases[nm] = ph

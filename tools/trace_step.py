@@ -28,7 +28,7 @@ if GRAPH:
     vb = torch.empty_like(kb)
     ob = torch.empty(L, nb, nq, d, dtype=torch.float32, device=dev)
 names = {0: "score", 1: "select", 2: "recall_sync", 3: "recall_bg", 4: "attn", 5: "attn_phase1", 6: "attn_phase2",
-         7: "merge", 8: "pre", 9: "score_bg", 10: "finalize_bg", 11: "radix_passes"}
+         7: "merge", 8: "pre", 9: "rank_phases", 10: "finalize_bg", 11: "radix_passes"}
 res = {}
 def steps():
     for i in range(12):
