@@ -115,7 +115,7 @@ struct Sizes {
     size_t o_summ, o_sink, o_slots, o_ring, o_qprev, o_res_pages, o_res_slot, o_res_front, o_res_valid, o_res_cnt,
         o_pend_cnt,
         o_pend_pages, o_pend_slot, o_pend_front, o_flags, o_cbar, o_fetch_page, o_fetch_slot, o_n_fetch, o_ctx,
-        o_n_off, o_qcur, o_scores, o_pend_valid, o_order, o_ord_cnt, o_score_done;
+        o_n_off, o_qcur, o_scores, o_pend_valid, o_order, o_ord_cnt, o_score_done, o_pre_done;
     size_t o_part_o, o_part_ml, o_page_rows, o_page_cnt, o_page_valid, o_page_dst, o_ready;
 };
 
@@ -214,6 +214,7 @@ Sizes compute_sizes(const freekv_config* c, const FkvDims& D) {
     s.o_order = take(U * 4);
     s.o_ord_cnt = take(4 * 4);
     s.o_score_done = take(U * 4);
+    s.o_pre_done = take(U * 4);
     s.layer_bytes = o;
     o = 0;
     s.o_part_o = take((size_t)4 * kMaxAttnWarps * D.G * D.d * 4);
@@ -623,6 +624,7 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         L.order = (int32_t*)(base + s.o_order);
         L.ord_cnt = (int32_t*)(base + s.o_ord_cnt);
         L.score_done = (int32_t*)(base + s.o_score_done);
+        L.pre_done = (int32_t*)(base + s.o_pre_done);
         L.host = (uint16_t*)(hd + s.host_layer_bytes * l);
         L.host_row0 = (int)(s.host_layer_bytes * l / (kHeadDim * 2));
         L.arena = (const uint16_t*)dev;
@@ -669,9 +671,9 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         // and a 2-CTA cluster at c2); FREEKV_SELECT_NT=256|1024 overrides
         const char* nte = getenv("FREEKV_SELECT_NT");
         int nt = (nc == 1 && P2 >= 1024 && P2 / 1024 <= 8) ? 1024 : 256;
-        if (nte && (atoi(nte) == 256 || atoi(nte) == 1024)) nt = atoi(nte);
-        if (nt == 1024 && (nc != 1 || P2 < 1024 || P2 / 1024 > 8)) nt = 256;
-        if (nt == 1024) h->sel_lpt = P2 / 1024;
+        if (nte && (atoi(nte) == 256 || atoi(nte) == 512 || atoi(nte) == 1024)) nt = atoi(nte);
+        if (nt > 256 && (nc != 1 || P2 < nt || P2 / nt > 8)) nt = 256;
+        if (nt > 256) h->sel_lpt = P2 / nt;
         h->sel_nt = nt;
         // speculative step: the corrected units' select (few units, critical path) as wide as the tree
         // allows (<= 8 CTAs, >= 256 leaves each); the side chain's select one CTA per unit (clusters
@@ -750,6 +752,8 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         h->D.dbg_order = lo2 ? atoi(lo2) : 0;
         const char* st = getenv("FREEKV_SEL_TRIGGER");
         h->D.sel_trig = st ? atoi(st) : 0;
+        const char* ae = getenv("FREEKV_ATTN_EARLY");
+        h->D.attn_early = ae ? atoi(ae) : 1;
         const char* sp = getenv("FREEKV_SCORE_PPT");
         h->D.score_ppt = sp ? atoi(sp) : 4;
     }

@@ -244,8 +244,13 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 3)
     // slabs are in flight before the wait for the select
     int flag = 0, Lc = 0, pre = 0;
     if (mode == 2) {
-        flag = L.flags[u];
         Lc = L.ctx[u] + pending;
+        if (D.sel_trig < 0) {  // launched beside the score grid: its correction check and append of
+                               // this unit must be complete (acquire)
+            if (tid == 0) spin_until_ge(L.pre_done + u, Lc);
+            __syncthreads();
+        }
+        flag = __ldcg(L.flags + u);
         if (!flag) {
             const ResSrc rsrc = res_src(D, L, u, Lc);
             const int n_pages = rsrc.count();
@@ -263,7 +268,11 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 3)
             }
         }
     }
-    pdl_wait();  // mode 0/2: the select kernel's page lists are complete; mode 1: the pre kernel is done
+    // a unit that is not corrected needs nothing from the select until its commit (R := S_i): with
+    // D.attn_early it attends its whole resident set while the select still runs and waits only
+    // before the commit (the selection leaves the attention's critical path)
+    const bool early = mode == 2 && !flag && D.attn_early;
+    if (!early) pdl_wait();  // mode 0/2: the select kernel's page lists are complete; mode 1: the pre kernel is done
     if (mode != 2) {
         flag = L.flags[u];
         Lc = L.ctx[u];
@@ -347,7 +356,16 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 3)
             });
             const size_t row = (size_t)b * D.n_qo + m * G + e / (kHeadDim / 4);
             reinterpret_cast<float4*>(out + row * kHeadDim)[e % (kHeadDim / 4)] = o4;
-            reinterpret_cast<uint2*>(L.q_prev + row * kHeadDim)[e % (kHeadDim / 4)] = qv[qi];  // q_prev := q_i
+        }
+        // q_prev := q_i -- after the select (and so the score grid, whose correction check reads
+        // q_prev) is complete when this unit attended early
+        if (early) pdl_wait();
+#pragma unroll
+        for (int qi = 0; qi < kQv; ++qi) {
+            const int e = tid + qi * (int)blockDim.x;
+            if (e >= G * (kHeadDim / 4)) break;
+            const size_t row = (size_t)b * D.n_qo + m * G + e / (kHeadDim / 4);
+            reinterpret_cast<uint2*>(L.q_prev + row * kHeadDim)[e % (kHeadDim / 4)] = qv[qi];
         }
         // commit R := S_i: every unit in modes 0 and 2; in mode 1 the corrected units (the
         // others' S_i is committed by the next step's pre kernel, after their background recall)

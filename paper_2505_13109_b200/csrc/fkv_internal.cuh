@@ -32,6 +32,7 @@ struct FkvDims {
     int mode;
     int full_refresh; // diagnostics (env FREEKV_DEBUG_FULL_REFRESH=1): no slot reuse, all pages re-fetched
     int dbg_order;    // A/B (env FREEKV_LAYER_ORDER): bit 0 = every uncorrected unit attends first
+    int attn_early;   // serial step: uncorrected units attend before the wait for the select (FREEKV_ATTN_EARLY)
     int score_ppt;    // pages per thread of the score kernel (parts -1/-2): 1, 2 or 4 (env FREEKV_SCORE_PPT)
     int sel_trig;     // serial step: where the select kernel lets the attention launch (PDL trigger):
                       // 0 at its start, 1 after the ranking, 2 at its end (env FREEKV_SEL_TRIGGER)
@@ -77,6 +78,9 @@ struct FkvLayer {
     int32_t* ord_cnt;     // [2][2]  per step parity (ctx & 1): fill counters of `order` (corrected from the
                           //         front, the others from the back)
     int32_t* score_done;  // [U]     score items of the unit finished this step (release/acquire hand-off)
+    int32_t* pre_done;    // [U]     context length including the token whose correction check and append
+                          //         are complete (release; the attention acquires it when it may start
+                          //         before the score grid has finished, D.sel_trig < 0)
     unsigned long long* trace;  // diagnostics (FREEKV_TRACE=1): %globaltimer stamps, else NULL
     uint16_t* host;       // device-mapped host pool of this layer: [nb][n_page_host][n_kv][2][p][d]
     const uint16_t* arena;  // base of the device arena (row 0 of the attention TMA tensor)

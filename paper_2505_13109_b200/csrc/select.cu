@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(NT, NT == kSelThreads && LPT * GM <= 16 ? 4 : 
     const int n_off = pending ? max(L.n_off[u], frontier_for(D, Lc)) : L.n_off[u];
     const int n_cand = n_off - D.n_sink;
     const bool rank_all = n_cand <= D.K;  // A-11: every candidate selected, no ranking (cluster-uniform)
+    if (part < 0 && D.sel_trig < 0) pdl_trigger();  // the attention may launch beside the scoring
     if (part >= 0) {  // this unit's score items are written (acquire)
         pdl_trigger();
         if (!rank_all && tid == 0) {
@@ -201,6 +202,18 @@ cudaError_t launch_select(const FkvDims& D, const FkvLayer& L, const FkvScratch&
 #define FKV_SELW(LP) \
     return launch_sel_g<LP, 1, 1024>(D, L, X, q, pages_out, corrected_out, flag_src, list_all, part, pdl, prio, s, \
                                      pending)
+#define FKV_SELM(LP) \
+    return launch_sel_g<LP, 1, 512>(D, L, X, q, pages_out, corrected_out, flag_src, list_all, part, pdl, prio, s, \
+                                    pending)
+    if (nc == 1 && nt == 512) {
+        switch (lpt) {
+            case 1: FKV_SELM(1);
+            case 2: FKV_SELM(2);
+            case 4: FKV_SELM(4);
+            case 8: FKV_SELM(8);
+            default: return cudaErrorInvalidValue;
+        }
+    }
     if (nc == 1 && nt == 1024) {  // one wide CTA per unit (few, short per-thread chains)
         switch (lpt) {
             case 1: FKV_SELW(1);
@@ -247,6 +260,7 @@ cudaError_t launch_select(const FkvDims& D, const FkvLayer& L, const FkvScratch&
     }
 #undef FKV_SEL
 #undef FKV_SELW
+#undef FKV_SELM
     return cudaErrorInvalidValue;
 }
 
