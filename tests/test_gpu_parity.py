@@ -286,18 +286,47 @@ FULL_SIZE = {
 }
 
 
-@pytest.mark.parametrize("name", sorted(FULL_SIZE))
-def test_parity_full_size_step_graph(name):
-    """BASELINE.json config sizes (d=128, page 32, budget 2048, S = W = 512) in the launch
-    configuration bench.py times: the whole-step CUDA graph, default kernels.  Two layers
-    (the per-layer path is identical for all of them), every unit compared with the oracle:
-    page indices, frontier and flags bit-exact, outputs within 2e-3.  Step 0 is all-flagged
-    (synchronous full recall), the later steps are speculative with seeded query dips
-    (event rate 0.05 as in the bench)."""
+def _report(rec):
+    """Append one parity record (JSON line) to $FKV_PARITY_REPORT when set (profiles/ evidence)."""
+    import json
+    import os
+    path = os.environ.get("FKV_PARITY_REPORT")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps(rec) + "\n")
+
+
+def elem_rel_err(out, ref):
+    """Elementwise relative error max |o - o_ref| / |o_ref| over the elements with |o_ref| >= 1e-3
+    (reported beside A-21's per-(b, h) inf-norm figure; tiny reference elements are excluded
+    because their relative error is not meaningful for an fp32-accumulated bf16 product)."""
+    m = np.abs(ref) >= 1e-3
+    return float((np.abs(out - ref)[m] / np.abs(ref)[m]).max())
+
+
+def inject_near_ties(k, page, n_sink_pages, every=5):
+    """Tie structure on keys k (bf16 NHD [b][L][kv][d]): for candidate pages j = n_sink+3, +every, ...
+    page j := page j-1 (exact duplicate: equal summaries, an exact pooled-score tie -> the lower id
+    wins, CFR-9), and page j+2 := page j+1 with the lowest mantissa bit of one key element flipped
+    (summaries one bf16 ulp apart in one channel: pooled scores equal or a few fp32 ulp apart)."""
+    n_pages = k.shape[1] // page
+    kb = k.view(torch.int16)
+    for j in range(n_sink_pages + 3, n_pages - 3, every):
+        kb[:, j * page:(j + 1) * page] = kb[:, (j - 1) * page:j * page]
+        kb[:, (j + 2) * page:(j + 3) * page] = kb[:, (j + 1) * page:(j + 2) * page]
+        kb[:, (j + 2) * page, :, 0] ^= 1
+    return k
+
+
+def run_full_size(name, c, n_layers=2, steps=4, gen="S", ties=False, check_fetch=False, seed=250513119):
+    """Full-size parity through the whole-step CUDA graph (the launch configuration bench.py
+    times): every unit of every layer and step vs the oracle -- page indices, frontier, flags (and
+    fetch lists) bit-exact, outputs within 2e-3 (A-21).  gen "S": GEN-S/GEN-Q as in the bench;
+    "X": unstructured i.i.d. keys and queries (alpha = beta = 0, rho = 0: no topic, cosines ~0,
+    every unit corrects every step, full churn)."""
     _need_gpu()
     import paper_2505_13109_b200 as P
-    c = FULL_SIZE[name]
-    nb, n_qo, n_kv, d, p, n_layers, steps = c["nb"], c["n_qo"], c["n_kv"], 128, 32, 2, 4
+    nb, n_qo, n_kv, d, p = c["nb"], c["n_qo"], c["n_kv"], 128, 32
     L0 = c["ctx"] - steps                   # the last step attends over exactly ctx tokens
     kw = dict(n_layers=n_layers, batch=nb, n_qo=n_qo, n_kv=n_kv, head_dim=d, page_size=p, budget_tokens=2048,
               sink_tokens=512, window_tokens=512, max_ctx_tokens=L0 + steps + 2, tau=c["tau"],
@@ -305,25 +334,32 @@ def test_parity_full_size_step_graph(name):
     fkv = P.FreeKV(P.FreeKVConfig(**kw))
     eng = O.OracleEngine(O.OracleConfig(**kw))
     dev = fkv.device
-    seed = 250513119
+    alpha = 0.0 if gen == "X" else synth.ALPHA
     for layer in range(n_layers):
-        k, v = synth.gen_prefill(nb, n_kv, d, p, L0, 512 // p, fkv.K, seed, layer, device=dev)
+        k, v = synth.gen_prefill(nb, n_kv, d, p, L0, 512 // p, fkv.K, seed, layer, device=dev, alpha=alpha)
+        if ties:
+            k = inject_near_ties(k, p, 512 // p)
         torch.cuda.synchronize()
         fkv.append_kv(layer, k, v)
         fkv.synchronize()
         eng.append(layer, synth.bf16_bits(k), synth.bf16_bits(v))
         del k, v
-    qps = [synth.QueryProcess(nb, n_qo, n_kv, d, seed, l, device=dev, event_rate=0.05) for l in range(n_layers)]
+    if gen == "X":
+        qps = [synth.QueryProcess(nb, n_qo, n_kv, d, seed, l, device=dev, beta=0.0, rho=0.0, event_rate=0.0)
+               for l in range(n_layers)]
+    else:
+        qps = [synth.QueryProcess(nb, n_qo, n_kv, d, seed, l, device=dev, event_rate=0.05) for l in range(n_layers)]
     qb = torch.empty(n_layers, nb, n_qo, d, dtype=torch.bfloat16, device=dev)
     kb = torch.empty(n_layers, nb, 1, n_kv, d, dtype=torch.bfloat16, device=dev)
     vb = torch.empty_like(kb)
     ob = torch.empty(n_layers, nb, n_qo, d, dtype=torch.float32, device=dev)
     fkv.step_graph_capture(qb, kb, vb, ob)
-    n_flag = 0
+    n_flag = n_fetch_tot = 0
+    worst = worst_el = 0.0
     for i in range(steps):
         for l in range(n_layers):
             q, _ = qps[l].next()
-            kn, vn = synth.gen_decode_kv(nb, n_kv, d, p, L0 + i, seed, l, device=dev)
+            kn, vn = synth.gen_decode_kv(nb, n_kv, d, p, L0 + i, seed, l, device=dev, alpha=alpha)
             qb[l].copy_(q); kb[l].copy_(kn); vb[l].copy_(vn)
         torch.cuda.synchronize()
         fkv.step_graph_launch()
@@ -334,11 +370,100 @@ def test_parity_full_size_step_graph(name):
             assert np.array_equal(sel["flags"], ref["flags"]), (i, l)
             assert np.array_equal(sel["frontier"], ref["frontier"]), (i, l)
             assert np.array_equal(sel["pages"], ref["sel"]), (i, l)
-            e = rel_err(ob[l].cpu().numpy().astype(np.float64), ref["out"])
+            if check_fetch:
+                n_fetch, fetch_pages = fkv.get_fetch(l)
+                for u in range(fkv.U):
+                    exp = ref["fetch_sync"][u] if ref["flags"][u] else ref["fetch_bg"][u]
+                    assert list(fetch_pages[u, :n_fetch[u]]) == exp, (i, l, u)
+                    n_fetch_tot += len(exp)
+            o = ob[l].cpu().numpy().astype(np.float64)
+            e = rel_err(o, ref["out"])
+            worst = max(worst, e)
+            worst_el = max(worst_el, elem_rel_err(o, ref["out"]))
             assert e <= REL_TOL, (i, l, e)
             if i > 0:
                 n_flag += int(ref["flags"].sum())
-    print(f"{name}: speculative-step correction rate {n_flag / ((steps - 1) * n_layers * nb * n_kv):.3f}")
+    rate = n_flag / max(1, (steps - 1) * n_layers * nb * n_kv)
+    _report({"test": name, "gen": gen, "ties": ties, "layers": n_layers, "steps": steps, "units": fkv.U,
+             "tau": c["tau"], "nb": nb, "correction_rate": round(rate, 4), "fetched_pages": n_fetch_tot,
+             "a21_rel_err_max": worst, "elementwise_rel_err_max": worst_el})
+    fkv.close()
+    return rate
+
+
+@pytest.mark.parametrize("name", sorted(FULL_SIZE))
+def test_parity_full_size_step_graph(name):
+    """BASELINE.json config sizes (d=128, page 32, budget 2048, S = W = 512) in the launch
+    configuration bench.py times: the whole-step CUDA graph, default kernels.  Two layers
+    (the per-layer path is identical for all of them), every unit compared with the oracle:
+    page indices, frontier and flags bit-exact, outputs within 2e-3.  Step 0 is all-flagged
+    (synchronous full recall), the later steps are speculative with seeded query dips
+    (event rate 0.05 as in the bench)."""
+    c = FULL_SIZE[name]
+    rate = run_full_size(name, c)
     if c["tau"] <= 0.8:
-        assert n_flag < (steps - 1) * n_layers * nb * n_kv   # speculative steps did not all correct
+        assert rate < 1.0   # speculative steps did not all correct
+
+
+def test_parity_full_size_deep_c2():
+    """configs[1] (c2) through the step graph for 8 layers x 16 steps, fetch lists included: the
+    delta / slot double-buffering state machine over many speculative steps at full size."""
+    run_full_size("c2_deep", FULL_SIZE["c2"], n_layers=8, steps=16, check_fetch=True)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_parity_full_size_unstructured(name):
+    """GEN-X at c2 / c3 sizes: i.i.d. keys and queries (no hot pages, no topic), so every unit
+    corrects every step and the top-K boundary falls in a dense, nearly flat score region."""
+    rate = run_full_size(name + "_genx", FULL_SIZE[name], n_layers=1, steps=3, gen="X", check_fetch=True)
+    assert rate == 1.0
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_parity_full_size_near_ties(name):
+    """Injected exact and 1-ulp near-duplicate pages at c2 / c3 sizes (CFR-9: equal pooled
+    scores -> lower page id; near-equal ones decided by the canonical fp32 recipe on both sides)."""
+    run_full_size(name + "_ties", FULL_SIZE[name], n_layers=1, steps=3, ties=True, check_fetch=True)
+
+
+@pytest.mark.parametrize("tau", [0.0, 0.8, 0.9, 1.0])
+def test_parity_full_size_c4_batch8_tau(tau):
+    """configs[3] heads and context (32q/8kv, 48K) at batch 8 across the correction threshold:
+    tau = 0 never corrects after bootstrap, tau = 1 corrects every unit every step."""
+    c = dict(FULL_SIZE["c4"], nb=8, tau=tau)
+    rate = run_full_size(f"c4_b8_tau{tau}", c)
+    if tau == 0.0:
+        assert rate == 0.0
+    if tau == 1.0:
+        assert rate == 1.0
+
+
+def test_summarize_pages_matches_oracle():
+    """freekv_summarize_pages rebuilds the channel-wise min/max summaries of offloaded pages from
+    the host pool; bit-exact against the oracle's page summaries, after the append's own
+    summaries were checked (so a rebuild that changed anything would show)."""
+    _need_gpu()
+    import paper_2505_13109_b200 as P
+    G, n_kv, nb, p, L0, n_layers = 4, 2, 2, 32, 3000, 2
+    kw = dict(n_layers=n_layers, batch=nb, n_qo=G * n_kv, n_kv=n_kv, head_dim=128, page_size=p,
+              budget_tokens=256, sink_tokens=64, window_tokens=64, max_ctx_tokens=L0 + 8)
+    fkv = P.FreeKV(P.FreeKVConfig(**kw))
+    eng = O.OracleEngine(O.OracleConfig(**kw))
+    for layer in range(n_layers):
+        k, v = synth.gen_prefill(nb, n_kv, 128, p, L0, 2, fkv.K, 7, layer)
+        eng.append(layer, synth.bf16_bits(k), synth.bf16_bits(v))
+        fkv.append_kv(layer, k.to(fkv.device), v.to(fkv.device))
+    fkv.synchronize()
+    for layer in range(n_layers):
+        n_off = eng.n_off[layer][0]
+        fkv.summarize_pages(layer, 0, n_off)
+        fkv.synchronize()
+        for u in range(fkv.U):
+            got = fkv.get_summaries(layer, u, 2, n_off)
+            assert np.array_equal(got, eng.summ[layer][u, 2:n_off]), (layer, u)
+        # a sub-range rebuild leaves the rest untouched and is again exact
+        fkv.summarize_pages(layer, n_off // 3, n_off // 2)
+        fkv.synchronize()
+        for u in range(fkv.U):
+            assert np.array_equal(fkv.get_summaries(layer, u, 2, n_off), eng.summ[layer][u, 2:n_off])
     fkv.close()
