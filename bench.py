@@ -59,7 +59,24 @@ def parse():
     ap.add_argument("--seed", type=int, default=None)
     ap.add_argument("--tau", type=float, default=None, help="correction threshold (default: the config's)")
     ap.add_argument("--eager", action="store_true", help="per-layer C-ABI calls instead of the whole-step graph")
+    ap.add_argument("--gen", default="S", choices=["S", "spec", "X"],
+                    help="input generator: S = GEN-S/GEN-Q as tuned (alpha 8, beta 6; the headline), spec = the "
+                         "survey's GEN-S parameters (alpha 4, beta 2.5), X = unstructured i.i.d. keys and queries")
+    ap.add_argument("--full-refresh", action="store_true",
+                    help="every unit re-fetches all K pages every step (recall stress; FREEKV_DEBUG_FULL_REFRESH)")
+    ap.add_argument("--n-layers", type=int, default=None, help="override the config's layer count")
+    ap.add_argument("--nested", action="store_true",
+                    help="sub-measurement run: no isolated-kernel, end-to-end, exposed-recall or CPU passes")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the nested survey-spec GEN-S and GEN-X full-refresh lines")
     return ap.parse_args()
+
+
+GEN = {  # (alpha, beta, rho, event_rate or None = the config's)
+    "S": (None, None, None, None),
+    "spec": (4.0, 2.5, None, None),   # SURVEY §8(d) GEN-S as specified
+    "X": (0.0, 0.0, 0.0, 0.0),        # GEN-X: no topic, no persistence -> every unit corrects every step
+}
 
 
 # --------------------------------------------------------------------- clocks
@@ -171,7 +188,20 @@ def run_ours(args, c, rank, world, local_rank):
     b0, b1 = sh.batch_begin, sh.batch_end
     nb_loc = sh.batch
     n_layers = c["n_layers"]
-    total_steps = args.warmup + 1 + args.steps + 2 * args.profile_steps + args.steps  # warm, timed, profiled x2, e2e
+    alpha, beta, rho, ev_rate = GEN[args.gen]
+    gkw = {} if alpha is None else {"alpha": alpha}
+    qkw = {}
+    if beta is not None:
+        qkw["beta"] = beta
+    if rho is not None:
+        qkw["rho"] = rho
+    event_rate = c["event_rate"] if ev_rate is None else ev_rate
+    if args.full_refresh:
+        os.environ["FREEKV_DEBUG_FULL_REFRESH"] = "1"
+    exp_steps = 0 if (args.nested or world > 1) else min(args.steps, 64)
+    # warm, timed, exposed-recall pair, profiled x2, e2e
+    total_steps = args.warmup + 1 + args.steps + 2 * (exp_steps + 2) + 2 * args.profile_steps + \
+        (0 if args.nested else args.steps)
     max_ctx = c["ctx"] + total_steps + 1
     stream = torch.cuda.Stream(dev, priority=-1)  # compute outranks the background recall stream
     t0 = time.time()
@@ -183,14 +213,14 @@ def run_ours(args, c, rank, world, local_rank):
     t0 = time.time()
     with torch.cuda.stream(stream):
         for layer in range(n_layers):
-            k, v = synth.gen_prefill(nb, n_kv, d, p, c["ctx"], c["sink"] // p, K, seed, layer, device=dev)
+            k, v = synth.gen_prefill(nb, n_kv, d, p, c["ctx"], c["sink"] // p, K, seed, layer, device=dev, **gkw)
             fkv.append_kv(layer, k[b0:b1, :, kv0:kv0 + kv_loc].contiguous(),
                           v[b0:b1, :, kv0:kv0 + kv_loc].contiguous())
             del k, v
     stream.synchronize()
     t_prefill = time.time() - t0
     # ---- pre-generate every step's inputs (GEN-Q / GEN-S) outside the timed regions
-    qps = [synth.QueryProcess(nb, n_qo, n_kv, d, seed, layer, device=dev, event_rate=c["event_rate"])
+    qps = [synth.QueryProcess(nb, n_qo, n_kv, d, seed, layer, device=dev, event_rate=event_rate, **qkw)
            for layer in range(n_layers)]
     Qs = torch.empty(total_steps, n_layers, nb_loc, kv_loc * G, d, dtype=torch.bfloat16, device=dev)
     Ks = torch.empty(total_steps, n_layers, nb_loc, 1, kv_loc, d, dtype=torch.bfloat16, device=dev)
@@ -199,7 +229,7 @@ def run_ours(args, c, rank, world, local_rank):
         for i in range(total_steps):
             for layer in range(n_layers):
                 q, _ = qps[layer].next()
-                kn, vn = synth.gen_decode_kv(nb, n_kv, d, p, c["ctx"] + i, seed, layer, device=dev)
+                kn, vn = synth.gen_decode_kv(nb, n_kv, d, p, c["ctx"] + i, seed, layer, device=dev, **gkw)
                 Qs[i, layer] = q[b0:b1, kv0 * G:(kv0 + kv_loc) * G]
                 Ks[i, layer] = kn[b0:b1, :, kv0:kv0 + kv_loc]
                 Vs[i, layer] = vn[b0:b1, :, kv0:kv0 + kv_loc]
@@ -266,6 +296,37 @@ def run_ours(args, c, rank, world, local_rank):
         t = torch.tensor([ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
+    # ---- exposed recall (the background recall should hide behind compute):
+    # the same step graph with and without its background-recall branches, back to back over the
+    # same number of steps.  Without recall the selections (from the summaries) are unchanged but
+    # the next step's resident pages are stale -- a timing-only pass, never a parity or bench value.
+    exposed = None
+    if exp_steps and not args.eager:
+        def timed_steps(n):
+            nonlocal step
+            fkv.step_graph_launch()  # one untimed replay of the freshly captured graph
+            step += 1
+            fkv.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(n):
+                graph_step(step)
+                step += 1
+            b.record(stream)
+            b.synchronize()
+            return a.elapsed_time(b)
+        os.environ["FREEKV_DEBUG_NO_RECALL"] = "1"
+        fkv.step_graph_capture(q_buf, k_buf, v_buf, o_buf)
+        ms_nr = timed_steps(exp_steps)
+        os.environ.pop("FREEKV_DEBUG_NO_RECALL")
+        fkv.step_graph_capture(q_buf, k_buf, v_buf, o_buf)
+        ms_wr = timed_steps(exp_steps)
+        exposed = {"exposed_recall_us_per_layer": round((ms_wr - ms_nr) / exp_steps / n_layers * 1e3, 3),
+                   "us_per_layer_with_recall": round(ms_wr / exp_steps / n_layers * 1e3, 3),
+                   "us_per_layer_without_recall": round(ms_nr / exp_steps / n_layers * 1e3, 3),
+                   "steps": exp_steps,
+                   "method": "step graph with vs without its background-recall branches (FREEKV_DEBUG_NO_RECALL), "
+                             "back to back on the same inputs; selections identical (summaries unchanged)"}
     # ---- profiled passes.  (a) roofline: the step graph re-captured with an event-record
     # node pair around every attention-split kernel only (the dominant kernel; the other
     # kernels keep their PDL edges), so each bracketed interval is that launch's device time
@@ -274,16 +335,19 @@ def run_ours(args, c, rank, world, local_rank):
     # path -- that is the timed region above).  Eager mode: the library's event profiler.
     import paper_2505_13109_b200.freekv as FK
     cls = {k: i for i, k in enumerate(FK.KERNEL_CLASSES)}
-    fetched = flagged = units = t_unit_tokens = j_pages = 0
+    fetched = fetched_sync = flagged = units = t_unit_tokens = j_pages = 0
     t_tok_p1 = t_tok_p2 = units_p1 = 0
 
     def sel_stats():
-        nonlocal fetched, flagged, units, t_unit_tokens, j_pages, t_tok_p1, t_tok_p2, units_p1
+        nonlocal fetched, fetched_sync, flagged, units, t_unit_tokens, j_pages, t_tok_p1, t_tok_p2, units_p1
         for layer in range(n_layers):
             n_fetch, _ = fkv.get_fetch(layer)
             sel = fkv.get_selection(layer)
             fl = sel["flags"].astype(bool)
-            fetched += int(n_fetch.sum())
+            # background recall (rs stream) moves the unflagged units' fetches; a corrected unit's
+            # fetched pages are read from the host pool by the attention kernel itself (direct mode)
+            fetched += int(n_fetch[~fl].sum())
+            fetched_sync += int(n_fetch[fl].sum())
             flagged += int(fl.sum())
             units += fkv.U
             Lc = fkv.context(layer)
@@ -331,7 +395,7 @@ def run_ours(args, c, rank, world, local_rank):
     # on its stream; a device sleep first keeps the host ahead so the events bracket the
     # kernels, not launch gaps
     iso_ms, iso_ms_dirty, iso_score = [], [], None
-    if world == 1:
+    if world == 1 and not args.nested:
         fkv.synchronize()
         flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
         # the write leaves L2 full of dirty lines whose write-back would be charged to the
@@ -371,6 +435,15 @@ def run_ours(args, c, rank, world, local_rank):
             else:
                 iso_ms_dirty = [ea.elapsed_time(eb) for ea, eb in evs]
         del flush, flush_r
+    link = host_link_peak(torch) if rank == 0 else None
+    res = dict(ms=ms, ms_e2e=None, prof=prof, roof_prof=roof_prof, iso_ms=iso_ms, iso_ms_dirty=iso_ms_dirty,
+               iso_score=iso_score, fetched=fetched, fetched_sync=fetched_sync, flagged=flagged, units=units,
+               t_unit_tokens=t_unit_tokens, j_pages=j_pages, t_tok_p1=t_tok_p1, t_tok_p2=t_tok_p2, units_p1=units_p1,
+               clocks=clk, link=link, t_alloc=t_alloc, t_prefill=t_prefill, h2d=0, d2h=0, K=K, G=G, kv_loc=kv_loc,
+               nb_loc=nb_loc, seed=seed, exposed=exposed, n_layers=n_layers)
+    if args.nested:
+        fkv.close()
+        return res
     if not args.eager:  # plain graph again for the end-to-end pass
         fkv.step_graph_capture(q_buf, k_buf, v_buf, o_buf)
     # ---- end-to-end pass: inputs from pinned host memory, outputs back to host, every step
@@ -441,10 +514,7 @@ def run_ours(args, c, rank, world, local_rank):
         t = torch.tensor([ms_e2e], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_e2e = float(t.item())
-    link = host_link_peak(torch) if rank == 0 else None
-    res = dict(ms=ms, ms_e2e=ms_e2e, prof=prof, roof_prof=roof_prof, iso_ms=iso_ms, iso_ms_dirty=iso_ms_dirty, iso_score=iso_score, fetched=fetched, flagged=flagged, units=units,
-               t_unit_tokens=t_unit_tokens, j_pages=j_pages, t_tok_p1=t_tok_p1, t_tok_p2=t_tok_p2, units_p1=units_p1, clocks=clk, link=link, t_alloc=t_alloc,
-               t_prefill=t_prefill, h2d=h2d, d2h=d2h, K=K, G=G, kv_loc=kv_loc, nb_loc=nb_loc, seed=seed)
+    res.update(ms_e2e=ms_e2e, h2d=h2d, d2h=d2h)
     fkv.close()
     return res
 
@@ -488,11 +558,44 @@ def run_oracle_sample(c, seconds, seed):
             "us_per_layer": full_step / c["n_layers"] * 1e6}
 
 
+def spawn_ranks(args):
+    """--gpus N outside torchrun: re-launch this command as N ranks (one per GPU) through
+    torch.distributed.run on 127.0.0.1 and return its exit code; rank 0 prints the line."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def nested_line(args, extra):
+    """One sub-measurement (own process: own handle and pinned pool) -> its parsed JSON line."""
+    cmd = [sys.executable, os.path.abspath(__file__), "--config", args.config, "--nested", "--no-cpu-baseline",
+           "--warmup", "4", "--profile-steps", "4"] + extra
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+        lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+        if out.returncode != 0 or not lines:
+            return {"error": f"rc={out.returncode}: {out.stderr.strip().splitlines()[-1:]}"}
+        return json.loads(lines[-1])
+    except Exception as e:  # noqa: BLE001
+        return {"error": str(e)}
+
+
 def main():
     args = parse()
     c = dict(CONFIGS[args.config])
     if args.tau is not None:
         c["tau"] = args.tau
+    if args.n_layers is not None:
+        c["n_layers"] = args.n_layers
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args))
+    if int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE')}", file=sys.stderr)
+        sys.exit(2)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -519,7 +622,7 @@ def main():
         return
     nb, L = c["batch"], c["n_layers"]
     tok_s = nb * args.steps / (r["ms"] / 1e3)
-    tok_s_e2e = nb * args.steps / (r["ms_e2e"] / 1e3)
+    tok_s_e2e = nb * args.steps / (r["ms_e2e"] / 1e3) if r["ms_e2e"] else None
     import json as _j
     peaks = _j.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
@@ -552,6 +655,8 @@ def main():
         sc_timing = "event-record graph nodes around each score launch inside the step graph"
     sc_bytes = sc_n * (j_per_launch * 2 * d * 2 + units_per_launch * G * d * 2)
     sc_gbs = sc_bytes / (sc_ms / 1e3) / 1e9 if sc_ms > 0 else 0.0
+    # background recall: the unflagged units' fetched pages (the corrected units' fetches are read by
+    # the attention kernel from the host pool in direct mode: recall_direct below)
     rec_ms = prof["recall_bg"][0] + prof["recall_sync"][0]
     rec_bytes = r["fetched"] * 2 * 32 * d * 2
     rec_gbs = rec_bytes / (rec_ms / 1e3) / 1e9 if rec_ms > 0 else 0.0
@@ -610,10 +715,21 @@ def main():
         "recall": {"achieved_gbs": round(rec_gbs, 2), "host_link_peak_gbs": round(r["link"], 2) if r["link"] else None,
                    "frac": round(rec_gbs / r["link"], 4) if r["link"] and rec_gbs else None,
                    "pages_per_layer_step": round(r["fetched"] / max(args.profile_steps * L, 1), 2),
-                   "mechanism": "zero-copy SM gather from the pinned, device-mapped host pool"},
+                   "sync_pages_per_layer_step": round(r["fetched_sync"] / max(args.profile_steps * L, 1), 2),
+                   "mechanism": "background recall kernel: TMA bulk copies (cp.async.bulk) from the pinned, "
+                                "device-mapped host pool into the free slots, on a low-priority stream; bytes = the "
+                                "unflagged units' fetched pages"},
+        "recall_direct": {"pages_per_layer_step": round(r["fetched_sync"] / max(args.profile_steps * L, 1), 2),
+                          "achieved_gbs": round(r["fetched_sync"] * 2 * 32 * d * 2 / (attn_ms / 1e3) / 1e9, 2)
+                          if attn_ms > 0 and r["fetched_sync"] else None,
+                          "host_link_peak_gbs": round(r["link"], 2) if r["link"] else None,
+                          "mechanism": "corrected units' fetched pages read by the attention kernel (2D TMA from the "
+                                       "device-mapped host pool) and written back to their slots; GB/s over the "
+                                       "attention launches' in-step time"},
+        "exposed_recall": r["exposed"],
         "correction_rate": round(r["flagged"] / max(r["units"], 1), 4),
         "kernels": kernels,
-        "e2e": {"value": round(tok_s_e2e, 2), "unit": "tokens/s", "h2d_bytes_per_step": r["h2d"],
+        "e2e": None if tok_s_e2e is None else {"value": round(tok_s_e2e, 2), "unit": "tokens/s", "h2d_bytes_per_step": r["h2d"],
                 "d2h_bytes_per_step": r["d2h"],
                 "note": "public API; per step H2D of q/k/v from pinned memory and D2H of the outputs, "
                         "double-buffered on a copy stream so they overlap the neighbouring steps"},
@@ -623,7 +739,28 @@ def main():
         "clocks": r["clocks"],
         "setup_s": {"alloc_pin": round(r["t_alloc"], 1), "prefill": round(r["t_prefill"], 1)},
     }
-    if not args.no_cpu_baseline and world == 1:
+    if args.gen != "S" or args.full_refresh or args.n_layers is not None:
+        line["data"] = f"synthetic (generator {args.gen}{', full refresh' if args.full_refresh else ''}" \
+                       f"{', %d layers' % L if args.n_layers is not None else ''}; seeded)"
+    if not args.nested and not args.no_extras and world == 1 and not args.eager:
+        # sensitivity lines (own processes): the survey's GEN-S parameters beside the tuned headline,
+        # and the recall stress (GEN-X: every unit corrects; full refresh: all K pages re-fetched)
+        sp = nested_line(args, ["--gen", "spec", "--steps", "64"])
+        line["survey_spec_gen"] = {k: sp.get(k) for k in ("value", "us_per_layer", "correction_rate", "recall",
+                                                            "recall_direct", "error") if k in sp}
+        line["survey_spec_gen"]["generator"] = "GEN-S alpha 4, GEN-Q beta 2.5 (SURVEY §8(d) as specified)"
+        gx = nested_line(args, ["--gen", "X", "--full-refresh", "--n-layers", "4", "--steps", "32"])
+        rd = gx.get("recall_direct") or {}
+        pk = rd.get("host_link_peak_gbs")
+        line["genx_full_refresh_recall"] = {
+            "us_per_layer": gx.get("us_per_layer"), "correction_rate": gx.get("correction_rate"),
+            "pages_per_layer_step": rd.get("pages_per_layer_step"), "achieved_gbs": rd.get("achieved_gbs"),
+            "host_link_peak_gbs": pk,
+            "frac": round(rd["achieved_gbs"] / pk, 4) if rd.get("achieved_gbs") and pk else None,
+            "mechanism": rd.get("mechanism"), "error": gx.get("error"),
+            "workload": "GEN-X keys/queries, FREEKV_DEBUG_FULL_REFRESH (all K pages of every unit from the host "
+                        "pool every step), 4 layers of the config"}
+    if not args.no_cpu_baseline and world == 1 and not args.nested:
         line["cpu_baseline"] = run_oracle_sample(c, args.cpu_sample_s, r["seed"])
     print(json.dumps(line))
 

@@ -90,6 +90,9 @@ struct freekv_handle {
     std::vector<int> recall_pending;
     bool pdl = true;                    // programmatic dependent launch (FREEKV_PDL=0 disables)
     bool serial_recall = false;  // f2 ablation: FREEKV_SERIAL_RECALL=1 runs background recall on the compute stream
+    bool no_bg_recall = false;   // measurement only (FREEKV_DEBUG_NO_RECALL=1, read per capture / call): skip the
+                                 // background recall -- selections unchanged, the next step's resident pages stale
+                                 // (bench.py exposed_recall_us: step time with minus without)
     // profiling (freekv_profile_begin/end)
     bool prof = false;
     uint32_t prof_mask = ~0u;  // kernel classes bracketed by events while profiling
@@ -272,6 +275,11 @@ freekv_status do_append(freekv_handle* h, int layer, const void* k, const void* 
 // Rows a2-a4 on stream s (primitive API and the serial decode step): page scoring, then the
 // select kernel.  flag_src 1: the pre kernel decided the correction flags; list_all: page lists of
 // every unit for the attention.
+static bool env_on(const char* name) {
+    const char* v = getenv(name);
+    return v && v[0] == '1';
+}
+
 freekv_status do_select(freekv_handle* h, int layer, const void* q, int32_t* pages_out, uint8_t* corr_out,
                         cudaStream_t s, int flag_src, int list_all, const void* k_new = nullptr,
                         const void* v_new = nullptr) {
@@ -368,7 +376,8 @@ freekv_status do_step_tail(freekv_handle* h, int layer, const void* q, float* ou
         } else {  // forked branch (graph capture: joined at the graph's end)
             FKV_CUDA(cudaEventRecord(h->ev_select[layer], cs));
             FKV_CUDA(cudaStreamWaitEvent(h->rs, h->ev_select[layer], 0));
-            FKV_CUDA(timed(h, K_RECALL_BG, h->rs, [&] { return launch_recall(D, L, 0, h->rs, h->X.trace); }));
+            if (!h->no_bg_recall)
+                FKV_CUDA(timed(h, K_RECALL_BG, h->rs, [&] { return launch_recall(D, L, 0, h->rs, h->X.trace); }));
             FKV_CUDA(cudaEventRecord(h->ev_recall[layer], h->rs));
             if (!h->capturing) h->recall_pending[layer] = 1;
         }
@@ -856,6 +865,7 @@ freekv_status freekv_decode_step(freekv_handle* h, int32_t layer, const void* q,
     if (st != FREEKV_OK) return st;
     if (!k_new || !v_new) return fail(FREEKV_EINVAL, "k_new/v_new is NULL");
     if (h->ctx_host[layer] + 1 > h->D.max_ctx) return fail(FREEKV_ERANGE, "context would exceed max_ctx_tokens");
+    h->no_bg_recall = env_on("FREEKV_DEBUG_NO_RECALL");
     return do_layer_step(h, layer, q, k_new, v_new, out);
 }
 
@@ -995,6 +1005,7 @@ freekv_status freekv_step_graph_capture(freekv_handle* h, const void* q_all, con
     if (!h) return fail(FREEKV_EINVAL, "handle is NULL");
     if (!q_all || !k_all || !v_all || !out_all) return fail(FREEKV_EINVAL, "NULL buffer");
     if (h->prof) return fail(FREEKV_ESTATE, "capture while profiling");
+    h->no_bg_recall = env_on("FREEKV_DEBUG_NO_RECALL");
     h->graph_recs.clear();
     if (profile) {  // event pool: <= 8 kernels per layer, 2 events each
         freekv_status ps = freekv_profile_begin(h, h->cfg.n_layers * 8 + 8);
