@@ -19,7 +19,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
                 "-I" + os.path.join(HERE, "..", "include")] + VARIANT_DEFS
 
-SOURCES = ["api.cu", "append.cu", "score.cu", "select.cu", "recall.cu", "attn.cu", "layer.cu"]
+SOURCES = ["api.cu", "append.cu", "score.cu", "select.cu", "recall.cu", "attn.cu"]
 HEADERS = ["fkv_internal.cuh", "append_unit.cuh", "attn_core.cuh", "select_core.cuh"]
 
 

@@ -76,8 +76,6 @@ struct freekv_handle {
     std::vector<cudaEvent_t> ev_select, ev_recall, ev_sync, ev_sync_x;
     bool one_graph = false;      // direct mode: recalls are forked branches of the one step graph
     bool spec = false;           // speculative decode step: attention beside the side chain (attn.cu mode 1)
-    bool fused = false;          // fused decode step: one cluster kernel per layer (layer.cu), the default
-    int ly_c = 0, ly_lpt = 0;    // its CTAs per unit and pages (tree leaves) per thread
     std::vector<cudaStream_t> side;  // side streams of the speculative step (score -> select -> recall)
     std::vector<cudaEvent_t> ev_pre;  // fork point of each layer's side chain (after its pre kernel)
     int prio_hi = 0;             // kernel priority of the critical path (pre, attention)
@@ -118,7 +116,7 @@ struct Sizes {
     size_t o_summ, o_sink, o_slots, o_ring, o_qprev, o_res_pages, o_res_slot, o_res_front, o_res_valid, o_res_cnt,
         o_pend_cnt,
         o_pend_pages, o_pend_slot, o_pend_front, o_flags, o_cbar, o_fetch_page, o_fetch_slot, o_n_fetch, o_ctx,
-        o_n_off, o_qcur, o_scores, o_pend_valid, o_order, o_ord_cnt, o_score_done, o_pre_done;
+        o_n_off, o_qcur, o_scores, o_pend_valid, o_order, o_ord_cnt, o_score_done;
     size_t o_part_o, o_part_ml, o_page_rows, o_page_cnt, o_page_valid, o_page_dst, o_ready;
 };
 
@@ -217,7 +215,6 @@ Sizes compute_sizes(const freekv_config* c, const FkvDims& D) {
     s.o_order = take(U * 4);
     s.o_ord_cnt = take(4 * 4);
     s.o_score_done = take(U * 4);
-    s.o_pre_done = take(U * 4);
     s.layer_bytes = o;
     o = 0;
     s.o_part_o = take((size_t)4 * kMaxAttnWarps * D.G * D.d * 4);
@@ -435,24 +432,6 @@ freekv_status do_layer_step(freekv_handle* h, int layer, const void* q, const vo
     if (!q || !out) return fail(FREEKV_EINVAL, "q/out is NULL");
     // the previous step's side chain / recall of this layer (its selection, its slots)
     if (!h->capturing && h->recall_pending[layer]) FKV_CUDA(cudaStreamWaitEvent(cs, h->ev_recall[layer], 0));
-    if (h->fused) {  // the whole layer step in one launch, then the background recall (rs)
-        FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] {
-            return launch_layer(D, L, h->X, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new, out,
-                                h->tmap_kv, h->tmap_host, h->ly_c, h->ly_lpt, h->pdl, cs);
-        }));
-        if (!h->capturing) h->ctx_host[layer] += 1;
-        if (h->serial_recall) {  // f2 ablation: no overlap
-            FKV_CUDA(timed(h, K_RECALL_BG, cs, [&] { return launch_recall(D, L, 0, cs, h->X.trace); }));
-            FKV_CUDA(cudaEventRecord(h->ev_recall[layer], cs));
-        } else {
-            FKV_CUDA(cudaEventRecord(h->ev_select[layer], cs));
-            FKV_CUDA(cudaStreamWaitEvent(h->rs, h->ev_select[layer], 0));
-            FKV_CUDA(timed(h, K_RECALL_BG, h->rs, [&] { return launch_recall(D, L, 0, h->rs, h->X.trace); }));
-            FKV_CUDA(cudaEventRecord(h->ev_recall[layer], h->rs));
-        }
-        if (!h->capturing) h->recall_pending[layer] = 1;
-        return FREEKV_OK;
-    }
     if (!h->spec && D.direct && D.n_win >= 1) {
         // serial step, three launches: score grid (+ correction check and append per unit, the token
         // pending) -> select (every unit's page list) -> attention (mode 2; its commit publishes the
@@ -633,7 +612,6 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         L.order = (int32_t*)(base + s.o_order);
         L.ord_cnt = (int32_t*)(base + s.o_ord_cnt);
         L.score_done = (int32_t*)(base + s.o_score_done);
-        L.pre_done = (int32_t*)(base + s.o_pre_done);
         L.host = (uint16_t*)(hd + s.host_layer_bytes * l);
         L.host_row0 = (int)(s.host_layer_bytes * l / (kHeadDim * 2));
         L.arena = (const uint16_t*)dev;
@@ -705,22 +683,12 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         h->one_graph = h->D.direct;  // recalls are forked branches of the one step graph
         const char* pd = getenv("FREEKV_PDL");
         h->pdl = !(pd && pd[0] == '0');
-        // step mode (FREEKV_STEP): fused (default: one kernel per layer, layer.cu), spec (pre kernel,
-        // attention beside the scoring/selection streams), serial (pre, score, select, attention)
+        // step mode (FREEKV_STEP): serial (default: score grid with the append / correction CTAs,
+        // select, attention), spec (the paper's overlap structure: pre kernel, attention beside the
+        // scoring / selection side streams; measured slower on B200)
         const char* ov = getenv("FREEKV_STEP");
         const std::string mode = ov ? ov : "serial";
         h->spec = h->D.direct && mode == "spec";
-        if (h->D.direct && mode == "fused") {
-            int c = 8;
-            while (c > 2 && D.U * c > 2 * sms) c >>= 1;
-            int lpt = 1;
-            while (c * 128 * lpt < P2) lpt <<= 1;
-            if (layer_supported(h->D, c, lpt)) {
-                h->fused = true;
-                h->ly_c = c;
-                h->ly_lpt = lpt;
-            }
-        }
     }
     {
         int warps = 0;
@@ -757,10 +725,6 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
     {
         const char* fr = getenv("FREEKV_DEBUG_FULL_REFRESH");
         h->D.full_refresh = (fr && fr[0] == '1') ? 1 : 0;
-        const char* lo2 = getenv("FREEKV_LAYER_ORDER");
-        h->D.dbg_order = lo2 ? atoi(lo2) : 0;
-        const char* st = getenv("FREEKV_SEL_TRIGGER");
-        h->D.sel_trig = st ? atoi(st) : 0;
         const char* ae = getenv("FREEKV_ATTN_EARLY");
         h->D.attn_early = ae ? atoi(ae) : 1;
         const char* sp = getenv("FREEKV_SCORE_PPT");

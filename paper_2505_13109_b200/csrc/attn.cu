@@ -245,11 +245,6 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 3)
     int flag = 0, Lc = 0, pre = 0;
     if (mode == 2) {
         Lc = L.ctx[u] + pending;
-        if (D.sel_trig < 0) {  // launched beside the score grid: its correction check and append of
-                               // this unit must be complete (acquire)
-            if (tid == 0) spin_until_ge(L.pre_done + u, Lc);
-            __syncthreads();
-        }
         flag = __ldcg(L.flags + u);
         if (!flag) {
             const ResSrc rsrc = res_src(D, L, u, Lc);

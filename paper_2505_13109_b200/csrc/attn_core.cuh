@@ -1,6 +1,5 @@
-// attn_core.cuh -- row a7 building blocks shared by the attention kernels (attn.cu) and the
-// fused layer kernel (layer.cu): TMA slab staging of head-major (2, p, d) pages, the per-slab
-// online-softmax step on mma.sync micro-tiles (S^T = K Q^T, O^T += V^T P^T), page-list sources
+// attn_core.cuh -- row a7 building blocks of the attention kernels (attn.cu): TMA slab staging
+// of head-major (2, p, d) pages, the per-slab online-softmax step on mma.sync micro-tiles (S^T = K Q^T, O^T += V^T P^T), page-list sources
 // and the per-warp page loop.  PAPER.md P:95-97 (sparse decode attention over the selected pages).
 #pragma once
 #include "fkv_internal.cuh"

@@ -31,11 +31,8 @@ struct FkvDims {
     int U;            // nb * n_kv
     int mode;
     int full_refresh; // diagnostics (env FREEKV_DEBUG_FULL_REFRESH=1): no slot reuse, all pages re-fetched
-    int dbg_order;    // A/B (env FREEKV_LAYER_ORDER): bit 0 = every uncorrected unit attends first
     int attn_early;   // serial step: uncorrected units attend before the wait for the select (FREEKV_ATTN_EARLY)
     int score_ppt;    // pages per thread of the score kernel (parts -1/-2): 1, 2 or 4 (env FREEKV_SCORE_PPT)
-    int sel_trig;     // serial step: where the select kernel lets the attention launch (PDL trigger):
-                      // 0 at its start, 1 after the ranking, 2 at its end (env FREEKV_SEL_TRIGGER)
     int pool;         // FREEKV_POOL_* group pooling of the selection (f3); 0 = MeanS
     int corr_pool;    // 0 = mean of the cosines, 1 = corrected when the least similar head is below tau
     float tau;
@@ -78,9 +75,6 @@ struct FkvLayer {
     int32_t* ord_cnt;     // [2][2]  per step parity (ctx & 1): fill counters of `order` (corrected from the
                           //         front, the others from the back)
     int32_t* score_done;  // [U]     score items of the unit finished this step (release/acquire hand-off)
-    int32_t* pre_done;    // [U]     context length including the token whose correction check and append
-                          //         are complete (release; the attention acquires it when it may start
-                          //         before the score grid has finished, D.sel_trig < 0)
     unsigned long long* trace;  // diagnostics (FREEKV_TRACE=1): %globaltimer stamps, else NULL
     uint16_t* host;       // device-mapped host pool of this layer: [nb][n_page_host][n_kv][2][p][d]
     const uint16_t* arena;  // base of the device arena (row 0 of the attention TMA tensor)
@@ -319,15 +313,10 @@ cudaError_t launch_attn_split(const FkvDims& D, const FkvLayer& L, const FkvScra
                               int phase, const CUtensorMap& tmap, const CUtensorMap& tmap_host,
                               const uint16_t* arena, bool pdl, cudaStream_t s);
 // mode 0: page lists of every unit from the select kernel (waits for it), commits every unit;
-// mode 1: speculative decode step (see attn.cu)
+// mode 1: speculative decode step (FREEKV_STEP=spec); mode 2: serial decode step (see attn.cu)
 cudaError_t launch_attn_cluster(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                                 float* out, const CUtensorMap& tmap, const CUtensorMap& tmap_h, int mode, int c,
                                 bool pdl, int prio, cudaStream_t s, int pending = 0);
 cudaError_t launch_attn_combine(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                                 float* out, int split, int commit, bool pdl, cudaStream_t s);
-// the fused decode step of one layer (layer.cu): c CTAs per unit, lpt pages per thread
-bool layer_supported(const FkvDims& D, int c, int lpt);
-cudaError_t launch_layer(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
-                         const uint16_t* k_new, const uint16_t* v_new, float* out, const CUtensorMap& tmap,
-                         const CUtensorMap& tmap_h, int c, int lpt, bool pdl, cudaStream_t s);
 }  // namespace fkv

@@ -118,8 +118,6 @@ __device__ __forceinline__ void pre_unit(const FkvDims& D, const FkvLayer& L, in
         }
     }
     append_unit(D, L, u, ctx0, k_new, v_new, 1, s_page);
-    __syncthreads();  // every thread's flag / page / summary writes before thread 0's release
-    if (tid == 0) st_release(L.pre_done + u, ctx0 + 1);
     if (full && tid == 0) {
         L.ctx[u] = ctx0 + 1;
         L.n_off[u] = max(L.n_off[u], frontier_for(D, ctx0 + 1));

@@ -73,7 +73,6 @@ __global__ void __launch_bounds__(NT, NT == kSelThreads && LPT * GM <= 16 ? 4 : 
     const int n_off = pending ? max(L.n_off[u], frontier_for(D, Lc)) : L.n_off[u];
     const int n_cand = n_off - D.n_sink;
     const bool rank_all = n_cand <= D.K;  // A-11: every candidate selected, no ranking (cluster-uniform)
-    if (part < 0 && D.sel_trig < 0) pdl_trigger();  // the attention may launch beside the scoring
     if (part >= 0) {  // this unit's score items are written (acquire)
         pdl_trigger();
         if (!rank_all && tid == 0) {
@@ -82,7 +81,7 @@ __global__ void __launch_bounds__(NT, NT == kSelThreads && LPT * GM <= 16 ? 4 : 
         }
     } else {
         pdl_wait();  // the scores (previous kernel) are complete; q_i is ready
-        if (D.sel_trig == 0) pdl_trigger();
+        pdl_trigger();
     }
     if (tid == 0) trace_stamp(X.trace, 1, blockIdx.x, 5);
     if constexpr (NC > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // every CTA started
@@ -108,7 +107,6 @@ __global__ void __launch_bounds__(NT, NT == kSelThreads && LPT * GM <= 16 ? 4 : 
             }
         if (tid == 0) trace_stamp(X.trace, 1, blockIdx.x, 1);
         rank_unit<LPT, GM, NC, NT>(D, rank, n_off, sv, S, X.trace, blockIdx.x);
-        if (D.sel_trig == 1) pdl_trigger();
         if (!leader) return;
         cnt = D.K;
     }

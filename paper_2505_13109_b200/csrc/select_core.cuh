@@ -1,5 +1,4 @@
-// select_core.cuh -- rows a3 / a4 as device functions, shared by the standalone select kernel
-// (select.cu) and the fused layer kernel (layer.cu):
+// select_core.cuh -- rows a3 / a4 as device functions of the select kernel (select.cu):
 //
 //   rank_unit    a3 + a4: per-head softmax over the candidate pages (CFR-4..7), group pooling
 //                (MeanS / MaxS, CFR-8; the QK variants pooled before), top-K with lowest-id ties

@@ -149,13 +149,14 @@ def test_parity_long_context_many_tiles():
     run_parity(G=4, n_kv=1, batch=1, page=16, sink=64, window=64, budget=640, L0=20000, steps=3, n_layers=1)
 
 
-@pytest.mark.parametrize("overlap", ["0", "1"])
-def test_step_graph_matches_eager(overlap, monkeypatch):
+@pytest.mark.parametrize("step_mode", ["serial", "spec"])
+def test_step_graph_matches_eager(step_mode, monkeypatch):
     """Whole-step CUDA graphs (one graph with forked recall branches) give the same selections and
-    bit-identical outputs as the eager per-layer calls, with the attention overlapping the select
-    (default) and waiting for it (FREEKV_OVERLAP=0)."""
+    bit-identical outputs as the eager per-layer calls, for the serial step (default: score grid,
+    select, attention) and the paper-structure speculative step (FREEKV_STEP=spec: attention beside
+    the scoring / selection side streams)."""
     _need_gpu()
-    monkeypatch.setenv("FREEKV_OVERLAP", overlap)
+    monkeypatch.setenv("FREEKV_STEP", step_mode)
     import paper_2505_13109_b200 as P
     nb, n_kv, G, d, p, L0, steps, n_layers = 2, 2, 4, 128, 32, 1200, 6, 3
     n_qo = G * n_kv
@@ -233,9 +234,27 @@ def test_parity_select_cluster_widths(nc, monkeypatch):
                tie_pages=True, event_rate=0.0)
 
 
-def test_parity_overlap_off(monkeypatch):
-    """FREEKV_OVERLAP=0: the attention waits for the whole select (page lists of every unit)."""
-    monkeypatch.setenv("FREEKV_OVERLAP", "0")
+def test_parity_step_spec(monkeypatch):
+    """FREEKV_STEP=spec (the paper's overlap structure): pre kernel, then the attention of the units
+    that pass the correction check beside the corrected units' scoring / selection (high-priority
+    stream) and the others' (side stream, committed by the next step's pre kernel)."""
+    monkeypatch.setenv("FREEKV_STEP", "spec")
+    run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=5)
+
+
+@pytest.mark.parametrize("nt", ["256", "512", "1024"])
+def test_parity_select_cta_widths(nt, monkeypatch):
+    """One select CTA per unit at 256 / 512 / 1024 threads (the CFR-6 tree over more or fewer
+    leaves per thread): bit-identical selections."""
+    monkeypatch.setenv("FREEKV_SELECT_NC", "1")
+    monkeypatch.setenv("FREEKV_SELECT_NT", nt)
+    run_parity(G=4, n_kv=2, batch=2, page=32, L0=40000, steps=3, n_layers=1)
+
+
+def test_parity_attention_waits_for_select(monkeypatch):
+    """FREEKV_ATTN_EARLY=0: every unit's attention waits for the select (no early attention of the
+    units that pass the correction check)."""
+    monkeypatch.setenv("FREEKV_ATTN_EARLY", "0")
     run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=5)
 
 
@@ -262,11 +281,11 @@ def test_parity_pooling_variants(pool):
                pool=pool)
 
 
-@pytest.mark.parametrize("overlap", ["0", "1"])
-def test_parity_max_pooled_correction(overlap, monkeypatch):
+@pytest.mark.parametrize("step_mode", ["serial", "spec"])
+def test_parity_max_pooled_correction(step_mode, monkeypatch):
     """Max-pooled correction (tab:abl-g-corr, reading R-11): corrected when any head's similarity
     is below tau; more units corrected than with mean pooling on the same inputs."""
-    monkeypatch.setenv("FREEKV_OVERLAP", overlap)
+    monkeypatch.setenv("FREEKV_STEP", step_mode)
     nf_max, _, _ = run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=5, corr_pool=1, event_rate=0.3)
     nf_mean, _, _ = run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=5, corr_pool=0, event_rate=0.3)
     assert nf_max >= nf_mean

@@ -15,7 +15,6 @@ FR="--layers 4 --steps 6 --warmup 3"
 run "HL page 16KiB"      "FREEKV_CORR=recall FREEKV_DEBUG_FULL_REFRESH=1" "$FR"
 run "HL frag 4KiB"       "FREEKV_CORR=recall FREEKV_DEBUG_FULL_REFRESH=1 FREEKV_RECALL_FRAG=4096" "$FR"
 run "HL frag 256B (NHD)" "FREEKV_CORR=recall FREEKV_DEBUG_FULL_REFRESH=1 FREEKV_RECALL_FRAG=256" "$FR"
-run "HL SM loads"        "FREEKV_CORR=recall FREEKV_DEBUG_FULL_REFRESH=1 FREEKV_RECALL_MODE=ld" "$FR"
 ST="--layers 32 --steps 10 --warmup 5"
 for r in 1 2; do
 run "SR speculative (default)" "BASE=1" "$ST"
