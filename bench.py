@@ -234,16 +234,27 @@ def run_ours(args, c, rank, world, local_rank):
                 Ks[i, layer] = kn[b0:b1, :, kv0:kv0 + kv_loc]
                 Vs[i, layer] = vn[b0:b1, :, kv0:kv0 + kv_loc]
     out_loc = [torch.empty(nb_loc, kv_loc * G, d, dtype=torch.float32, device=dev) for _ in range(n_layers)]
-    out_full = [torch.empty(world, nb_loc, kv_loc * G, d, dtype=torch.float32, device=dev) for _ in range(n_layers)] \
-        if world > 1 else None
+    comm_info = None
+    if world > 1:
+        # the library's own NCCL communicator (id from rank 0, broadcast over the torch process
+        # group); every layer's step then ends with its all-gather of the head outputs on the
+        # compute stream, inside the step graph (the one exchange step)
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.tensor(list(P.FreeKV.comm_unique_id()), dtype=torch.uint8))
+        torch.distributed.broadcast(uid, 0)
+        fkv.comm_init(bytes(uid.cpu().tolist()), world, rank)
+        gather_all = torch.empty(n_layers, world, nb_loc, kv_loc * G, d, dtype=torch.float32, device=dev)
+        fkv.set_gather_output(gather_all)
+        comm_info = {"ranks": world, "collective": "ncclAllGather per layer (library communicator, in the step graph)",
+                     "bytes_per_layer_per_rank": nb_loc * kv_loc * G * d * 4}
+        print(f"[rank {rank}/{world}] freekv NCCL communicator ready: kv heads [{kv0}, {kv0 + kv_loc}) x batch "
+              f"[{b0}, {b1}), all-gather {comm_info['bytes_per_layer_per_rank']} B per layer", file=sys.stderr)
     stream.synchronize()
 
     def one_step(i):
         for layer in range(n_layers):
             fkv.decode_step(layer, Qs[i, layer], Ks[i, layer], Vs[i, layer], out_loc[layer])
-            if world > 1:
-                with torch.cuda.stream(stream):
-                    torch.distributed.all_gather_into_tensor(out_full[layer], out_loc[layer])
 
     # whole-step graph: fixed input/output buffers, one replay per step
     q_buf, k_buf, v_buf = torch.empty_like(Qs[0]), torch.empty_like(Ks[0]), torch.empty_like(Vs[0])
@@ -255,10 +266,6 @@ def run_ours(args, c, rank, world, local_rank):
             k_buf.copy_(Ks[i], non_blocking=True)
             v_buf.copy_(Vs[i], non_blocking=True)
         fkv.step_graph_launch()
-        if world > 1:
-            with torch.cuda.stream(stream):
-                for layer in range(n_layers):
-                    torch.distributed.all_gather_into_tensor(out_full[layer], o_buf[layer])
 
     def barrier():
         if world > 1:
@@ -440,7 +447,7 @@ def run_ours(args, c, rank, world, local_rank):
                iso_score=iso_score, fetched=fetched, fetched_sync=fetched_sync, flagged=flagged, units=units,
                t_unit_tokens=t_unit_tokens, j_pages=j_pages, t_tok_p1=t_tok_p1, t_tok_p2=t_tok_p2, units_p1=units_p1,
                clocks=clk, link=link, t_alloc=t_alloc, t_prefill=t_prefill, h2d=0, d2h=0, K=K, G=G, kv_loc=kv_loc,
-               nb_loc=nb_loc, seed=seed, exposed=exposed, n_layers=n_layers)
+               nb_loc=nb_loc, seed=seed, exposed=exposed, n_layers=n_layers, comm=comm_info)
     if args.nested:
         fkv.close()
         return res
@@ -737,6 +744,7 @@ def main():
         "gpu_launches_per_step": int(sum(v[1] for v in prof.values()) / max(args.profile_steps, 1)),
         "execution": "eager per-layer C-ABI calls" if args.eager else "whole-step CUDA graphs (compute + recall)",
         "clocks": r["clocks"],
+        "comm": r["comm"],
         "setup_s": {"alloc_pin": round(r["t_alloc"], 1), "prefill": round(r["t_prefill"], 1)},
     }
     if args.gen != "S" or args.full_refresh or args.n_layers is not None:

@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define FREEKV_ABI_VERSION 2
+#define FREEKV_ABI_VERSION 3
 
 typedef int32_t freekv_status;
 enum {
@@ -41,7 +41,7 @@ enum {
     FREEKV_EINVAL = -1,        /* invalid argument / violated config invariant */
     FREEKV_ENOMEM = -2,        /* buffer smaller than freekv_query_sizes() */
     FREEKV_ECUDA = -3,         /* CUDA runtime error (possibly from earlier async work) */
-    FREEKV_ENCCL = -4,         /* reserved: collective failure */
+    FREEKV_ENCCL = -4,         /* NCCL (communicator / collective) failure */
     FREEKV_ESTATE = -5,        /* call out of order / handle in wrong state */
     FREEKV_ERANGE = -6,        /* context would exceed max_ctx_tokens */
     FREEKV_EUNSUPPORTED = -7   /* head_dim != 128, page_size not in {16,32,64}, G > 8, batch*n_kv > 4096 */
@@ -64,7 +64,9 @@ typedef struct freekv_config {
     int32_t max_ctx_tokens;  /* capacity of the host pool per sequence */
     float tau;               /* correction threshold */
     int32_t mode;            /* FREEKV_MODE_* */
-    int32_t first_layer_dense; /* must be 0 in ABI v1 (P:560 layer-0 exemption is served outside) */
+    int32_t first_layer_dense; /* 1: layer 0 is not compressed (O-7): every page stays resident
+                                  in a dense device pool and its attention (decode_step,
+                                  sparse_decode_attn) covers all Lc tokens; no selection or recall */
     /* multi-GPU shard description; informational in ABI v1 */
     int32_t kv_head_begin, kv_head_end, batch_begin, batch_end;
     int32_t n_ranks, rank;
@@ -131,8 +133,13 @@ freekv_status freekv_select_pages(freekv_handle* h, int32_t layer, const void* q
  * resident, reading A-18) from the host pool into free cache slots.  Units
  * whose correction flag is set are recalled synchronously on `stream` (before
  * attention); the others are recalled in the background on the recall
- * stream for use at the next step.  sync_mask must be NULL
- * in ABI v1 (the flags of select_pages are used). */
+ * stream for use at the next step.  sync_mask (device uint8
+ * [nb][n_kv], nullable): the units to recall synchronously instead of the
+ * correction flags (copied on `stream`; the caller's buffer may be reused at
+ * once).  In direct mode (default) any mask gives the same results -- a
+ * corrected unit's attention reads its missing pages from the host pool if
+ * they are not resident yet; in the paper-order recall mode (FREEKV_CORR=recall)
+ * the mask must include every corrected unit. */
 freekv_status freekv_recall_pages(freekv_handle* h, int32_t layer, const uint8_t* sync_mask,
                                   void* stream);
 
@@ -182,6 +189,15 @@ freekv_status freekv_get_resident(freekv_handle* h, int32_t layer, int32_t* page
 freekv_status freekv_get_fetch(freekv_handle* h, int32_t layer, int32_t* n_fetch /*[U]*/,
                                int32_t* fetch_pages /*[U][K]*/);
 /* Summaries of pages [page_begin, page_end) of unit u as [n][2][d] bf16 (min, max). */
+/* Recall accounting of the last step (or select_pages) of `layer` (blocking): units
+ * corrected this step, the pages their synchronous path fetches (in direct mode read by the
+ * attention from the host pool), the pages the background recall moves for the others, and
+ * the bytes of each (page = 2 * p * d bf16). */
+typedef struct {
+    int32_t corrected_units, sync_pages, bg_pages;
+    int64_t sync_bytes, bg_bytes;
+} freekv_step_stats;
+freekv_status freekv_get_step_stats(freekv_handle* h, int32_t layer, freekv_step_stats* out);
 freekv_status freekv_get_summaries(freekv_handle* h, int32_t layer, int32_t unit, int32_t page_begin,
                                    int32_t page_end, uint16_t* out);
 freekv_status freekv_get_context(freekv_handle* h, int32_t layer, int32_t* ctx_tokens);
@@ -212,6 +228,23 @@ freekv_status freekv_synchronize(freekv_handle* h);
 void freekv_destroy(freekv_handle* h);
 const char* freekv_last_error(void);
 int32_t freekv_abi_version(void);
+
+/* ---- multi-GPU: one process per GPU, each handle
+ * configured with its kv-head / batch shard.  The units never interact; the
+ * one exchange step is gathering every rank's head outputs per layer.
+ *
+ * freekv_comm_unique_id: rank 0 creates the NCCL id (FREEKV_COMM_ID_BYTES
+ * bytes, host) and the caller broadcasts it (e.g. over torch.distributed).
+ * freekv_comm_init: every rank builds the communicator on its handle's device
+ * (blocking, collective over n_ranks).  freekv_set_gather_output: device fp32
+ * [n_layers][n_ranks][nb][n_qo][d] (caller-owned, NULL to stop): every
+ * decode step of layer l then ends with an all-gather of `out` into slice l
+ * on the compute stream -- a node of the step graph when captured.  Both
+ * invalidate a captured step graph (capture again).  ENCCL on NCCL errors. */
+#define FREEKV_COMM_ID_BYTES 128
+freekv_status freekv_comm_unique_id(uint8_t* id_out);
+freekv_status freekv_comm_init(freekv_handle* h, const uint8_t* id, int32_t n_ranks, int32_t rank);
+freekv_status freekv_set_gather_output(freekv_handle* h, float* gather_all);
 
 #ifdef __cplusplus
 }

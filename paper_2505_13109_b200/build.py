@@ -16,8 +16,25 @@ OBJ = os.path.join(HERE, "..", "build", "obj" + ("_" + VARIANT if VARIANT else "
 LIB = os.path.join(HERE, "libfreekv" + ("_" + VARIANT if VARIANT else "") + ".so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+def _nccl_dir():
+    """The NCCL torch loads (nvidia-nccl wheel) -- one libnccl.so.2 per process; system copy otherwise."""
+    try:
+        import nvidia.nccl as nn
+        d = list(nn.__path__)[0]
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    except Exception:  # noqa: BLE001
+        pass
+    return None
+
+
+NCCL = _nccl_dir()
+NCCL_INC = ["-I" + os.path.join(NCCL, "include")] if NCCL else []
+NCCL_LINK = (["-L" + os.path.join(NCCL, "lib"), "-Xlinker", "-rpath=" + os.path.join(NCCL, "lib"),
+              "-l:libnccl.so.2"] if NCCL else ["-lnccl"])
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
-                "-I" + os.path.join(HERE, "..", "include")] + VARIANT_DEFS
+                "-I" + os.path.join(HERE, "..", "include")] + NCCL_INC + VARIANT_DEFS
 
 SOURCES = ["api.cu", "append.cu", "score.cu", "select.cu", "recall.cu", "attn.cu"]
 HEADERS = ["fkv_internal.cuh", "append_unit.cuh", "attn_core.cuh", "select_core.cuh"]
@@ -48,7 +65,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
         if verbose or ptxas_v:
             print(out, file=sys.stderr)
     if force or procs or _mtime(LIB) < max(_mtime(o) for o in objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + NCCL_LINK
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}{r.stderr}")

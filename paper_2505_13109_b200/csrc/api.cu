@@ -24,6 +24,8 @@
 #include <string>
 #include <vector>
 
+#include <nccl.h>
+
 #include "../../include/freekv.h"
 #include "fkv_internal.cuh"
 
@@ -102,6 +104,11 @@ struct freekv_handle {
     bool capturing = false;
     cudaGraphExec_t g_compute = nullptr, g_recall = nullptr;
     std::vector<Rec> graph_recs;  // event pairs captured into the step graph (profile mode)
+    // multi-GPU: this rank's NCCL communicator over the kv-head / batch shards and
+    // the gathered per-layer output [n_layers][n_ranks][nb][n_qo][d] fp32 (the one exchange step)
+    ncclComm_t comm = nullptr;
+    int n_ranks = 1, rank = 0;
+    float* gather_all = nullptr;
 };
 
 namespace {
@@ -111,12 +118,12 @@ constexpr int kMaxAttnWarps = 148 * 16;
 size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
 
 struct Sizes {
-    size_t layer_bytes, scratch_bytes, dev_bytes, host_layer_bytes, host_bytes;
+    size_t layer_bytes, scratch_bytes, dense_bytes, dev_bytes, host_layer_bytes, host_bytes;
     // offsets inside one layer block
     size_t o_summ, o_sink, o_slots, o_ring, o_qprev, o_res_pages, o_res_slot, o_res_front, o_res_valid, o_res_cnt,
         o_pend_cnt,
         o_pend_pages, o_pend_slot, o_pend_front, o_flags, o_cbar, o_fetch_page, o_fetch_slot, o_n_fetch, o_ctx,
-        o_n_off, o_qcur, o_scores, o_pend_valid, o_order, o_ord_cnt, o_score_done;
+        o_n_off, o_qcur, o_scores, o_pend_valid, o_order, o_ord_cnt, o_score_done, o_sync_mask;
     size_t o_part_o, o_part_ml, o_page_rows, o_page_cnt, o_page_valid, o_page_dst, o_ready;
 };
 
@@ -147,7 +154,7 @@ freekv_status validate(const freekv_config* c, FkvDims* D) {
     if (n_page_host > 8192) return fail(FREEKV_EUNSUPPORTED, "max_ctx_tokens / page_size > 8191 pages");
     if (!(c->mode == 0 || c->mode == 1 || c->mode == 2)) return fail(FREEKV_EINVAL, "mode must be 0, 1 or 2");
     if (!std::isfinite(c->tau)) return fail(FREEKV_EINVAL, "tau must be finite");
-    if (c->first_layer_dense) return fail(FREEKV_EUNSUPPORTED, "first_layer_dense is not served by ABI v1");
+    if (!(c->first_layer_dense == 0 || c->first_layer_dense == 1)) return fail(FREEKV_EINVAL, "first_layer_dense must be 0 or 1");
     if ((long long)c->batch * c->n_kv > 4096) return fail(FREEKV_EUNSUPPORTED, "batch * n_kv must be <= 4096");
     if (c->pool < 0 || c->pool > 5) return fail(FREEKV_EINVAL, "pool must be a FREEKV_POOL_* value");
     if (c->corr_pool < 0 || c->corr_pool > 1) return fail(FREEKV_EINVAL, "corr_pool must be 0 or 1");
@@ -215,6 +222,7 @@ Sizes compute_sizes(const freekv_config* c, const FkvDims& D) {
     s.o_order = take(U * 4);
     s.o_ord_cnt = take(4 * 4);
     s.o_score_done = take(U * 4);
+    s.o_sync_mask = take(U);
     s.layer_bytes = o;
     o = 0;
     s.o_part_o = take((size_t)4 * kMaxAttnWarps * D.G * D.d * 4);
@@ -225,7 +233,10 @@ Sizes compute_sizes(const freekv_config* c, const FkvDims& D) {
     s.o_page_dst = take(U * D.P_max * 4);
     s.o_ready = take(U * 4);
     s.scratch_bytes = o;
-    s.dev_bytes = s.layer_bytes * c->n_layers + s.scratch_bytes;
+    // first_layer_dense (O-7): layer 0 keeps every page of every unit resident for its dense
+    // attention, [U][n_page_max][2][p][d] after the scratch block
+    s.dense_bytes = c->first_layer_dense ? align_up(U * D.n_page_max * pe_b) : 0;
+    s.dev_bytes = s.layer_bytes * c->n_layers + s.scratch_bytes + s.dense_bytes;
     s.host_layer_bytes = (size_t)D.nb * D.n_page_host * D.n_kv * pe_b;
     s.host_bytes = s.host_layer_bytes * c->n_layers;
     return s;
@@ -307,15 +318,21 @@ freekv_status do_select(freekv_handle* h, int layer, const void* q, int32_t* pag
     return FREEKV_OK;
 }
 
-freekv_status do_recall(freekv_handle* h, int layer, cudaStream_t s) {
-    FKV_CUDA(timed(h, K_RECALL_SYNC, s, [&] { return launch_recall(h->D, h->layers[layer], 1, s); }));
+freekv_status do_recall(freekv_handle* h, int layer, cudaStream_t s, const uint8_t* sync_mask = nullptr) {
+    const FkvLayer& L = h->layers[layer];
+    const uint8_t* mk = nullptr;
+    if (sync_mask) {  // the caller's mask, copied on s into the layer's own [U] (the background part reads it later)
+        FKV_CUDA(cudaMemcpyAsync(L.sync_mask, sync_mask, h->D.U, cudaMemcpyDeviceToDevice, s));
+        mk = L.sync_mask;
+    }
+    FKV_CUDA(timed(h, K_RECALL_SYNC, s, [&] { return launch_recall(h->D, L, 1, s, nullptr, mk); }));
     if (h->serial_recall) {
-        FKV_CUDA(timed(h, K_RECALL_BG, s, [&] { return launch_recall(h->D, h->layers[layer], 0, s); }));
+        FKV_CUDA(timed(h, K_RECALL_BG, s, [&] { return launch_recall(h->D, L, 0, s, nullptr, mk); }));
         return FREEKV_OK;
     }
     FKV_CUDA(cudaEventRecord(h->ev_select[layer], s));
     FKV_CUDA(cudaStreamWaitEvent(h->rs, h->ev_select[layer], 0));
-    FKV_CUDA(timed(h, K_RECALL_BG, h->rs, [&] { return launch_recall(h->D, h->layers[layer], 0, h->rs); }));
+    FKV_CUDA(timed(h, K_RECALL_BG, h->rs, [&] { return launch_recall(h->D, L, 0, h->rs, nullptr, mk); }));
     FKV_CUDA(cudaEventRecord(h->ev_recall[layer], h->rs));
     h->recall_pending[layer] = 1;
     return FREEKV_OK;
@@ -324,6 +341,13 @@ freekv_status do_recall(freekv_handle* h, int layer, cudaStream_t s) {
 // primitive attention: every unit's page list comes from select_pages (mode 0)
 freekv_status do_attn(freekv_handle* h, int layer, const void* q, float* out, cudaStream_t s) {
     if (!q || !out) return fail(FREEKV_EINVAL, "q/out is NULL");
+    if (h->layers[layer].dense) {  // first_layer_dense: dense attention over [0, Lc)
+        FKV_CUDA(timed(h, K_ATTN_SPLIT, s, [&] {
+            return launch_attn_cluster(h->D, h->layers[layer], h->X, (const uint16_t*)q, out, h->tmap_kv,
+                                       h->tmap_host, 3, h->attn_cluster, false, 0, s);
+        }));
+        return FREEKV_OK;
+    }
     if (h->D.direct) {
         FKV_CUDA(timed(h, K_ATTN_SPLIT, s, [&] {
             return launch_attn_cluster(h->D, h->layers[layer], h->X, (const uint16_t*)q, out, h->tmap_kv, h->tmap_host,
@@ -424,7 +448,7 @@ freekv_status do_step_tail(freekv_handle* h, int layer, const void* q, float* ou
 //
 // Serial step (FREEKV_OVERLAP=0, and the paper-order recall mode FREEKV_CORR=recall): pre ->
 // score -> select (every unit's page list) -> attention / recall tail on the compute stream.
-freekv_status do_layer_step(freekv_handle* h, int layer, const void* q, const void* k_new, const void* v_new,
+freekv_status do_layer_step_core(freekv_handle* h, int layer, const void* q, const void* k_new, const void* v_new,
                             float* out) {
     cudaStream_t cs = h->cs;
     const FkvDims& D = h->D;
@@ -432,6 +456,21 @@ freekv_status do_layer_step(freekv_handle* h, int layer, const void* q, const vo
     if (!q || !out) return fail(FREEKV_EINVAL, "q/out is NULL");
     // the previous step's side chain / recall of this layer (its selection, its slots)
     if (!h->capturing && h->recall_pending[layer]) FKV_CUDA(cudaStreamWaitEvent(cs, h->ev_recall[layer], 0));
+    if (L.dense) {
+        // first_layer_dense (O-7): layer 0 appends its token and attends every page [0, Lc)
+        // from its dense pool -- no scoring, selection or recall.  The attention launches without
+        // PDL (it reads the context length the append wrote before its prologue).
+        FKV_CUDA(timed(h, K_APPEND, cs, [&] {
+            return launch_append(D, L, (const uint16_t*)k_new, (const uint16_t*)v_new, 1, cs);
+        }));
+        if (!h->capturing) h->ctx_host[layer] += 1;
+        FKV_CUDA(timed(h, K_ATTN_SPLIT, cs, [&] {
+            return launch_attn_cluster(D, L, h->X, (const uint16_t*)q, out, h->tmap_kv, h->tmap_host, 3,
+                                       h->attn_cluster, false, h->prio_hi, cs);
+        }));
+        if (h->capturing) FKV_CUDA(cudaEventRecord(h->ev_recall[layer], cs));  // joined at the graph's end
+        return FREEKV_OK;
+    }
     if (!h->spec && D.direct && D.n_win >= 1) {
         // serial step, three launches: score grid (+ correction check and append per unit, the token
         // pending) -> select (every unit's page list) -> attention (mode 2; its commit publishes the
@@ -486,6 +525,19 @@ freekv_status do_layer_step(freekv_handle* h, int layer, const void* q, const vo
         FKV_CUDA(cudaEventRecord(h->ev_recall[layer], ss2));
     }
     if (!h->capturing) h->recall_pending[layer] = 1;
+    return FREEKV_OK;
+}
+
+// One layer of the decode step, then (multi-GPU) the per-layer all-gather of the head outputs of
+// every rank on the compute stream -- inside the step graph when capturing.
+freekv_status do_layer_step(freekv_handle* h, int layer, const void* q, const void* k_new, const void* v_new,
+                            float* out) {
+    freekv_status st = do_layer_step_core(h, layer, q, k_new, v_new, out);
+    if (st != FREEKV_OK || !h->comm || !h->gather_all) return st;
+    const size_t count = (size_t)h->D.nb * h->D.n_qo * h->D.d;
+    float* dst = h->gather_all + (size_t)layer * h->n_ranks * count;
+    const ncclResult_t r = ncclAllGather(out, dst, count, ncclFloat, h->comm, h->cs);
+    if (r != ncclSuccess) return fail(FREEKV_ENCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));
     return FREEKV_OK;
 }
 
@@ -612,10 +664,12 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         L.order = (int32_t*)(base + s.o_order);
         L.ord_cnt = (int32_t*)(base + s.o_ord_cnt);
         L.score_done = (int32_t*)(base + s.o_score_done);
+        L.sync_mask = (uint8_t*)(base + s.o_sync_mask);
         L.host = (uint16_t*)(hd + s.host_layer_bytes * l);
         L.host_row0 = (int)(s.host_layer_bytes * l / (kHeadDim * 2));
         L.arena = (const uint16_t*)dev;
     }
+    if (s.dense_bytes) h->layers[0].dense = (uint16_t*)(dev + s.layer_bytes * cfg->n_layers + s.scratch_bytes);
     uint8_t* sb = dev + s.layer_bytes * cfg->n_layers;
     h->X.part_o = (float*)(sb + s.o_part_o);
     h->X.part_ml = (float*)(sb + s.o_part_ml);
@@ -813,8 +867,7 @@ freekv_status freekv_select_pages(freekv_handle* h, int32_t layer, const void* q
 freekv_status freekv_recall_pages(freekv_handle* h, int32_t layer, const uint8_t* sync_mask, void* stream) {
     freekv_status st = check_layer(h, layer);
     if (st != FREEKV_OK) return st;
-    if (sync_mask) return fail(FREEKV_EUNSUPPORTED, "sync_mask must be NULL in ABI v1");
-    return do_recall(h, layer, pick(h, stream));
+    return do_recall(h, layer, pick(h, stream), sync_mask);
 }
 
 freekv_status freekv_sparse_decode_attn(freekv_handle* h, int32_t layer, const void* q, float* out, void* stream) {
@@ -867,6 +920,33 @@ freekv_status freekv_get_fetch(freekv_handle* h, int32_t layer, int32_t* n_fetch
     const size_t U = h->D.U, K = h->D.K;
     if (n_fetch) FKV_CUDA(cudaMemcpy(n_fetch, L.n_fetch, U * 4, cudaMemcpyDeviceToHost));
     if (fetch_pages) FKV_CUDA(cudaMemcpy(fetch_pages, L.fetch_page, U * K * 4, cudaMemcpyDeviceToHost));
+    return FREEKV_OK;
+}
+
+freekv_status freekv_get_step_stats(freekv_handle* h, int32_t layer, freekv_step_stats* out) {
+    freekv_status st = check_layer(h, layer);
+    if (st != FREEKV_OK) return st;
+    if (!out) return fail(FREEKV_EINVAL, "out is NULL");
+    if ((st = sync_both(h)) != FREEKV_OK) return st;
+    const FkvLayer& L = h->layers[layer];
+    const size_t U = h->D.U;
+    std::vector<uint8_t> fl(U);
+    std::vector<int32_t> nf(U);
+    FKV_CUDA(cudaMemcpy(fl.data(), L.flags, U, cudaMemcpyDeviceToHost));
+    FKV_CUDA(cudaMemcpy(nf.data(), L.n_fetch, U * 4, cudaMemcpyDeviceToHost));
+    const int64_t page_bytes = (int64_t)page_elems(h->D) * 2;
+    freekv_step_stats s{};
+    for (size_t u = 0; u < U; ++u) {
+        if (fl[u]) {
+            s.corrected_units += 1;
+            s.sync_pages += nf[u];
+        } else {
+            s.bg_pages += nf[u];
+        }
+    }
+    s.sync_bytes = s.sync_pages * page_bytes;
+    s.bg_bytes = s.bg_pages * page_bytes;
+    *out = s;
     return FREEKV_OK;
 }
 
@@ -1076,6 +1156,41 @@ freekv_status freekv_step_graph_launch(freekv_handle* h) {
     return FREEKV_OK;
 }
 
+freekv_status freekv_comm_unique_id(uint8_t* id_out) {
+    if (!id_out) return fail(FREEKV_EINVAL, "id_out is NULL");
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return fail(FREEKV_ENCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    static_assert(sizeof(ncclUniqueId) == FREEKV_COMM_ID_BYTES, "ncclUniqueId size");
+    std::memcpy(id_out, &id, sizeof(id));
+    return FREEKV_OK;
+}
+
+freekv_status freekv_comm_init(freekv_handle* h, const uint8_t* id, int32_t n_ranks, int32_t rank) {
+    if (!h || !id) return fail(FREEKV_EINVAL, "handle/id is NULL");
+    if (n_ranks < 1 || rank < 0 || rank >= n_ranks) return fail(FREEKV_EINVAL, "bad n_ranks / rank");
+    if (h->comm) return fail(FREEKV_ESTATE, "communicator already initialised");
+    FKV_CUDA(cudaSetDevice(h->device));
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    ncclComm_t c = nullptr;
+    const ncclResult_t r = ncclCommInitRank(&c, n_ranks, uid, rank);
+    if (r != ncclSuccess) return fail(FREEKV_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    h->comm = c;
+    h->n_ranks = n_ranks;
+    h->rank = rank;
+    drop_graphs(h);  // a captured step graph has no all-gather nodes
+    return FREEKV_OK;
+}
+
+freekv_status freekv_set_gather_output(freekv_handle* h, float* gather_all) {
+    if (!h) return fail(FREEKV_EINVAL, "handle is NULL");
+    if (gather_all && !h->comm) return fail(FREEKV_ESTATE, "freekv_comm_init first");
+    h->gather_all = gather_all;
+    drop_graphs(h);
+    return FREEKV_OK;
+}
+
 void freekv_destroy(freekv_handle* h) {
     if (!h) return;
     cudaStreamSynchronize(h->cs);
@@ -1099,6 +1214,7 @@ void freekv_destroy(freekv_handle* h) {
     }
     if (h->ss) cudaStreamDestroy(h->ss);
     if (h->X.trace) cudaFree(h->X.trace);
+    if (h->comm) ncclCommDestroy(h->comm);
     delete h;
 }
 

@@ -57,16 +57,20 @@ __device__ __forceinline__ void append_unit(const FkvDims& D, const FkvLayer& L,
         else if (j >= ring_lo)
             dst = reinterpret_cast<uint4*>(L.ring + ((size_t)u * D.R_loc + (j % D.R_loc)) * pe);
         const bool completes = j >= D.n_sink && t0 + p <= L1;
+        // dense layer (first_layer_dense): every page also in its dense-pool home
+        uint4* dn = L.dense ? reinterpret_cast<uint4*>(L.dense + ((size_t)u * D.n_page_max + j) * pe) : nullptr;
         if (!completes) {
             // fast path (most decode steps): copy the new token rows straight to their page
-            if (dst) {
+            if (dst || dn) {
                 const int ta = max(t0, L0), tb = min(t0 + p, L1);
                 const int n_u4 = (tb - ta) * row_u4;
                 for (int i = threadIdx.x; i < 2 * n_u4; i += blockDim.x) {
                     const int kv = i / n_u4, rem = i % n_u4, r = rem / row_u4, c = rem % row_u4;
                     const int t = ta + r;
                     const uint16_t* src = (kv == 0 ? k : v) + (((size_t)b * n_new + (t - L0)) * D.n_kv + m) * d;
-                    dst[((size_t)kv * p + (t - t0)) * row_u4 + c] = reinterpret_cast<const uint4*>(src)[c];
+                    const uint4 val = reinterpret_cast<const uint4*>(src)[c];
+                    if (dst) dst[((size_t)kv * p + (t - t0)) * row_u4 + c] = val;
+                    if (dn) dn[((size_t)kv * p + (t - t0)) * row_u4 + c] = val;
                 }
             }
             continue;
@@ -91,6 +95,7 @@ __device__ __forceinline__ void append_unit(const FkvDims& D, const FkvLayer& L,
         uint4* host = reinterpret_cast<uint4*>(L.host + (((size_t)b * D.n_page_host + j) * D.n_kv + m) * pe);
         for (int i = threadIdx.x; i < page_u4; i += blockDim.x) {
             host[i] = sm[i];
+            if (dn) dn[i] = sm[i];
             if (dst) {
                 const int r = (i % (p * row_u4)) / row_u4;
                 if (t0 + r >= L0) dst[i] = sm[i];

@@ -191,6 +191,8 @@ static int attn_stages();
 //   A unit that is not corrected attends its resident set R = S_{i-1} at once (list built here,
 //   ResSrc); its S_i is committed by the next step's pre kernel.  A corrected unit waits for
 //   X.ready[u] (its S_i page list from the side chain's select) and commits S_i itself.
+// mode 2 (serial decode step): see below; the select of this step runs before it.
+// mode 3 (first_layer_dense): every page [0, Lc) of the unit from the dense pool; no commit.
 template <int NST, int C>
 __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 3)
     fkv_attn_cluster_kernel(FkvDims D, FkvLayer L, FkvScratch X, const uint16_t* __restrict__ q,
@@ -226,7 +228,8 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 3)
     const int k = crank * W + warp;
     // this warp's share of the unit's page list, in 16-token slabs (an even split of P_max * spp
     // slabs; whole entries [pa, pbc) minus `skip` slabs at the front and `trim` at the back)
-    const int spp = D.p >> 4, TS = D.P_max * spp;
+    // mode 3 (dense layer): launched without PDL after the append, so the context is final here
+    const int spp = D.p >> 4, TS = (mode == 3 ? (L.ctx[u] + D.p - 1) / D.p : D.P_max) * spp;
     const int sa = (int)((long long)k * TS / NW), sb = (int)((long long)(k + 1) * TS / NW);
     const int pa = sa / spp, pbc = (sb + spp - 1) / spp;
     const int skip = sa - pa * spp, trim = pbc * spp - sb;
@@ -269,7 +272,7 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 3)
     const bool early = mode == 2 && !flag && D.attn_early;
     if (!early) pdl_wait();  // mode 0/2: the select kernel's page lists are complete; mode 1: the pre kernel is done
     if (mode != 2) {
-        flag = L.flags[u];
+        flag = mode == 3 ? 0 : L.flags[u];
         Lc = L.ctx[u];
     }
     load_q_frags(D, q, u, qa);
@@ -278,7 +281,12 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 3)
             spin_until_ge(X.ready + u, 1);
         __syncwarp();
     }
-    if (mode == 0 || flag) {
+    if (mode == 3) {  // first_layer_dense: T = [0, Lc) (O-7), every page from the dense pool
+        const DenseSrc dsrc{(int)((L.dense - L.arena) / kHeadDim) + u * D.n_page_max * 2 * D.p, D.p, Lc, 2 * D.p};
+        const int pe = min(pbc, dsrc.count());
+        attend_pages<NST>(D, X, qa, &tmap, &tmap_h, dsrc, pa, pe, ring, bar[warp], phase_bits, m_run, l_run, oacc, 4,
+                          w, 0, skip, pe == pbc ? trim : 0);
+    } else if (mode == 0 || flag) {
         const TableSrc tsrc{X.page_rows + (size_t)u * D.P_max, X.page_valid + (size_t)u * D.P_max,
                             X.page_dst + (size_t)u * D.P_max};
         const int pe = min(pbc, __ldcg(X.page_cnt + u));
@@ -364,7 +372,7 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 3)
         }
         // commit R := S_i: every unit in modes 0 and 2; in mode 1 the corrected units (the
         // others' S_i is committed by the next step's pre kernel, after their background recall)
-        if (mode != 1 || flag) {
+        if (mode != 3 && (mode != 1 || flag)) {
             for (int i = tid; i < D.K; i += blockDim.x) {
                 L.res_pages[(size_t)u * D.K + i] = __ldcg(L.pend_pages + (size_t)u * D.K + i);
                 L.res_slot[(size_t)u * D.K + i] = __ldcg(L.pend_slot + (size_t)u * D.K + i);

@@ -218,6 +218,18 @@ struct ResSrc {
     }
 };
 
+// The dense page list of a unit (first_layer_dense, layer 0, O-7 / P:560): every page [0, Lc)
+// from the dense pool
+struct DenseSrc {
+    int row0, p, Lc, page_rows;
+    __device__ __forceinline__ void load(int i, int& r, int& v, int& d) const {
+        d = 0;
+        r = row0 + i * page_rows;
+        v = min(p, Lc - i * p);
+    }
+    __device__ __forceinline__ int count() const { return (Lc + p - 1) / p; }
+};
+
 __device__ __forceinline__ ResSrc res_src(const FkvDims& D, const FkvLayer& L, int u, int Lc) {
     ResSrc s;
     s.p = D.p;

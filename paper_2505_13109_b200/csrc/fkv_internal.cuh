@@ -74,10 +74,13 @@ struct FkvLayer {
     int32_t* order;       // [U]     units in scoring/selection priority order (corrected units first)
     int32_t* ord_cnt;     // [2][2]  per step parity (ctx & 1): fill counters of `order` (corrected from the
                           //         front, the others from the back)
+    uint8_t* sync_mask;   // [U]     freekv_recall_pages' sync_mask, copied (read by the background part)
     int32_t* score_done;  // [U]     score items of the unit finished this step (release/acquire hand-off)
     unsigned long long* trace;  // diagnostics (FREEKV_TRACE=1): %globaltimer stamps, else NULL
     uint16_t* host;       // device-mapped host pool of this layer: [nb][n_page_host][n_kv][2][p][d]
     const uint16_t* arena;  // base of the device arena (row 0 of the attention TMA tensor)
+    uint16_t* dense;      // first_layer_dense, layer 0 only: [U][n_page_max][2][p][d] every page resident
+                          // (dense attention); NULL otherwise
     int host_row0;        // first row of this layer's host pool in the host TMA tensor (256-byte rows)
 };
 
@@ -306,8 +309,10 @@ cudaError_t launch_score(const FkvDims& D, const FkvLayer& L, const FkvScratch& 
 cudaError_t launch_select(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                           int32_t* pages_out, uint8_t* corrected_out, int flag_src, int list_all, int part,
                           int nc, int lpt, bool pdl, int prio, cudaStream_t s, int pending = 0, int nt = 256);
+// mask (device [U], nullable): the units recalled synchronously (sync_mode 1) / not (0) instead of
+// the correction flags (freekv_recall_pages' sync_mask)
 cudaError_t launch_recall(const FkvDims& D, const FkvLayer& L, int sync_mode, cudaStream_t s,
-                          unsigned long long* trace = nullptr);
+                          unsigned long long* trace = nullptr, const uint8_t* mask = nullptr);
 cudaError_t attn_resident_warps(int cps, int* warps);  // warps of the split kernel's grid (cps CTAs per SM)
 cudaError_t launch_attn_split(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                               int phase, const CUtensorMap& tmap, const CUtensorMap& tmap_host,

@@ -31,7 +31,7 @@ constexpr int kRecallMaxU = 4096;
 
 __global__ void __launch_bounds__(kRecallThreads) fkv_recall_kernel(FkvDims D, FkvLayer L, int sync_mode,
                                                                     unsigned long long* __restrict__ trace,
-                                                                    int frag) {
+                                                                    int frag, const uint8_t* __restrict__ mask) {
     __shared__ int s_off[kRecallMaxU + 1];  // exclusive prefix of the eligible units' fetch counts
     __shared__ int s_wsum[kRecallThreads / 32];
     if (threadIdx.x == 0) trace_stamp(trace, 2 + (sync_mode ? 0 : 1), blockIdx.x, 0);
@@ -43,7 +43,8 @@ __global__ void __launch_bounds__(kRecallThreads) fkv_recall_kernel(FkvDims D, F
         const int u = tid * per + i;
         int n = 0;
         if (u < D.U) {
-            const int f = L.flags[u], nf = L.n_fetch[u];
+            // which units are synchronous: the correction flags, or the caller's sync_mask
+            const int f = mask ? mask[u] : L.flags[u], nf = L.n_fetch[u];
             n = ((f != 0) == (sync_mode != 0)) ? nf : 0;
         }
         s_off[u < D.U ? u : D.U] = n;  // temporarily the count
@@ -131,7 +132,7 @@ static int recall_ctas(int sync_mode) {
 }
 
 cudaError_t launch_recall(const FkvDims& D, const FkvLayer& L, int sync_mode, cudaStream_t s,
-                          unsigned long long* trace) {
+                          unsigned long long* trace, const uint8_t* mask) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -148,7 +149,7 @@ cudaError_t launch_recall(const FkvDims& D, const FkvLayer& L, int sync_mode, cu
         int v = fe ? std::max(0, atoi(fe)) : 0;
         frag = (v % 16) ? 0 : v;  // bulk copies move multiples of 16 bytes
     }
-    fkv_recall_kernel<<<grid, kRecallThreads, smem, s>>>(D, L, sync_mode, trace, frag);
+    fkv_recall_kernel<<<grid, kRecallThreads, smem, s>>>(D, L, sync_mode, trace, frag, mask);
     return cudaGetLastError();
 }
 

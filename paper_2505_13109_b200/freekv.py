@@ -28,6 +28,7 @@ EXPORTED = [
     "freekv_get_context", "freekv_get_dims", "freekv_synchronize", "freekv_destroy",
     "freekv_last_error", "freekv_abi_version", "freekv_profile_begin", "freekv_profile_end",
     "freekv_step_graph_capture", "freekv_step_graph_launch", "freekv_step_graph_profile", "freekv_debug_trace",
+    "freekv_get_step_stats", "freekv_comm_unique_id", "freekv_comm_init", "freekv_set_gather_output",
 ]
 KERNEL_CLASSES = ["append", "score", "select_finalize", "recall_sync", "recall_bg", "attn_split", "attn_combine",
                   "attn_split_phase2", "prep", "score_bg", "select_finalize_bg"]
@@ -45,6 +46,11 @@ class _Config(ctypes.Structure):
         "window_tokens", "max_ctx_tokens")] + [("tau", ctypes.c_float)] + [(n, ctypes.c_int32) for n in (
             "mode", "first_layer_dense", "kv_head_begin", "kv_head_end", "batch_begin", "batch_end",
             "n_ranks", "rank", "pool", "corr_pool")]
+
+
+class _StepStats(ctypes.Structure):
+    _fields_ = [("corrected_units", ctypes.c_int32), ("sync_pages", ctypes.c_int32), ("bg_pages", ctypes.c_int32),
+                ("sync_bytes", ctypes.c_int64), ("bg_bytes", ctypes.c_int64)]
 
 
 class _Buffers(ctypes.Structure):
@@ -123,6 +129,10 @@ def load_library():
             "freekv_get_selection": [vp, i32, vp, vp, vp, vp],
             "freekv_get_resident": [vp, i32, vp, vp],
             "freekv_get_fetch": [vp, i32, vp, vp],
+            "freekv_get_step_stats": [vp, i32, P(_StepStats)],
+            "freekv_comm_unique_id": [vp],
+            "freekv_comm_init": [vp, vp, i32, i32],
+            "freekv_set_gather_output": [vp, vp],
             "freekv_get_summaries": [vp, i32, i32, i32, i32, vp],
             "freekv_get_context": [vp, i32, P(i32)],
             "freekv_get_dims": [vp, P(i32), P(i32), P(i32)],
@@ -210,8 +220,9 @@ class FreeKV:
         _check(self.L.freekv_select_pages(self.h, layer, q.data_ptr(), _ptr(pages_out), _ptr(corrected_out),
                                           self._s(stream)))
 
-    def recall_pages(self, layer, stream=None):
-        _check(self.L.freekv_recall_pages(self.h, layer, None, self._s(stream)))
+    def recall_pages(self, layer, sync_mask=None, stream=None):
+        """sync_mask: optional device uint8 [nb][n_kv] (units recalled synchronously)."""
+        _check(self.L.freekv_recall_pages(self.h, layer, _ptr(sync_mask), self._s(stream)))
 
     def sparse_decode_attn(self, layer, q, out, stream=None):
         _check(self.L.freekv_sparse_decode_attn(self.h, layer, q.data_ptr(), out.data_ptr(), self._s(stream)))
@@ -276,6 +287,30 @@ class FreeKV:
         pages = np.empty((self.U, self.K), np.int32)
         _check(self.L.freekv_get_fetch(self.h, layer, _np_ptr(n), _np_ptr(pages)))
         return n, pages
+
+    # -- multi-GPU: the library's own NCCL communicator and per-layer all-gather ---------------
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        """Rank 0: a fresh NCCL unique id (128 bytes) to broadcast to the other ranks."""
+        L = load_library()
+        buf = (ctypes.c_uint8 * 128)()
+        _check(L.freekv_comm_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+        return bytes(buf)
+
+    def comm_init(self, uid: bytes, n_ranks: int, rank: int):
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        _check(self.L.freekv_comm_init(self.h, ctypes.cast(buf, ctypes.c_void_p), n_ranks, rank))
+
+    def set_gather_output(self, gather_all):
+        """gather_all: device fp32 [n_layers][n_ranks][nb][n_qo][d] (or None)."""
+        self._gather = gather_all
+        _check(self.L.freekv_set_gather_output(self.h, _ptr(gather_all)))
+
+    def get_step_stats(self, layer):
+        """Recall accounting of the layer's last step (freekv_get_step_stats)."""
+        st = _StepStats()
+        _check(self.L.freekv_get_step_stats(self.h, layer, ctypes.byref(st)))
+        return {f: getattr(st, f) for f, _ in _StepStats._fields_}
 
     def get_summaries(self, layer, unit, page_begin, page_end):
         out = np.empty((page_end - page_begin, 2, self.cfg.head_dim), np.uint16)

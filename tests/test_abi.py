@@ -32,7 +32,7 @@ def test_library_exports_every_header_symbol():
     L = P.load_library()
     for s in syms:
         assert hasattr(L, s)
-    assert L.freekv_abi_version() == 2
+    assert L.freekv_abi_version() == 3
 
 
 def test_library_is_sm100a():
@@ -79,3 +79,10 @@ def test_no_cpu_fallback():
         pytest.skip("GPU present")
     with pytest.raises(P.FreeKVError):
         P.FreeKV(cfg(n_layers=1, batch=1, max_ctx_tokens=4096))
+
+
+def test_comm_unique_id_without_gpu():
+    """The NCCL id is created through the library (no device needed): 128 bytes, fresh each call."""
+    from paper_2505_13109_b200.freekv import FreeKV
+    a, b = FreeKV.comm_unique_id(), FreeKV.comm_unique_id()
+    assert len(a) == 128 and len(b) == 128 and a != b

@@ -31,7 +31,8 @@ def rel_err(out, ref):
 
 def run_parity(G=4, n_kv=2, batch=2, page=32, sink=64, window=64, budget=256, L0=700, steps=6,
                n_layers=2, tau=0.8, mode=O.MODE_SPECULATIVE, event_rate=0.3, seed=11, tie_pages=False,
-               check_summaries=True, use_primitives=False, check_fetch=True, pool=0, corr_pool=0):
+               check_summaries=True, use_primitives=False, check_fetch=True, pool=0, corr_pool=0, dense0=0,
+               sync_mask=None):
     _need_gpu()
     import paper_2505_13109_b200 as P
     d = 128
@@ -39,11 +40,11 @@ def run_parity(G=4, n_kv=2, batch=2, page=32, sink=64, window=64, budget=256, L0
     max_ctx = L0 + steps + 3
     cfg = P.FreeKVConfig(n_layers=n_layers, batch=batch, n_qo=n_qo, n_kv=n_kv, head_dim=d, page_size=page,
                          budget_tokens=budget, sink_tokens=sink, window_tokens=window, max_ctx_tokens=max_ctx,
-                         tau=tau, mode=mode, pool=pool, corr_pool=corr_pool)
+                         tau=tau, mode=mode, pool=pool, corr_pool=corr_pool, first_layer_dense=dense0)
     fkv = P.FreeKV(cfg)
     ocfg = O.OracleConfig(n_layers=n_layers, batch=batch, n_qo=n_qo, n_kv=n_kv, head_dim=d, page_size=page,
                           budget_tokens=budget, sink_tokens=sink, window_tokens=window, max_ctx_tokens=max_ctx,
-                          tau=tau, mode=mode, pool=pool, corr_pool=corr_pool)
+                          tau=tau, mode=mode, pool=pool, corr_pool=corr_pool, first_layer_dense=bool(dense0))
     eng = O.OracleEngine(ocfg)
     dev = fkv.device
     for layer in range(n_layers):
@@ -72,11 +73,21 @@ def run_parity(G=4, n_kv=2, batch=2, page=32, sink=64, window=64, budget=256, L0
                 pages_out = torch.full((batch, n_kv, cfg.K), -7, dtype=torch.int32, device=dev)
                 corr_out = torch.zeros((batch, n_kv), dtype=torch.uint8, device=dev)
                 fkv.select_pages(layer, qd, pages_out, corr_out)
-                fkv.recall_pages(layer)
+                mask = None
+                if sync_mask == "all":
+                    mask = torch.ones((batch, n_kv), dtype=torch.uint8, device=dev)
+                elif sync_mask == "alternate":
+                    mask = (torch.arange(batch * n_kv, device=dev) % 2).to(torch.uint8).view(batch, n_kv)
+                fkv.recall_pages(layer, sync_mask=mask)
                 fkv.sparse_decode_attn(layer, qd, out)
             else:
                 fkv.decode_step(layer, qd, kd, vd, out)
             fkv.synchronize()
+            if dense0 and layer == 0:  # O-7: dense attention over [0, Lc), no selection to compare
+                e = rel_err(out.cpu().numpy().astype(np.float64), ref["out"])
+                worst = max(worst, e)
+                assert e <= REL_TOL, (i, layer, e)
+                continue
             sel = fkv.get_selection(layer)
             assert np.array_equal(sel["flags"], ref["flags"]), (i, layer, sel["flags"], ref["flags"])
             assert np.array_equal(sel["cbar"].view(np.uint32), ref["cbar"].view(np.uint32)) or i == 0
@@ -89,6 +100,12 @@ def run_parity(G=4, n_kv=2, batch=2, page=32, sink=64, window=64, budget=256, L0
             for u in range(fkv.U if check_fetch else 0):
                 exp = ref["fetch_sync"][u] if ref["flags"][u] else ref["fetch_bg"][u]
                 assert list(fetch_pages[u, :n_fetch[u]]) == exp, (i, layer, u)
+            st = fkv.get_step_stats(layer)  # freekv_get_step_stats vs the oracle's fetch lists
+            assert st["corrected_units"] == int(ref["flags"].sum())
+            if check_fetch:
+                assert st["sync_pages"] == sum(len(x) for x in ref["fetch_sync"])
+                assert st["bg_pages"] == sum(len(x) for x in ref["fetch_bg"])
+            assert st["sync_bytes"] == st["sync_pages"] * 2 * page * d * 2
             e = rel_err(out.cpu().numpy().astype(np.float64), ref["out"])
             worst = max(worst, e)
             assert e <= REL_TOL, (i, layer, e)
@@ -107,6 +124,20 @@ def run_parity(G=4, n_kv=2, batch=2, page=32, sink=64, window=64, budget=256, L0
 def test_parity_llama_shape_speculative():
     nf, nu, worst = run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=6)
     assert nf > 0 and nu > 0  # both paths (corrected / speculative) exercised
+
+
+@pytest.mark.parametrize("prims", [False, True])
+def test_parity_first_layer_dense(prims):
+    """first_layer_dense (O-7): layer 0 attends all Lc tokens from its dense pool (decode_step
+    and the primitive API), the other layers run FreeKV unchanged."""
+    run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=4, n_layers=2, dense0=1, use_primitives=prims)
+
+
+@pytest.mark.parametrize("mask", ["all", "alternate"])
+def test_parity_recall_sync_mask(mask):
+    """freekv_recall_pages with a caller sync_mask (every unit / every other unit synchronous)
+    instead of the correction flags: identical selections, fetch lists and outputs (direct mode)."""
+    run_parity(G=4, n_kv=2, batch=2, page=32, L0=1500, steps=4, use_primitives=True, sync_mask=mask)
 
 
 def test_parity_primitives():
