@@ -41,6 +41,11 @@ CONFIGS = {
     # the correction threshold
     "c4": dict(workload="r1-distill-llama-8b-32layers-ctx48k-b8-budget2048", n_layers=32, batch=8, n_qo=32,
                n_kv=8, ctx=49152, budget=2048, sink=512, window=512, tau=0.8, event_rate=0.05),
+    # BASELINE.json configs[4]: Llama-3.1-70B heads (64q/8kv), 80 layers, ctx 128K, batch 16.  Host KV for
+    # 80 layers is 640 GiB at one GPU, so l_inst = 4 layers are instantiated and the step graph cycles
+    # through them (virtual layer v runs layer v % 4; SURVEY §7 hard part 9)
+    "c5": dict(workload="llama3.1-70b-80layers-ctx128k-b16-budget2048", n_layers=80, batch=16, n_qo=64, n_kv=8,
+               ctx=131072, budget=2048, sink=512, window=512, tau=0.8, event_rate=0.05, l_inst=4),
 }
 
 METRIC = "decode-step µs/layer and tokens/s at 32K ctx; attn HBM GB/s; recall GB/s vs host link"
@@ -187,7 +192,9 @@ def run_ours(args, c, rank, world, local_rank):
     kv_loc, kv0 = sh.n_kv, sh.kv_begin
     b0, b1 = sh.batch_begin, sh.batch_end
     nb_loc = sh.batch
-    n_layers = c["n_layers"]
+    n_layers = c["n_layers"]                          # virtual layers of the step
+    n_inst = min(c.get("l_inst", n_layers), n_layers)  # instantiated layers (handle)
+    tok_per_step = (n_layers + n_inst - 1) // n_inst   # tokens each instantiated layer appends per step
     alpha, beta, rho, ev_rate = GEN[args.gen]
     gkw = {} if alpha is None else {"alpha": alpha}
     qkw = {}
@@ -202,17 +209,19 @@ def run_ours(args, c, rank, world, local_rank):
     # warm, timed, exposed-recall pair, profiled x2, e2e
     total_steps = args.warmup + 1 + args.steps + 2 * (exp_steps + 2) + 2 * args.profile_steps + \
         (0 if args.nested else args.steps)
-    max_ctx = c["ctx"] + total_steps + 1
+    max_ctx = c["ctx"] + total_steps * tok_per_step + 1
     stream = torch.cuda.Stream(dev, priority=-1)  # compute outranks the background recall stream
+    from paper_2505_13109_b200.numa import bind_to_gpu_node
+    numa = bind_to_gpu_node(local_rank)  # the pinned host shard below lands on the GPU's NUMA node
     t0 = time.time()
-    cfg, fkv = build_handle(P, dict(c, batch=nb_loc), kv_loc, kv_loc * G, max_ctx, stream)
+    cfg, fkv = build_handle(P, dict(c, batch=nb_loc, n_layers=n_inst), kv_loc, kv_loc * G, max_ctx, stream)
     t_alloc = time.time() - t0
     K = cfg.K
     p = 32
     # ---- prefill every layer (GEN-S keys, seeded from global ids, identical for any world size)
     t0 = time.time()
     with torch.cuda.stream(stream):
-        for layer in range(n_layers):
+        for layer in range(n_inst):
             k, v = synth.gen_prefill(nb, n_kv, d, p, c["ctx"], c["sink"] // p, K, seed, layer, device=dev, **gkw)
             fkv.append_kv(layer, k[b0:b1, :, kv0:kv0 + kv_loc].contiguous(),
                           v[b0:b1, :, kv0:kv0 + kv_loc].contiguous())
@@ -220,16 +229,21 @@ def run_ours(args, c, rank, world, local_rank):
     stream.synchronize()
     t_prefill = time.time() - t0
     # ---- pre-generate every step's inputs (GEN-Q / GEN-S) outside the timed regions
+    # one query process / token stream per instantiated layer: with layer cycling its successive
+    # occurrences are successive decode steps of that layer (the correction statistics of a model
+    # whose every layer is stepped once per token)
     qps = [synth.QueryProcess(nb, n_qo, n_kv, d, seed, layer, device=dev, event_rate=event_rate, **qkw)
-           for layer in range(n_layers)]
+           for layer in range(n_inst)]
     Qs = torch.empty(total_steps, n_layers, nb_loc, kv_loc * G, d, dtype=torch.bfloat16, device=dev)
     Ks = torch.empty(total_steps, n_layers, nb_loc, 1, kv_loc, d, dtype=torch.bfloat16, device=dev)
     Vs = torch.empty_like(Ks)
     with torch.cuda.stream(stream):
         for i in range(total_steps):
             for layer in range(n_layers):
-                q, _ = qps[layer].next()
-                kn, vn = synth.gen_decode_kv(nb, n_kv, d, p, c["ctx"] + i, seed, layer, device=dev, **gkw)
+                li, occ = layer % n_inst, layer // n_inst  # instantiated layer, occurrence in the step
+                q, _ = qps[li].next()
+                kn, vn = synth.gen_decode_kv(nb, n_kv, d, p, c["ctx"] + i * tok_per_step + occ, seed, li, device=dev,
+                                             **gkw)
                 Qs[i, layer] = q[b0:b1, kv0 * G:(kv0 + kv_loc) * G]
                 Ks[i, layer] = kn[b0:b1, :, kv0:kv0 + kv_loc]
                 Vs[i, layer] = vn[b0:b1, :, kv0:kv0 + kv_loc]
@@ -254,7 +268,13 @@ def run_ours(args, c, rank, world, local_rank):
 
     def one_step(i):
         for layer in range(n_layers):
-            fkv.decode_step(layer, Qs[i, layer], Ks[i, layer], Vs[i, layer], out_loc[layer])
+            fkv.decode_step(layer % n_inst, Qs[i, layer], Ks[i, layer], Vs[i, layer], out_loc[layer])
+
+    def capture(profile=0):
+        if n_inst == n_layers:
+            fkv.step_graph_capture(q_buf, k_buf, v_buf, o_buf, profile=profile)
+        else:
+            fkv.step_graph_capture_cycle(n_layers, q_buf, k_buf, v_buf, o_buf, profile=profile)
 
     # whole-step graph: fixed input/output buffers, one replay per step
     q_buf, k_buf, v_buf = torch.empty_like(Qs[0]), torch.empty_like(Ks[0]), torch.empty_like(Vs[0])
@@ -279,7 +299,7 @@ def run_ours(args, c, rank, world, local_rank):
         step += 1
     fkv.synchronize()
     if not args.eager:
-        fkv.step_graph_capture(q_buf, k_buf, v_buf, o_buf)
+        capture()
         graph_step(step)  # first replay (instantiation warm-up) is a warm-up step too
         step += 1
         fkv.synchronize()
@@ -323,10 +343,10 @@ def run_ours(args, c, rank, world, local_rank):
             b.synchronize()
             return a.elapsed_time(b)
         os.environ["FREEKV_DEBUG_NO_RECALL"] = "1"
-        fkv.step_graph_capture(q_buf, k_buf, v_buf, o_buf)
+        capture()
         ms_nr = timed_steps(exp_steps)
         os.environ.pop("FREEKV_DEBUG_NO_RECALL")
-        fkv.step_graph_capture(q_buf, k_buf, v_buf, o_buf)
+        capture()
         ms_wr = timed_steps(exp_steps)
         exposed = {"exposed_recall_us_per_layer": round((ms_wr - ms_nr) / exp_steps / n_layers * 1e3, 3),
                    "us_per_layer_with_recall": round(ms_wr / exp_steps / n_layers * 1e3, 3),
@@ -347,7 +367,7 @@ def run_ours(args, c, rank, world, local_rank):
 
     def sel_stats():
         nonlocal fetched, fetched_sync, flagged, units, t_unit_tokens, j_pages, t_tok_p1, t_tok_p2, units_p1
-        for layer in range(n_layers):
+        for layer in range(n_inst):
             n_fetch, _ = fkv.get_fetch(layer)
             sel = fkv.get_selection(layer)
             fl = sel["flags"].astype(bool)
@@ -376,7 +396,7 @@ def run_ours(args, c, rank, world, local_rank):
             fkv.synchronize()
             fkv.profile_begin(args.profile_steps * n_layers * 12 + 64)
         else:
-            fkv.step_graph_capture(q_buf, k_buf, v_buf, o_buf, profile=mask)
+            capture(profile=mask)
         for _ in range(args.profile_steps):
             if args.eager:
                 with torch.cuda.stream(stream):
@@ -421,7 +441,7 @@ def run_ours(args, c, rank, world, local_rank):
             for _ in range(8):
                 flush.fill_(1)
                 torch.sum(flush_r, dim=0, out=flush_acc)
-                fkv.select_pages(n_layers - 1, q_last, stream=stream)
+                fkv.select_pages(n_inst - 1, q_last, stream=stream)
         iso_score = fkv.profile_end()
         # (b) the dominant kernel alone: the attention of the last layer over those page lists
         # (idempotent: it commits the same selection), bracketed by CUDA events on its stream
@@ -434,7 +454,7 @@ def run_ours(args, c, rank, world, local_rank):
                     if clean:
                         torch.sum(flush_r, dim=0, out=flush_acc)
                     ea.record(stream)
-                    fkv.sparse_decode_attn(n_layers - 1, q_last, o_tmp, stream=stream)
+                    fkv.sparse_decode_attn(n_inst - 1, q_last, o_tmp, stream=stream)
                     eb.record(stream)
             stream.synchronize()
             if clean:
@@ -447,12 +467,13 @@ def run_ours(args, c, rank, world, local_rank):
                iso_score=iso_score, fetched=fetched, fetched_sync=fetched_sync, flagged=flagged, units=units,
                t_unit_tokens=t_unit_tokens, j_pages=j_pages, t_tok_p1=t_tok_p1, t_tok_p2=t_tok_p2, units_p1=units_p1,
                clocks=clk, link=link, t_alloc=t_alloc, t_prefill=t_prefill, h2d=0, d2h=0, K=K, G=G, kv_loc=kv_loc,
-               nb_loc=nb_loc, seed=seed, exposed=exposed, n_layers=n_layers, comm=comm_info)
+               nb_loc=nb_loc, seed=seed, exposed=exposed, n_layers=n_layers, comm=comm_info, n_inst=n_inst,
+               numa=numa)
     if args.nested:
         fkv.close()
         return res
     if not args.eager:  # plain graph again for the end-to-end pass
-        fkv.step_graph_capture(q_buf, k_buf, v_buf, o_buf)
+        capture()
     # ---- end-to-end pass: inputs from pinned host memory, outputs back to host, every step
     Qh = Qs[step:step + args.steps].cpu().pin_memory()
     Kh = Ks[step:step + args.steps].cpu().pin_memory()
@@ -499,7 +520,7 @@ def run_ours(args, c, rank, world, local_rank):
             in_free[i % 2].record(stream)
         if args.eager:
             for layer in range(n_layers):
-                fkv.decode_step(layer, q_buf[layer], k_buf[layer], v_buf[layer], o_buf[layer])
+                fkv.decode_step(layer % n_inst, q_buf[layer], k_buf[layer], v_buf[layer], o_buf[layer])
         else:
             fkv.step_graph_launch()
         with torch.cuda.stream(stream):
@@ -612,6 +633,9 @@ def main():
                "window": c["window"], "tau": c["tau"], "correction_event_rate": c["event_rate"],
                "parallelism": f"kv-head/batch shard x{args.gpus} + per-layer NCCL all-gather of head outputs", "l2": "inputs larger than L2 (~100 MB per layer, "
                f"{c['n_layers']} layers per step)", "seed": seed}
+    if c.get("l_inst", c["n_layers"]) < c["n_layers"]:
+        cfg_out["l_inst"] = c["l_inst"]
+        cfg_out["layer_cycling"] = f"{c['l_inst']} instantiated layers, virtual layer v runs layer v % {c['l_inst']}"
     if args.impl == "reference":
         if rank != 0:
             return
@@ -628,6 +652,7 @@ def main():
     if rank != 0:
         return
     nb, L = c["batch"], c["n_layers"]
+    Li = r["n_inst"]  # per-layer selection statistics are sampled on the instantiated layers
     tok_s = nb * args.steps / (r["ms"] / 1e3)
     tok_s_e2e = nb * args.steps / (r["ms_e2e"] / 1e3) if r["ms_e2e"] else None
     import json as _j
@@ -647,12 +672,14 @@ def main():
     two_phase = p2_n > 0
     tok1 = r["t_tok_p1"] if two_phase else r["t_unit_tokens"]
     units1 = r["units_p1"] if two_phase else r["units"]
-    attn_bytes = tok1 * 2 * d * 2 + units1 * G * d * 2
+    # with layer cycling the statistics cover the Li instantiated layers and the launches all L
+    cyc = L / Li
+    attn_bytes = (tok1 * 2 * d * 2 + units1 * G * d * 2) * cyc
     attn_gbs = attn_bytes / (attn_ms / 1e3) / 1e9 if attn_ms > 0 else 0.0
-    p2_bytes = r["t_tok_p2"] * 2 * d * 2
+    p2_bytes = r["t_tok_p2"] * 2 * d * 2 * cyc
     # scoring: algorithmic bytes = |J| * 2 * d * 2 B summaries + G * d * 2 B q per unit; isolated
     # launches (select_pages of the last layer, L2 flushed, library event profiler) when available
-    j_per_launch = r["j_pages"] / max(args.profile_steps * L, 1)
+    j_per_launch = r["j_pages"] / max(args.profile_steps * Li, 1)
     if r["iso_score"] and r["iso_score"]["score"][1] > 0:
         sc_ms, sc_n = r["iso_score"]["score"]
         sc_timing = "CUDA events around each score launch (select_pages of the last layer through the C ABI), L2 " \
@@ -665,7 +692,7 @@ def main():
     # background recall: the unflagged units' fetched pages (the corrected units' fetches are read by
     # the attention kernel from the host pool in direct mode: recall_direct below)
     rec_ms = prof["recall_bg"][0] + prof["recall_sync"][0]
-    rec_bytes = r["fetched"] * 2 * 32 * d * 2
+    rec_bytes = r["fetched"] * 2 * 32 * d * 2 * cyc
     rec_gbs = rec_bytes / (rec_ms / 1e3) / 1e9 if rec_ms > 0 else 0.0
     kernels = {k: {"ms_total": round(v[0], 4), "launches": v[1],
                    "us_avg": round(v[0] / v[1] * 1e3, 3) if v[1] else None} for k, v in prof.items()}
@@ -721,13 +748,13 @@ def main():
                         "algorithmic_bytes_per_launch": int(sc_bytes / max(sc_n, 1)), "timing": sc_timing},
         "recall": {"achieved_gbs": round(rec_gbs, 2), "host_link_peak_gbs": round(r["link"], 2) if r["link"] else None,
                    "frac": round(rec_gbs / r["link"], 4) if r["link"] and rec_gbs else None,
-                   "pages_per_layer_step": round(r["fetched"] / max(args.profile_steps * L, 1), 2),
-                   "sync_pages_per_layer_step": round(r["fetched_sync"] / max(args.profile_steps * L, 1), 2),
+                   "pages_per_layer_step": round(r["fetched"] / max(args.profile_steps * Li, 1), 2),
+                   "sync_pages_per_layer_step": round(r["fetched_sync"] / max(args.profile_steps * Li, 1), 2),
                    "mechanism": "background recall kernel: TMA bulk copies (cp.async.bulk) from the pinned, "
                                 "device-mapped host pool into the free slots, on a low-priority stream; bytes = the "
                                 "unflagged units' fetched pages"},
-        "recall_direct": {"pages_per_layer_step": round(r["fetched_sync"] / max(args.profile_steps * L, 1), 2),
-                          "achieved_gbs": round(r["fetched_sync"] * 2 * 32 * d * 2 / (attn_ms / 1e3) / 1e9, 2)
+        "recall_direct": {"pages_per_layer_step": round(r["fetched_sync"] / max(args.profile_steps * Li, 1), 2),
+                          "achieved_gbs": round(r["fetched_sync"] * 2 * 32 * d * 2 * cyc / (attn_ms / 1e3) / 1e9, 2)
                           if attn_ms > 0 and r["fetched_sync"] else None,
                           "host_link_peak_gbs": round(r["link"], 2) if r["link"] else None,
                           "mechanism": "corrected units' fetched pages read by the attention kernel (2D TMA from the "
@@ -745,6 +772,7 @@ def main():
         "execution": "eager per-layer C-ABI calls" if args.eager else "whole-step CUDA graphs (compute + recall)",
         "clocks": r["clocks"],
         "comm": r["comm"],
+        "host_pool_numa": r["numa"],
         "setup_s": {"alloc_pin": round(r["t_alloc"], 1), "prefill": round(r["t_prefill"], 1)},
     }
     if args.gen != "S" or args.full_refresh or args.n_layers is not None:

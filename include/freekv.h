@@ -175,6 +175,14 @@ freekv_status freekv_decode_step(freekv_handle* h, int32_t layer, const void* q,
 freekv_status freekv_step_graph_capture(freekv_handle* h, const void* q_all, const void* k_all,
                                         const void* v_all, float* out_all, int32_t profile);
 freekv_status freekv_step_graph_launch(freekv_handle* h);
+/* The same with n_virtual >= n_layers virtual layers: virtual layer v runs layer v % n_layers
+ * with q_all / k_all / v_all / out_all slices v (buffers sized for n_virtual) -- L_inst
+ * cycling, so an 80-layer model's step is timed with a handle of L_inst instantiated layers
+ * whose host KV fits (SURVEY §7 hard part 9).  Each instantiated layer then appends
+ * n_virtual / n_layers tokens per step. */
+freekv_status freekv_step_graph_capture_cycle(freekv_handle* h, int32_t n_virtual, const void* q_all,
+                                              const void* k_all, const void* v_all, float* out_all,
+                                              int32_t profile);
 /* With profile != 0 at capture, the selected kernel nodes are bracketed by event-record
  * nodes; after a replay has completed, this returns per kernel class the summed
  * device milliseconds and launch counts of that replay (classes as in

@@ -104,6 +104,7 @@ struct freekv_handle {
     bool capturing = false;
     cudaGraphExec_t g_compute = nullptr, g_recall = nullptr;
     std::vector<Rec> graph_recs;  // event pairs captured into the step graph (profile mode)
+    std::vector<int> graph_tokens;  // tokens one replay appends to each layer (> 1 with layer cycling)
     // multi-GPU: this rank's NCCL communicator over the kv-head / batch shards and
     // the gathered per-layer output [n_layers][n_ranks][nb][n_qo][d] fp32 (the one exchange step)
     ncclComm_t comm = nullptr;
@@ -1047,12 +1048,22 @@ static void drop_graphs(freekv_handle* h) {
 freekv_status freekv_step_graph_capture(freekv_handle* h, const void* q_all, const void* k_all, const void* v_all,
                                         float* out_all, int32_t profile) {
     if (!h) return fail(FREEKV_EINVAL, "handle is NULL");
+    return freekv_step_graph_capture_cycle(h, h->cfg.n_layers, q_all, k_all, v_all, out_all, profile);
+}
+
+freekv_status freekv_step_graph_capture_cycle(freekv_handle* h, int32_t n_virtual, const void* q_all,
+                                              const void* k_all, const void* v_all, float* out_all,
+                                              int32_t profile) {
+    if (!h) return fail(FREEKV_EINVAL, "handle is NULL");
+    if (n_virtual < h->cfg.n_layers) return fail(FREEKV_EINVAL, "n_virtual < n_layers");
+    if (n_virtual != h->cfg.n_layers && (!h->one_graph || h->spec))
+        return fail(FREEKV_EUNSUPPORTED, "layer cycling needs the serial direct-mode step");
     if (!q_all || !k_all || !v_all || !out_all) return fail(FREEKV_EINVAL, "NULL buffer");
     if (h->prof) return fail(FREEKV_ESTATE, "capture while profiling");
     h->no_bg_recall = env_on("FREEKV_DEBUG_NO_RECALL");
     h->graph_recs.clear();
     if (profile) {  // event pool: <= 8 kernels per layer, 2 events each
-        freekv_status ps = freekv_profile_begin(h, h->cfg.n_layers * 8 + 8);
+        freekv_status ps = freekv_profile_begin(h, n_virtual * 8 + 8);
         if (ps != FREEKV_OK) return ps;
         h->prof_mask = profile == 1 ? ~0u : (uint32_t)profile;
     }
@@ -1067,11 +1078,19 @@ freekv_status freekv_step_graph_capture(freekv_handle* h, const void* q_all, con
     cudaGraph_t gc = nullptr, gr = nullptr;
     h->capturing = true;
     cudaError_t e = cudaStreamBeginCapture(h->cs, cudaStreamCaptureModeThreadLocal);
-    for (int l = 0; l < h->cfg.n_layers && e == cudaSuccess && st == FREEKV_OK; ++l) {
-        const uint8_t* q = (const uint8_t*)q_all + q_stride * l;
-        const uint8_t* k = (const uint8_t*)k_all + kv_stride * l;
-        const uint8_t* v = (const uint8_t*)v_all + kv_stride * l;
-        st = do_layer_step(h, l, q, k, v, out_all + o_stride * l);
+    for (int vl = 0; vl < n_virtual && e == cudaSuccess && st == FREEKV_OK; ++vl) {
+        // virtual layer vl runs instantiated layer vl % n_layers (L_inst cycling for models whose
+        // host KV does not fit: SURVEY §7 hard part 9); a layer met again in the same graph first
+        // joins its previous background recall (its slots are this occurrence's resident set)
+        const int l = vl % h->cfg.n_layers;
+        if (vl >= h->cfg.n_layers) e = cudaStreamWaitEvent(h->cs, h->ev_recall[l], 0);
+        if (e != cudaSuccess) break;
+        if (vl == 0) h->graph_tokens.assign(h->cfg.n_layers, 0);
+        h->graph_tokens[l] += 1;
+        const uint8_t* q = (const uint8_t*)q_all + q_stride * vl;
+        const uint8_t* k = (const uint8_t*)k_all + kv_stride * vl;
+        const uint8_t* v = (const uint8_t*)v_all + kv_stride * vl;
+        st = do_layer_step(h, l, q, k, v, out_all + o_stride * vl);
     }
     if (h->one_graph) {  // join every layer's recall branch (and the corrected units' chain)
         for (int l = 0; l < h->cfg.n_layers && e == cudaSuccess && st == FREEKV_OK; ++l)
@@ -1142,12 +1161,13 @@ freekv_status freekv_step_graph_profile(freekv_handle* h, float* ms, int32_t* la
 freekv_status freekv_step_graph_launch(freekv_handle* h) {
     if (!h) return fail(FREEKV_EINVAL, "handle is NULL");
     if (!h->g_compute || (!h->g_recall && !h->one_graph)) return fail(FREEKV_ESTATE, "no captured step graph");
+    const auto tok = [&](int l) { return l < (int)h->graph_tokens.size() ? h->graph_tokens[l] : 1; };
     for (int l = 0; l < h->cfg.n_layers; ++l)
-        if (h->ctx_host[l] + 1 > h->D.max_ctx) return fail(FREEKV_ERANGE, "context would exceed max_ctx_tokens");
+        if (h->ctx_host[l] + tok(l) > h->D.max_ctx) return fail(FREEKV_ERANGE, "context would exceed max_ctx_tokens");
     FKV_CUDA(cudaGraphLaunch(h->g_compute, h->cs));
     if (h->g_recall) FKV_CUDA(cudaGraphLaunch(h->g_recall, h->rs));
     for (int l = 0; l < h->cfg.n_layers; ++l) {
-        h->ctx_host[l] += 1;
+        h->ctx_host[l] += tok(l);
         // one graph: its recall branches are joined into its end, so the graph's completion
         // on cs stands for them (for callers that later use other streams)
         if (h->one_graph) FKV_CUDA(cudaEventRecord(h->ev_recall[l], h->cs));

@@ -28,7 +28,7 @@ EXPORTED = [
     "freekv_get_context", "freekv_get_dims", "freekv_synchronize", "freekv_destroy",
     "freekv_last_error", "freekv_abi_version", "freekv_profile_begin", "freekv_profile_end",
     "freekv_step_graph_capture", "freekv_step_graph_launch", "freekv_step_graph_profile", "freekv_debug_trace",
-    "freekv_get_step_stats", "freekv_comm_unique_id", "freekv_comm_init", "freekv_set_gather_output",
+    "freekv_get_step_stats", "freekv_step_graph_capture_cycle", "freekv_comm_unique_id", "freekv_comm_init", "freekv_set_gather_output",
 ]
 KERNEL_CLASSES = ["append", "score", "select_finalize", "recall_sync", "recall_bg", "attn_split", "attn_combine",
                   "attn_split_phase2", "prep", "score_bg", "select_finalize_bg"]
@@ -140,6 +140,7 @@ def load_library():
             "freekv_profile_begin": [vp, i32],
             "freekv_profile_end": [vp, vp, vp],
             "freekv_step_graph_capture": [vp, vp, vp, vp, vp, i32],
+            "freekv_step_graph_capture_cycle": [vp, i32, vp, vp, vp, vp, i32],
             "freekv_step_graph_profile": [vp, vp, vp],
             "freekv_debug_trace": [vp, vp, sz],
             "freekv_step_graph_launch": [vp],
@@ -236,6 +237,12 @@ class FreeKV:
         [L][nb][1][n_kv][d] and writing out_all [L][nb][n_qo][d] (fixed device buffers)."""
         _check(self.L.freekv_step_graph_capture(self.h, q_all.data_ptr(), k_all.data_ptr(), v_all.data_ptr(),
                                                 out_all.data_ptr(), int(profile)))
+        self._graph_bufs = (q_all, k_all, v_all, out_all)
+
+    def step_graph_capture_cycle(self, n_virtual, q_all, k_all, v_all, out_all, profile=False):
+        """L_inst cycling: n_virtual virtual layers over the handle's n_layers (buffers [n_virtual]...)."""
+        _check(self.L.freekv_step_graph_capture_cycle(self.h, n_virtual, q_all.data_ptr(), k_all.data_ptr(),
+                                                      v_all.data_ptr(), out_all.data_ptr(), int(profile)))
         self._graph_bufs = (q_all, k_all, v_all, out_all)
 
     def step_graph_launch(self):
