@@ -517,3 +517,56 @@ def test_summarize_pages_matches_oracle():
         for u in range(fkv.U):
             assert np.array_equal(fkv.get_summaries(layer, u, 2, n_off), eng.summ[layer][u, 2:n_off])
     fkv.close()
+
+
+def test_step_graph_layer_cycling_matches_eager():
+    """freekv_step_graph_capture_cycle (L_inst cycling, bench c5): 6 virtual layers over 2
+    instantiated ones -- the graph gives the selections and bit-identical outputs of the eager
+    calls decode_step(v % 2) in the same order, and each replay appends 3 tokens per layer."""
+    _need_gpu()
+    import paper_2505_13109_b200 as P
+    nb, n_kv, G, d, p, L0, steps, n_inst, n_virt = 2, 2, 4, 128, 32, 1200, 4, 2, 6
+    n_qo = G * n_kv
+    mk = lambda: P.FreeKV(P.FreeKVConfig(n_layers=n_inst, batch=nb, n_qo=n_qo, n_kv=n_kv, budget_tokens=256,
+                                         sink_tokens=64, window_tokens=64,
+                                         max_ctx_tokens=L0 + steps * (n_virt // n_inst) + 2))
+    a, b = mk(), mk()
+    dev = a.device
+    seed = 78
+    for layer in range(n_inst):
+        k, v = synth.gen_prefill(nb, n_kv, d, p, L0, 2, a.K, seed, layer, device=dev)
+        torch.cuda.synchronize()
+        a.append_kv(layer, k, v)
+        b.append_kv(layer, k, v)
+        a.synchronize()
+        b.synchronize()
+    qps = [synth.QueryProcess(nb, n_qo, n_kv, d, seed, l, device=dev, event_rate=0.3) for l in range(n_inst)]
+    Q = torch.empty(steps, n_virt, nb, n_qo, d, dtype=torch.bfloat16, device=dev)
+    Kn = torch.empty(steps, n_virt, nb, 1, n_kv, d, dtype=torch.bfloat16, device=dev)
+    Vn = torch.empty_like(Kn)
+    for i in range(steps):
+        for vl in range(n_virt):
+            li, occ = vl % n_inst, vl // n_inst
+            q, _ = qps[li].next()
+            kn, vn = synth.gen_decode_kv(nb, n_kv, d, p, L0 + i * (n_virt // n_inst) + occ, seed, li, device=dev)
+            Q[i, vl], Kn[i, vl], Vn[i, vl] = q, kn, vn
+    torch.cuda.synchronize()
+    qb, kb, vb = torch.empty_like(Q[0]), torch.empty_like(Kn[0]), torch.empty_like(Vn[0])
+    ob = torch.empty(n_virt, nb, n_qo, d, dtype=torch.float32, device=dev)
+    b.step_graph_capture_cycle(n_virt, qb, kb, vb, ob)
+    oa = torch.empty(n_virt, nb, n_qo, d, dtype=torch.float32, device=dev)
+    for i in range(steps):
+        with torch.cuda.stream(b.stream):
+            qb.copy_(Q[i]); kb.copy_(Kn[i]); vb.copy_(Vn[i])
+        b.step_graph_launch()
+        b.synchronize()
+        for vl in range(n_virt):
+            a.decode_step(vl % n_inst, Q[i, vl], Kn[i, vl], Vn[i, vl], oa[vl])
+        a.synchronize()
+        assert torch.equal(oa, ob), i
+        for l in range(n_inst):
+            sa, sb = a.get_selection(l), b.get_selection(l)
+            assert np.array_equal(sa["pages"], sb["pages"]) and np.array_equal(sa["flags"], sb["flags"]), (i, l)
+            assert a.context(l) == b.context(l) == L0 + (i + 1) * (n_virt // n_inst)
+    a.close()
+    b.close()
