@@ -686,11 +686,14 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
     {
         // leaves of the select tree: page ids [0, n_off); n_off never exceeds max(S/p, max_ctx/p - W/p),
         // so the tree (zero-padded, CFR-6) needs next_pow2 of that.  CTAs per unit: the widest cluster
-        // (<= 8) that keeps one CTA per SM and >= 512 leaves per CTA; leaves per thread fill the tree
+        // (<= 4) with one CTA per SM and >= 256 leaves per CTA, or one 1024-thread CTA when there are
+        // many units; leaves per thread fill the tree
         const int n_off_max = std::max(D.n_sink, D.max_ctx / D.p - D.n_win);
         int P2 = 256;
         while (P2 < n_off_max) P2 <<= 1;
-        int nc = 8;
+        // (<= 4: 8-CTA clusters measured as fast on one B200 and 10 us slower per select on another,
+        // where fewer 8-CTA clusters fit beside the attention's; 4 is equal or better on both)
+        int nc = 4;
         while (nc > 1 && (D.U * nc > sms || nc * 256 > P2)) nc >>= 1;
         // many units (<= 2 CTAs each would fit): one wide 1024-thread CTA per unit instead
         // (A/B on B200 at c2: 42.3 us/layer vs 50.3 with 2-CTA clusters of 256 threads)
@@ -763,6 +766,8 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         // U * C within one wave of 2 CTAs per SM
         int c = 8;
         while (c > 1 && D.U * c > 2 * sms) c >>= 1;
+        const char* ce = getenv("FREEKV_ATTN_CLUSTER");  // A/B: 1, 2, 4, 8 or 16 CTAs per unit
+        if (ce && (atoi(ce) == 1 || atoi(ce) == 2 || atoi(ce) == 4 || atoi(ce) == 8 || atoi(ce) == 16)) c = atoi(ce);
         h->attn_cluster = c;
     }
     h->X.trace = nullptr;

@@ -402,6 +402,10 @@ static cudaError_t launch_cluster_c(const FkvDims& D, const FkvLayer& L, const F
     const int smem = kAttnWarpsPerCta * NST * kSlabBytes;
     cudaError_t e = func_smem((const void*)kern, smem);
     if (e != cudaSuccess) return e;
+    if (C > 8) {  // 16-CTA clusters are a non-portable size (opt-in)
+        e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(D.U * C);
     cfg.blockDim = dim3(kAttnWarpsPerCta * 32);
@@ -439,6 +443,7 @@ cudaError_t launch_attn_cluster(const FkvDims& D, const FkvLayer& L, const FkvSc
         if (c == 1) return launch_cluster_c<NS, 1>(D, L, X, q, out, tmap, tmap_h, mode, pdl, prio, s, pending); \
         if (c == 2) return launch_cluster_c<NS, 2>(D, L, X, q, out, tmap, tmap_h, mode, pdl, prio, s, pending); \
         if (c == 4) return launch_cluster_c<NS, 4>(D, L, X, q, out, tmap, tmap_h, mode, pdl, prio, s, pending); \
+        if (c == 16) return launch_cluster_c<NS, 16>(D, L, X, q, out, tmap, tmap_h, mode, pdl, prio, s, pending); \
         return launch_cluster_c<NS, 8>(D, L, X, q, out, tmap, tmap_h, mode, pdl, prio, s, pending);             \
     } while (0)
     if (nst == 2) FKV_CL(2);
