@@ -570,3 +570,70 @@ def test_step_graph_layer_cycling_matches_eager():
             assert a.context(l) == b.context(l) == L0 + (i + 1) * (n_virt // n_inst)
     a.close()
     b.close()
+
+
+def test_step_graph_back_to_back_no_host_sync():
+    """Step-graph replays issued back to back with no host synchronisation between them (inputs
+    staged and outputs saved by stream-ordered copies): the same outputs, bit for bit, and the
+    same final selections as synchronised eager steps -- the stream / event ordering alone
+    (recall joins, PDL chains) carries every dependency between steps."""
+    _need_gpu()
+    import paper_2505_13109_b200 as P
+    nb, n_kv, G, d, p, L0, steps, n_layers = 2, 2, 4, 128, 32, 1300, 8, 3
+    n_qo = G * n_kv
+    mk = lambda: P.FreeKV(P.FreeKVConfig(n_layers=n_layers, batch=nb, n_qo=n_qo, n_kv=n_kv, budget_tokens=256,
+                                         sink_tokens=64, window_tokens=64, max_ctx_tokens=L0 + steps + 2))
+    a, b, c = mk(), mk(), mk()
+    dev = a.device
+    seed = 91
+    for layer in range(n_layers):
+        k, v = synth.gen_prefill(nb, n_kv, d, p, L0, 2, a.K, seed, layer, device=dev)
+        torch.cuda.synchronize()
+        a.append_kv(layer, k, v)
+        b.append_kv(layer, k, v)
+        c.append_kv(layer, k, v)
+    a.synchronize()
+    b.synchronize()
+    c.synchronize()
+    qps = [synth.QueryProcess(nb, n_qo, n_kv, d, seed, l, device=dev, event_rate=0.3) for l in range(n_layers)]
+    Q = torch.empty(steps, n_layers, nb, n_qo, d, dtype=torch.bfloat16, device=dev)
+    Kn = torch.empty(steps, n_layers, nb, 1, n_kv, d, dtype=torch.bfloat16, device=dev)
+    Vn = torch.empty_like(Kn)
+    for i in range(steps):
+        for l in range(n_layers):
+            q, _ = qps[l].next()
+            kn, vn = synth.gen_decode_kv(nb, n_kv, d, p, L0 + i, seed, l, device=dev)
+            Q[i, l], Kn[i, l], Vn[i, l] = q, kn, vn
+    torch.cuda.synchronize()
+    qb, kb, vb = torch.empty_like(Q[0]), torch.empty_like(Kn[0]), torch.empty_like(Vn[0])
+    ob = torch.empty(n_layers, nb, n_qo, d, dtype=torch.float32, device=dev)
+    saved = torch.empty(steps, n_layers, nb, n_qo, d, dtype=torch.float32, device=dev)
+    b.step_graph_capture(qb, kb, vb, ob)
+    for i in range(steps):  # no host sync inside this loop
+        with torch.cuda.stream(b.stream):
+            qb.copy_(Q[i]); kb.copy_(Kn[i]); vb.copy_(Vn[i])
+        b.step_graph_launch()
+        with torch.cuda.stream(b.stream):
+            saved[i].copy_(ob)
+    # eager calls, also without host sync (stream-ordered output saves)
+    saved_c = torch.empty_like(saved)
+    c.stream.wait_stream(torch.cuda.current_stream())
+    for i in range(steps):
+        for l in range(n_layers):
+            c.decode_step(l, Q[i, l], Kn[i, l], Vn[i, l], saved_c[i, l])
+    b.synchronize()
+    c.synchronize()
+    oa = torch.empty(nb, n_qo, d, dtype=torch.float32, device=dev)
+    for i in range(steps):
+        for l in range(n_layers):
+            a.decode_step(l, Q[i, l], Kn[i, l], Vn[i, l], oa)
+            a.synchronize()
+            assert torch.equal(oa, saved[i, l]), (i, l)
+            assert torch.equal(oa, saved_c[i, l]), (i, l)
+    for l in range(n_layers):
+        sa, sb, sc = a.get_selection(l), b.get_selection(l), c.get_selection(l)
+        assert np.array_equal(sa["pages"], sb["pages"]) and np.array_equal(sa["flags"], sb["flags"]), l
+        assert np.array_equal(sa["pages"], sc["pages"]) and np.array_equal(sa["flags"], sc["flags"]), l
+    a.close()
+    b.close()
+    c.close()

@@ -19,7 +19,7 @@ WANT = [
     ("score c2", r"fkv_score_kernelILi4ELi4E"),
     ("score c3", r"fkv_score_kernelILi7ELi4E"),
     ("select c2", r"fkv_select_kernelILi1ELi4ELi1ELi1024E"),
-    ("select c3", r"fkv_select_kernelILi2ELi8ELi8ELi256E"),
+    ("select c3", r"fkv_select_kernelILi4ELi8ELi4ELi256E"),
     ("attention c2", r"fkv_attn_cluster_kernelILi3ELi4E"),
     ("attention c3", r"fkv_attn_cluster_kernelILi3ELi8E"),
     ("recall", r"fkv_recall_kernel"),
