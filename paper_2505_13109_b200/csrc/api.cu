@@ -478,7 +478,9 @@ freekv_status do_layer_step_core(freekv_handle* h, int layer, const void* q, con
         // new context length).  A window of >= 1 page keeps the page the append completes out of
         // this step's candidates, so the append may run beside the scoring.
         if (!h->capturing) h->ctx_host[layer] += 1;
-        freekv_status st = do_select(h, layer, q, nullptr, nullptr, cs, 1, 1, k_new, v_new);
+        // page lists only for the corrected units when the others attend R early (they build theirs)
+        const int list_all = (D.attn_early && !getenv("FREEKV_LIST_ALL")) ? 0 : 1;
+        freekv_status st = do_select(h, layer, q, nullptr, nullptr, cs, 1, list_all, k_new, v_new);
         if (st != FREEKV_OK) return st;
         return do_step_tail(h, layer, q, out, 1);
     }
@@ -787,8 +789,12 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         h->D.full_refresh = (fr && fr[0] == '1') ? 1 : 0;
         const char* ae = getenv("FREEKV_ATTN_EARLY");
         h->D.attn_early = ae ? atoi(ae) : 1;
-        const char* sp = getenv("FREEKV_SCORE_PPT");
-        h->D.score_ppt = sp ? atoi(sp) : 4;
+        // score CTAs of 8 warps (1024 pages) when there are many units with few (<= 2048) candidate
+        // pages each (A/B on B200, c2: 40.4 vs 41.7 us/layer); with more pages per unit the 4-warp
+        // CTAs' larger grid wins (c3 44.0 vs 44.9, c5 145 vs 162); FREEKV_SCORE_WARPS=4|8
+        const char* sw = getenv("FREEKV_SCORE_WARPS");
+        const int n_off_cap = std::max(h->D.n_sink, h->D.max_ctx / h->D.p - h->D.n_win);
+        h->D.score_warps = sw ? (atoi(sw) == 8 ? 8 : 4) : ((h->D.U >= 64 && n_off_cap <= 2048) ? 8 : 4);
     }
     {
         const char* sr = getenv("FREEKV_SERIAL_RECALL");

@@ -15,8 +15,11 @@ constexpr int kMaxG = 8;        // GQA group size supported (Llama 4, Qwen 7, 70
 // pages scored by one score CTA (score.cu): the throughput variant (4 pages per thread) of the
 // serial step and the side chain, and the latency variant (1 page per thread, 4x more CTAs) that
 // scores the corrected units on the critical path
-constexpr int kScoreCtaPages = 512;
-constexpr int kScoreCtaPagesFast = 128;
+#ifndef FKV_SC_WARPS
+#define FKV_SC_WARPS 4  // warps per score CTA (A/B builds: -DFKV_SC_WARPS=2)
+#endif
+constexpr int kScoreCtaPages = FKV_SC_WARPS * 128;
+constexpr int kScoreCtaPagesFast = FKV_SC_WARPS * 32;
 
 struct FkvDims {
     int nb, n_qo, n_kv, G, d, p;
@@ -32,7 +35,7 @@ struct FkvDims {
     int mode;
     int full_refresh; // diagnostics (env FREEKV_DEBUG_FULL_REFRESH=1): no slot reuse, all pages re-fetched
     int attn_early;   // serial step: uncorrected units attend before the wait for the select (FREEKV_ATTN_EARLY)
-    int score_ppt;    // pages per thread of the score kernel (parts -1/-2): 1, 2 or 4 (env FREEKV_SCORE_PPT)
+    int score_warps;  // warps per score CTA (parts -1/-2): 4 or 8 (1024 pages per CTA)
     int pool;         // FREEKV_POOL_* group pooling of the selection (f3); 0 = MeanS
     int corr_pool;    // 0 = mean of the cosines, 1 = corrected when the least similar head is below tau
     float tau;

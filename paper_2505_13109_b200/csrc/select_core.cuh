@@ -290,15 +290,18 @@ __device__ __forceinline__ void topk_keys(const FkvDims& D, int rank, int n_off,
     bool cand[LPT];
 #pragma unroll
     for (int l = 0; l < LPT; ++l) cand[l] = jb + l >= D.n_sink && jb + l < n_off;
-    // ---- exact K-th largest key: radix passes of 12, 12 and 8 bits over the cluster-summed
+    // ---- exact K-th largest key: radix passes of 12, 12 and 7 bits over the cluster-summed
     // histogram; as soon as the boundary bin holds <= 32 keys, they are ranked directly
     uint32_t prefix = 0u, mask = 0u, T = 0u;
     int k_rem = K;
     bool resolved = false;
 #pragma unroll 1
     for (int pass = 0; pass < 3; ++pass) {
-        const int shift = pass == 0 ? 20 : (pass == 1 ? 8 : 0);
-        const int nbits = pass == 2 ? 8 : 12;
+        // keys are bits of non-negative floats (bit 31 always 0): the digits cover bits 30..19,
+        // 18..7 and 6..0, so the first one is exponent + 4 mantissa bits (1/16-octave bins) and
+        // the boundary bin usually holds <= 32 keys after it
+        const int shift = pass == 0 ? 19 : (pass == 1 ? 7 : 0);
+        const int nbits = pass == 2 ? 7 : 12;
         const uint32_t dmask = (1u << nbits) - 1u;
         if (pass > 0) {  // fallback passes (rare): every CTA is done reading the histograms
             csync<NC>();

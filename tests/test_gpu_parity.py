@@ -637,3 +637,12 @@ def test_step_graph_back_to_back_no_host_sync():
     a.close()
     b.close()
     c.close()
+
+
+@pytest.mark.parametrize("warps", ["4", "8"])
+def test_parity_score_cta_warps(warps, monkeypatch):
+    """Score CTAs of 4 or 8 warps (512 / 1024 pages per CTA; 8 is the default for >= 64 units):
+    bit-identical scores, selections and fetch lists, ragged last item."""
+    monkeypatch.setenv("FREEKV_SCORE_WARPS", warps)
+    run_parity(G=4, n_kv=2, batch=2, page=32, L0=40000, steps=3, n_layers=1)
+    run_parity(G=7, n_kv=1, batch=2, page=32, L0=3000, steps=3, n_layers=1)
