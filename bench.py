@@ -209,7 +209,10 @@ def run_ours(args, c, rank, world, local_rank):
     # warm, timed, exposed-recall pair, profiled x2, e2e
     total_steps = args.warmup + 1 + args.steps + 2 * (exp_steps + 2) + 2 * args.profile_steps + \
         (0 if args.nested else args.steps)
-    max_ctx = c["ctx"] + total_steps * tok_per_step + 1
+    # the prefill leaves room for every step of the run, so the context never exceeds the config's
+    # (the select tree is sized for max_ctx: P2 = next_pow2(max pages))
+    L0 = c["ctx"] - total_steps * tok_per_step
+    max_ctx = c["ctx"] + 1
     stream = torch.cuda.Stream(dev, priority=-1)  # compute outranks the background recall stream
     from paper_2505_13109_b200.numa import bind_to_gpu_node
     numa = bind_to_gpu_node(local_rank)  # the pinned host shard below lands on the GPU's NUMA node
@@ -222,7 +225,7 @@ def run_ours(args, c, rank, world, local_rank):
     t0 = time.time()
     with torch.cuda.stream(stream):
         for layer in range(n_inst):
-            k, v = synth.gen_prefill(nb, n_kv, d, p, c["ctx"], c["sink"] // p, K, seed, layer, device=dev, **gkw)
+            k, v = synth.gen_prefill(nb, n_kv, d, p, L0, c["sink"] // p, K, seed, layer, device=dev, **gkw)
             fkv.append_kv(layer, k[b0:b1, :, kv0:kv0 + kv_loc].contiguous(),
                           v[b0:b1, :, kv0:kv0 + kv_loc].contiguous())
             del k, v
@@ -242,7 +245,7 @@ def run_ours(args, c, rank, world, local_rank):
             for layer in range(n_layers):
                 li, occ = layer % n_inst, layer // n_inst  # instantiated layer, occurrence in the step
                 q, _ = qps[li].next()
-                kn, vn = synth.gen_decode_kv(nb, n_kv, d, p, c["ctx"] + i * tok_per_step + occ, seed, li, device=dev,
+                kn, vn = synth.gen_decode_kv(nb, n_kv, d, p, L0 + i * tok_per_step + occ, seed, li, device=dev,
                                              **gkw)
                 Qs[i, layer] = q[b0:b1, kv0 * G:(kv0 + kv_loc) * G]
                 Ks[i, layer] = kn[b0:b1, :, kv0:kv0 + kv_loc]
@@ -629,7 +632,9 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     seed = args.seed if args.seed is not None else 250513109 + 1 + list(CONFIGS).index(args.config)
     cfg_out = {"workload": c["workload"], "n_layers": c["n_layers"], "batch": c["batch"], "n_qo": c["n_qo"],
-               "n_kv": c["n_kv"], "ctx": c["ctx"], "page": 32, "budget": c["budget"], "sink": c["sink"],
+               "n_kv": c["n_kv"], "ctx": c["ctx"], "context": "prefill of ctx minus every step of the run "
+               "(warm-up, timed, profiled, end to end), so the decode contexts end at ctx",
+               "page": 32, "budget": c["budget"], "sink": c["sink"],
                "window": c["window"], "tau": c["tau"], "correction_event_rate": c["event_rate"],
                "parallelism": f"kv-head/batch shard x{args.gpus} + per-layer NCCL all-gather of head outputs", "l2": "inputs larger than L2 (~100 MB per layer, "
                f"{c['n_layers']} layers per step)", "seed": seed}

@@ -693,8 +693,10 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         const int n_off_max = std::max(D.n_sink, D.max_ctx / D.p - D.n_win);
         int P2 = 256;
         while (P2 < n_off_max) P2 <<= 1;
-        // (<= 4: 8-CTA clusters measured as fast on one B200 and 10 us slower per select on another,
-        // where fewer 8-CTA clusters fit beside the attention's; 4 is equal or better on both)
+        // (<= 4: at c3 4- and 8-CTA clusters measure the same, 44.6 / 44.4 us per layer; the smaller
+        // cluster leaves the attention's clusters more room.)  The tree is sized for max_ctx: a handle
+        // whose page count crosses a power of two runs the doubled tree from its first step (c3 with
+        // max_ctx just above 4096 pages: select 35-41 us instead of 22)
         int nc = 4;
         while (nc > 1 && (D.U * nc > sms || nc * 256 > P2)) nc >>= 1;
         // many units (<= 2 CTAs each would fit): one wide 1024-thread CTA per unit instead
