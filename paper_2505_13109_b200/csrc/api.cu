@@ -82,8 +82,14 @@ struct freekv_handle {
     std::vector<cudaEvent_t> ev_pre;  // fork point of each layer's side chain (after its pre kernel)
     int prio_hi = 0;             // kernel priority of the critical path (pre, attention)
     int attn_cluster = 1;        // CTAs per unit of the clustered attention
-    int sel_nc = 1, sel_lpt = 1; // select: CTAs per unit (cluster), leaves per thread (CFR-6 tree)
-    int sel_nt = 256;            // select: threads per CTA (256, or 1024 for one CTA per unit)
+    int sms = 148;               // SM count of the handle's device
+    int graph_p2 = 0;            // the captured step graph's select tree (leaves)
+    int graph_ctx_limit = 0;     // ... covers contexts up to this many tokens (re-captured beyond)
+    struct {
+        int n_virtual = 0, profile = 0;
+        const void *q = nullptr, *k = nullptr, *v = nullptr;
+        float* out = nullptr;
+    } cap;                       // arguments of the last step-graph capture
     int fsel_nc = 1, fsel_lpt = 1;  // the corrected units' select on the critical path (speculative step)
     int bsel_nc = 1, bsel_lpt = 1;  // the other units' select in the side chain (speculative step)
     std::vector<int> ctx_host;
@@ -289,6 +295,49 @@ static bool env_on(const char* name) {
     return v && v[0] == '1';
 }
 
+// The select kernel's instance for a CFR-6 tree of P2 leaves (page ids [0, P2), zero-padded; any
+// P2 >= next_pow2(n_off) gives the same Z).  CTAs per unit: the widest cluster (<= 4) with one CTA
+// per SM and >= 256 leaves per CTA, or one 1024-thread CTA when there are many units; leaves per
+// thread fill the tree.  (<= 4: at c3 4- and 8-CTA clusters measure the same, 44.6 / 44.4 us per
+// layer; the smaller cluster leaves the attention's clusters more room.)  Returns false above 8192
+// leaves.
+struct SelCfg {
+    int nc, lpt, nt;
+};
+static bool select_config(const FkvDims& D, int sms, int P2, SelCfg* out) {
+    int nc = 4;
+    while (nc > 1 && (D.U * nc > sms || nc * 256 > P2)) nc >>= 1;
+    // many units (<= 2 CTAs each would fit): one wide 1024-thread CTA per unit instead
+    // (A/B on B200 at c2: 42.3 us/layer vs 50.3 with 2-CTA clusters of 256 threads)
+    if (nc <= 2 && P2 >= 1024 && P2 / 1024 <= 8) nc = 1;
+    const char* ne = getenv("FREEKV_SELECT_NC");  // A/B: force the cluster width (1, 2, 4, 8)
+    if (ne && (atoi(ne) == 1 || atoi(ne) == 2 || atoi(ne) == 4 || atoi(ne) == 8)) nc = atoi(ne);
+    int lpt = std::max(1, P2 / (nc * 256));
+    if (nc > 1 && lpt > 4) {  // cluster instances are built for <= 4 leaves per thread
+        nc = 1;
+        lpt = P2 / 256;
+    }
+    if (lpt > 32) return false;
+    // one 1024-thread CTA per unit when there are enough units to fill the GPU with clusters of
+    // one (the wide CTA's short per-thread chains beat the 256-thread CTA and a 2-CTA cluster at
+    // c2); FREEKV_SELECT_NT=256|512|1024 overrides
+    const char* nte = getenv("FREEKV_SELECT_NT");
+    int nt = (nc == 1 && P2 >= 1024 && P2 / 1024 <= 8) ? 1024 : 256;
+    if (nte && (atoi(nte) == 256 || atoi(nte) == 512 || atoi(nte) == 1024)) nt = atoi(nte);
+    if (nt > 256 && (nc != 1 || P2 < nt || P2 / nt > 8)) nt = 256;
+    if (nt > 256) lpt = P2 / nt;
+    *out = SelCfg{nc, lpt, nt};
+    return true;
+}
+
+// Leaves of the tree for contexts up to ctx tokens
+static int tree_leaves(const FkvDims& D, int ctx) {
+    const int n_off = std::max(D.n_sink, ctx / D.p - D.n_win);
+    int P2 = 256;
+    while (P2 < n_off) P2 <<= 1;
+    return P2;
+}
+
 freekv_status do_select(freekv_handle* h, int layer, const void* q, int32_t* pages_out, uint8_t* corr_out,
                         cudaStream_t s, int flag_src, int list_all, const void* k_new = nullptr,
                         const void* v_new = nullptr) {
@@ -313,8 +362,12 @@ freekv_status do_select(freekv_handle* h, int layer, const void* q, int32_t* pag
                                 0, s, (const uint16_t*)k_new, (const uint16_t*)v_new);
         }));
     FKV_CUDA(timed(h, K_FINALIZE, s, [&] {
+        // the smallest CFR-6 tree covering this step's candidates (the graph's: its capture's)
+        const int P2 = h->capturing ? h->graph_p2 : tree_leaves(h->D, h->ctx_host[layer]);
+        SelCfg sc;
+        if (!select_config(h->D, h->sms, P2, &sc)) return cudaErrorInvalidValue;
         return launch_select(h->D, L, h->X, (const uint16_t*)q, pages_out, corr_out, flag_src, list_all, -1,
-                             h->sel_nc, h->sel_lpt, h->pdl, 0, s, pending, h->sel_nt);
+                             sc.nc, sc.lpt, h->pdl, 0, s, pending, sc.nt);
     }));
     return FREEKV_OK;
 }
@@ -686,44 +739,15 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
     {
-        // leaves of the select tree: page ids [0, n_off); n_off never exceeds max(S/p, max_ctx/p - W/p),
-        // so the tree (zero-padded, CFR-6) needs next_pow2 of that.  CTAs per unit: the widest cluster
-        // (<= 4) with one CTA per SM and >= 256 leaves per CTA, or one 1024-thread CTA when there are
-        // many units; leaves per thread fill the tree
-        const int n_off_max = std::max(D.n_sink, D.max_ctx / D.p - D.n_win);
-        int P2 = 256;
-        while (P2 < n_off_max) P2 <<= 1;
-        // (<= 4: at c3 4- and 8-CTA clusters measure the same, 44.6 / 44.4 us per layer; the smaller
-        // cluster leaves the attention's clusters more room.)  The tree is sized for max_ctx: a handle
-        // whose page count crosses a power of two runs the doubled tree from its first step (c3 with
-        // max_ctx just above 4096 pages: select 35-41 us instead of 22)
-        int nc = 4;
-        while (nc > 1 && (D.U * nc > sms || nc * 256 > P2)) nc >>= 1;
-        // many units (<= 2 CTAs each would fit): one wide 1024-thread CTA per unit instead
-        // (A/B on B200 at c2: 42.3 us/layer vs 50.3 with 2-CTA clusters of 256 threads)
-        if (nc <= 2 && P2 >= 1024 && P2 / 1024 <= 8) nc = 1;
-        const char* ne = getenv("FREEKV_SELECT_NC");  // A/B: force the cluster width (1, 2, 4, 8)
-        if (ne && (atoi(ne) == 1 || atoi(ne) == 2 || atoi(ne) == 4 || atoi(ne) == 8)) nc = atoi(ne);
-        int lpt = std::max(1, P2 / (nc * 256));
-        if (nc > 1 && lpt > 4) {  // cluster instances are built for <= 4 leaves per thread
-            nc = 1;
-            lpt = P2 / 256;
-        }
-        if (lpt > 32) {
+        // the select's instance is chosen per launch for the tree the current context needs
+        // (select_config); here only the largest one (max_ctx) is validated
+        const int P2 = tree_leaves(D, D.max_ctx);
+        SelCfg sc;
+        if (!select_config(D, sms, P2, &sc)) {
             delete h;
             return fail(FREEKV_EUNSUPPORTED, "max_ctx_tokens / page_size > 8192 pages");
         }
-        h->sel_nc = nc;
-        h->sel_lpt = lpt;
-        // one 1024-thread CTA per unit when there are enough units to fill the GPU with clusters
-        // of one (A/B on B200: the wide CTA's short per-thread chains beat both the 256-thread CTA
-        // and a 2-CTA cluster at c2); FREEKV_SELECT_NT=256|1024 overrides
-        const char* nte = getenv("FREEKV_SELECT_NT");
-        int nt = (nc == 1 && P2 >= 1024 && P2 / 1024 <= 8) ? 1024 : 256;
-        if (nte && (atoi(nte) == 256 || atoi(nte) == 512 || atoi(nte) == 1024)) nt = atoi(nte);
-        if (nt > 256 && (nc != 1 || P2 < nt || P2 / nt > 8)) nt = 256;
-        if (nt > 256) h->sel_lpt = P2 / nt;
-        h->sel_nt = nt;
+        h->sms = sms;
         // speculative step: the corrected units' select (few units, critical path) as wide as the tree
         // allows (<= 8 CTAs, >= 256 leaves each); the side chain's select one CTA per unit (clusters
         // would constrain the placement of the attention's clusters it runs beside)
@@ -1071,6 +1095,21 @@ freekv_status freekv_step_graph_capture_cycle(freekv_handle* h, int32_t n_virtua
     if (n_virtual < h->cfg.n_layers) return fail(FREEKV_EINVAL, "n_virtual < n_layers");
     if (n_virtual != h->cfg.n_layers && (!h->one_graph || h->spec))
         return fail(FREEKV_EUNSUPPORTED, "layer cycling needs the serial direct-mode step");
+    {
+        // the select tree of the graph: the smallest covering the first replay's contexts; the
+        // graph is re-captured (freekv_step_graph_launch) once a context outgrows it
+        const int tok = (n_virtual + h->cfg.n_layers - 1) / h->cfg.n_layers;
+        int cmax = 0;
+        for (int l = 0; l < h->cfg.n_layers; ++l) cmax = std::max(cmax, h->ctx_host[l]);
+        h->graph_p2 = tree_leaves(h->D, std::min(h->D.max_ctx, cmax + tok));
+        h->graph_ctx_limit = (h->graph_p2 + h->D.n_win + 1) * h->D.p - 1;
+        h->cap.n_virtual = n_virtual;
+        h->cap.profile = profile;
+        h->cap.q = q_all;
+        h->cap.k = k_all;
+        h->cap.v = v_all;
+        h->cap.out = out_all;
+    }
     if (!q_all || !k_all || !v_all || !out_all) return fail(FREEKV_EINVAL, "NULL buffer");
     if (h->prof) return fail(FREEKV_ESTATE, "capture while profiling");
     h->no_bg_recall = env_on("FREEKV_DEBUG_NO_RECALL");
@@ -1177,6 +1216,13 @@ freekv_status freekv_step_graph_launch(freekv_handle* h) {
     const auto tok = [&](int l) { return l < (int)h->graph_tokens.size() ? h->graph_tokens[l] : 1; };
     for (int l = 0; l < h->cfg.n_layers; ++l)
         if (h->ctx_host[l] + tok(l) > h->D.max_ctx) return fail(FREEKV_ERANGE, "context would exceed max_ctx_tokens");
+    for (int l = 0; l < h->cfg.n_layers; ++l)
+        if (h->ctx_host[l] + tok(l) > h->graph_ctx_limit) {  // the select tree must grow: capture again
+            const auto c = h->cap;
+            freekv_status st = freekv_step_graph_capture_cycle(h, c.n_virtual, c.q, c.k, c.v, c.out, c.profile);
+            if (st != FREEKV_OK) return st;
+            break;
+        }
     FKV_CUDA(cudaGraphLaunch(h->g_compute, h->cs));
     if (h->g_recall) FKV_CUDA(cudaGraphLaunch(h->g_recall, h->rs));
     for (int l = 0; l < h->cfg.n_layers; ++l) {

@@ -646,3 +646,50 @@ def test_parity_score_cta_warps(warps, monkeypatch):
     monkeypatch.setenv("FREEKV_SCORE_WARPS", warps)
     run_parity(G=4, n_kv=2, batch=2, page=32, L0=40000, steps=3, n_layers=1)
     run_parity(G=7, n_kv=1, batch=2, page=32, L0=3000, steps=3, n_layers=1)
+
+
+def test_select_tree_grows_across_power_of_two():
+    """The select's CFR-6 tree is the smallest power of two covering the current candidates
+    (chosen per launch; the step graph is re-captured when a context outgrows its tree): contexts
+    crossing n_off = 256 pages, eagerly vs the oracle and through the step graph vs eager calls."""
+    _need_gpu()
+    import paper_2505_13109_b200 as P
+    L0 = (256 + 2) * 32 - 3          # n_off = ctx/p - W/p crosses 256 after 3 tokens
+    run_parity(G=4, n_kv=2, batch=2, page=32, L0=L0, steps=8, n_layers=1)
+    nb, n_kv, G, d, p, steps, n_layers = 2, 2, 4, 128, 32, 8, 2
+    n_qo = G * n_kv
+    mk = lambda: P.FreeKV(P.FreeKVConfig(n_layers=n_layers, batch=nb, n_qo=n_qo, n_kv=n_kv, budget_tokens=256,
+                                         sink_tokens=64, window_tokens=64, max_ctx_tokens=L0 + 4000))
+    a, b = mk(), mk()
+    dev = a.device
+    seed = 93
+    for layer in range(n_layers):
+        k, v = synth.gen_prefill(nb, n_kv, d, p, L0, 2, a.K, seed, layer, device=dev)
+        torch.cuda.synchronize()
+        a.append_kv(layer, k, v)
+        b.append_kv(layer, k, v)
+    a.synchronize()
+    b.synchronize()
+    qps = [synth.QueryProcess(nb, n_qo, n_kv, d, seed, l, device=dev, event_rate=0.3) for l in range(n_layers)]
+    qb = torch.empty(n_layers, nb, n_qo, d, dtype=torch.bfloat16, device=dev)
+    kb = torch.empty(n_layers, nb, 1, n_kv, d, dtype=torch.bfloat16, device=dev)
+    vb = torch.empty_like(kb)
+    ob = torch.empty(n_layers, nb, n_qo, d, dtype=torch.float32, device=dev)
+    b.step_graph_capture(qb, kb, vb, ob)
+    oa = torch.empty(nb, n_qo, d, dtype=torch.float32, device=dev)
+    for i in range(steps):
+        for l in range(n_layers):
+            q, _ = qps[l].next()
+            kn, vn = synth.gen_decode_kv(nb, n_kv, d, p, L0 + i, seed, l, device=dev)
+            qb[l], kb[l], vb[l] = q, kn, vn
+        torch.cuda.synchronize()
+        b.step_graph_launch()
+        b.synchronize()
+        for l in range(n_layers):
+            a.decode_step(l, qb[l], kb[l], vb[l], oa)
+            a.synchronize()
+            sa, sb = a.get_selection(l), b.get_selection(l)
+            assert np.array_equal(sa["pages"], sb["pages"]) and np.array_equal(sa["flags"], sb["flags"]), (i, l)
+            assert torch.equal(oa, ob[l]), (i, l)
+    a.close()
+    b.close()
