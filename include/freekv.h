@@ -174,6 +174,10 @@ freekv_status freekv_decode_step(freekv_handle* h, int32_t layer, const void* q,
  * classes to bracket -- fewer event nodes disturb the step less. */
 freekv_status freekv_step_graph_capture(freekv_handle* h, const void* q_all, const void* k_all,
                                         const void* v_all, float* out_all, int32_t profile);
+/* Replay the captured step on the compute stream (each layer appends one token; with layer
+ * cycling n_virtual / n_layers tokens).  The select's CFR-6 tree in the graph is the smallest
+ * covering the contexts at capture; a replay whose contexts outgrow it first re-captures the
+ * graph with the same buffers (once per power of two of pages).  ERANGE past max_ctx_tokens. */
 freekv_status freekv_step_graph_launch(freekv_handle* h);
 /* The same with n_virtual >= n_layers virtual layers: virtual layer v runs layer v % n_layers
  * with q_all / k_all / v_all / out_all slices v (buffers sized for n_virtual) -- L_inst
