@@ -249,7 +249,8 @@ int32_t freekv_abi_version(void);
  * bytes, host) and the caller broadcasts it (e.g. over torch.distributed).
  * freekv_comm_init: every rank builds the communicator on its handle's device
  * (blocking, collective over n_ranks).  freekv_set_gather_output: device fp32
- * [n_layers][n_ranks][nb][n_qo][d] (caller-owned, NULL to stop): every
+ * [n_layers (n_virtual for a cycled step graph)][n_ranks][nb][n_qo][d]
+ * (caller-owned, NULL to stop): every
  * decode step of layer l then ends with an all-gather of `out` into slice l
  * on the compute stream -- a node of the step graph when captured.  Both
  * invalidate a captured step graph (capture again).  ENCCL on NCCL errors. */

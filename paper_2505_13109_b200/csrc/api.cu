@@ -587,11 +587,12 @@ freekv_status do_layer_step_core(freekv_handle* h, int layer, const void* q, con
 // One layer of the decode step, then (multi-GPU) the per-layer all-gather of the head outputs of
 // every rank on the compute stream -- inside the step graph when capturing.
 freekv_status do_layer_step(freekv_handle* h, int layer, const void* q, const void* k_new, const void* v_new,
-                            float* out) {
+                            float* out, int gather_slot = -1) {
     freekv_status st = do_layer_step_core(h, layer, q, k_new, v_new, out);
     if (st != FREEKV_OK || !h->comm || !h->gather_all) return st;
     const size_t count = (size_t)h->D.nb * h->D.n_qo * h->D.d;
-    float* dst = h->gather_all + (size_t)layer * h->n_ranks * count;
+    // slice of the gathered output: the layer, or the virtual layer of a cycled step graph
+    float* dst = h->gather_all + (size_t)(gather_slot >= 0 ? gather_slot : layer) * h->n_ranks * count;
     const ncclResult_t r = ncclAllGather(out, dst, count, ncclFloat, h->comm, h->cs);
     if (r != ncclSuccess) return fail(FREEKV_ENCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));
     return FREEKV_OK;
@@ -1142,7 +1143,7 @@ freekv_status freekv_step_graph_capture_cycle(freekv_handle* h, int32_t n_virtua
         const uint8_t* q = (const uint8_t*)q_all + q_stride * vl;
         const uint8_t* k = (const uint8_t*)k_all + kv_stride * vl;
         const uint8_t* v = (const uint8_t*)v_all + kv_stride * vl;
-        st = do_layer_step(h, l, q, k, v, out_all + o_stride * vl);
+        st = do_layer_step(h, l, q, k, v, out_all + o_stride * vl, vl);
     }
     if (h->one_graph) {  // join every layer's recall branch (and the corrected units' chain)
         for (int l = 0; l < h->cfg.n_layers && e == cudaSuccess && st == FREEKV_OK; ++l)
