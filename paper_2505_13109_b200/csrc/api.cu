@@ -822,6 +822,12 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         const char* sw = getenv("FREEKV_SCORE_WARPS");
         const int n_off_cap = std::max(h->D.n_sink, h->D.max_ctx / h->D.p - h->D.n_win);
         h->D.score_warps = sw ? (atoi(sw) == 8 ? 8 : 4) : ((h->D.U >= 64 && n_off_cap <= 2048) ? 8 : 4);
+        // 4-warp score CTAs: an 8-deep stage ring when the whole scoring grid is resident at once
+        // (c3: 128 CTAs, 40.5 vs 44.1 us/layer), else 4 (c5's 1024 CTAs: 146 vs 115.5 -- 128 KiB
+        // CTAs leave fewer resident); FREEKV_SCORE_STAGES=4|6|8
+        const char* ss = getenv("FREEKV_SCORE_STAGES");
+        const long long sc_ctas = (long long)h->D.U * ((n_off_cap + 511) / 512);
+        h->D.score_stages = ss ? atoi(ss) : (sc_ctas <= h->sms ? 8 : 4);
     }
     {
         const char* sr = getenv("FREEKV_SERIAL_RECALL");

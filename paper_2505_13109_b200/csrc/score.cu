@@ -25,12 +25,11 @@
 namespace fkv {
 
 constexpr int kScWarps = FKV_SC_WARPS;  // warps per CTA of the speculative step's parts 0/1
-constexpr int kScStages = 4;                                   // ring depth per warp
-template <int PPT, int W> struct ScGeom {                       // PPT pages per thread, W warps per CTA
+template <int PPT, int W, int S = 4> struct ScGeom {            // PPT pages/thread, W warps/CTA, S stages/warp
     static constexpr int WarpPages = 32 * PPT;
     static constexpr int CtaPages = W * WarpPages;              // a power of two
     static constexpr int StageBytes = 2 * WarpPages * 16;       // {min, max} x pages x 8 channels
-    static constexpr int Smem = W * kScStages * StageBytes;
+    static constexpr int Smem = W * S * StageBytes;
 };
 static_assert(ScGeom<4, kScWarps>::CtaPages == kScoreCtaPages, "score CTA page count (the select waits per item)");
 static_assert(ScGeom<1, kScWarps>::CtaPages == kScoreCtaPagesFast, "score CTA page count (the select waits per item)");
@@ -143,14 +142,14 @@ cudaError_t launch_pre(const FkvDims& D, const FkvLayer& L, const uint16_t* q, c
 // (CP = 512 for PPT = 4, 128 for PPT = 1).  part >= 0 (speculative step): the unit of CTA i is
 // part_unit(i / items_per_unit) and every CTA counts itself done in L.score_done[u] (release),
 // which the select kernel acquires per unit instead of waiting for the whole grid.
-template <int G, int PPT, int W>
+template <int G, int PPT, int W, int S>
 __global__ void __launch_bounds__(W * 32) fkv_score_kernel(FkvDims D, FkvLayer L, const uint16_t* __restrict__ q,
                                                                int items_per_unit, int part,
                                                                const uint16_t* __restrict__ k_new,
                                                                const uint16_t* __restrict__ v_new) {
     constexpr int GP = (G + 1) / 2;  // head pairs
     constexpr int kScPPT = PPT, kScWarpPages = ScGeom<PPT, W>::WarpPages, kScCtaPages = ScGeom<PPT, W>::CtaPages;
-    constexpr int kScStageBytes = ScGeom<PPT, W>::StageBytes;
+    constexpr int kScStageBytes = ScGeom<PPT, W>::StageBytes, kScStages = S;  // ring depth per warp
     const int ordered = part >= 0;
     extern __shared__ __align__(128) uint8_t s_raw[];
     __shared__ __align__(16) float4 s_q[kHeadDim][GP];  // {q+_h, q+_h', q-_h, q-_h'} of pair (h, h') at c
@@ -320,17 +319,17 @@ __global__ void __launch_bounds__(W * 32) fkv_score_kernel(FkvDims D, FkvLayer L
     if (threadIdx.x == 0) trace_stamp(trace, 0, item, 2);
 }
 
-template <int G, int PPT, int W>
+template <int G, int PPT, int W, int S = 4>
 static cudaError_t launch_score_gp(const FkvDims& D, const FkvLayer& L, const uint16_t* q, int max_n_off, int part,
                                    bool pdl, int prio, cudaStream_t s, const uint16_t* k_new, const uint16_t* v_new) {
     constexpr int CP = ScGeom<PPT, W>::CtaPages;
-    const int SM = std::max<int>(ScGeom<PPT, W>::Smem, (int)(page_elems(D) * sizeof(uint16_t)));
+    const int SM = std::max<int>(ScGeom<PPT, W, S>::Smem, (int)(page_elems(D) * sizeof(uint16_t)));
     const int ipu = std::max(0, (max_n_off + CP - 1) / CP);
     if (ipu == 0 && part != -2) return cudaSuccess;
-    cudaError_t e = func_smem((const void*)fkv_score_kernel<G, PPT, W>, SM);
+    cudaError_t e = func_smem((const void*)fkv_score_kernel<G, PPT, W, S>, SM);
     if (e != cudaSuccess) return e;
     const int grid = (part == -2 ? D.U : 0) + D.U * ipu;
-    return launch_ex(fkv_score_kernel<G, PPT, W>, dim3(grid), dim3(W * 32), SM, s, pdl, prio, D, L, q,
+    return launch_ex(fkv_score_kernel<G, PPT, W, S>, dim3(grid), dim3(W * 32), SM, s, pdl, prio, D, L, q,
                      std::max(ipu, 1), part, k_new, v_new);
 }
 
@@ -340,6 +339,10 @@ static cudaError_t launch_score_g(const FkvDims& D, const FkvLayer& L, const uin
     if (part == 0) return launch_score_gp<G, 1, kScWarps>(D, L, q, max_n_off, part, pdl, prio, s, k_new, v_new);
     if (part < 0 && D.score_warps == 8)
         return launch_score_gp<G, 4, 8>(D, L, q, max_n_off, part, pdl, prio, s, k_new, v_new);
+    if (part < 0 && D.score_stages == 6)
+        return launch_score_gp<G, 4, kScWarps, 6>(D, L, q, max_n_off, part, pdl, prio, s, k_new, v_new);
+    if (part < 0 && D.score_stages == 8)
+        return launch_score_gp<G, 4, kScWarps, 8>(D, L, q, max_n_off, part, pdl, prio, s, k_new, v_new);
     return launch_score_gp<G, 4, kScWarps>(D, L, q, max_n_off, part, pdl, prio, s, k_new, v_new);
 }
 

@@ -693,3 +693,13 @@ def test_select_tree_grows_across_power_of_two():
             assert torch.equal(oa, ob[l]), (i, l)
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("stages", ["4", "6", "8"])
+def test_parity_score_ring_depth(stages, monkeypatch):
+    """4-warp score CTAs with a 4-, 6- or 8-deep stage ring per warp (8 is the default when the
+    scoring grid fits the GPU at once): bit-identical selections (odd and even G)."""
+    monkeypatch.setenv("FREEKV_SCORE_WARPS", "4")
+    monkeypatch.setenv("FREEKV_SCORE_STAGES", stages)
+    run_parity(G=7, n_kv=1, batch=2, page=32, L0=9000, steps=3, n_layers=1)
+    run_parity(G=4, n_kv=2, batch=1, page=32, L0=3000, steps=3, n_layers=1)
