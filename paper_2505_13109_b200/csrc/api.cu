@@ -798,6 +798,10 @@ freekv_status freekv_init(const freekv_config* cfg, const freekv_buffers* bufs, 
         const char* ce = getenv("FREEKV_ATTN_CLUSTER");  // A/B: 1, 2, 4, 8 or 16 CTAs per unit
         if (ce && (atoi(ce) == 1 || atoi(ce) == 2 || atoi(ce) == 4 || atoi(ce) == 8 || atoi(ce) == 16)) c = atoi(ce);
         h->attn_cluster = c;
+        // slab ring: 2 stages when the attention grid is one CTA per SM or less (its smaller
+        // footprint leaves room for the next layer's score CTAs: c3 39.6 vs 40.5 us/layer), else 3
+        // (two CTAs per SM: c2 40.0 vs 41.5); FREEKV_ATTN_STAGES overrides
+        h->D.attn_nst = getenv("FREEKV_ATTN_STAGES") ? 0 : (D.U * c <= sms ? 2 : 3);
     }
     h->X.trace = nullptr;
     {

@@ -437,7 +437,7 @@ static cudaError_t launch_cluster_c(const FkvDims& D, const FkvLayer& L, const F
 cudaError_t launch_attn_cluster(const FkvDims& D, const FkvLayer& L, const FkvScratch& X, const uint16_t* q,
                                 float* out, const CUtensorMap& tmap, const CUtensorMap& tmap_h, int mode, int c,
                                 bool pdl, int prio, cudaStream_t s, int pending) {
-    const int nst = attn_stages();
+    const int nst = D.attn_nst ? D.attn_nst : attn_stages();
 #define FKV_CL(NS)                                                                                         \
     do {                                                                                                   \
         if (c == 1) return launch_cluster_c<NS, 1>(D, L, X, q, out, tmap, tmap_h, mode, pdl, prio, s, pending); \

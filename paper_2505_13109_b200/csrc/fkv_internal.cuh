@@ -37,6 +37,7 @@ struct FkvDims {
     int attn_early;   // serial step: uncorrected units attend before the wait for the select (FREEKV_ATTN_EARLY)
     int score_warps;  // warps per score CTA (parts -1/-2): 4 or 8 (1024 pages per CTA)
     int score_stages; // ring depth per warp of the 4-warp score CTAs (parts -1/-2): 4, 6 or 8
+    int attn_nst;     // slab stages per warp of the clustered attention (2 or 3; 0 = env / default 3)
     int pool;         // FREEKV_POOL_* group pooling of the selection (f3); 0 = MeanS
     int corr_pool;    // 0 = mean of the cosines, 1 = corrected when the least similar head is below tau
     float tau;
