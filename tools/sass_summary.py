@@ -16,12 +16,12 @@ LIB = os.path.join(ROOT, "paper_2505_13109_b200", "libfreekv.so")
 # select LPT 1 / GM 4 / one 1024-thread CTA (c2) and LPT 4 / GM 8 / 4-CTA cluster (c3); attention
 # 3 stages x cluster 4 (c2) / 8 (c3))
 WANT = [
-    ("score c2", r"fkv_score_kernelILi4ELi4E"),
-    ("score c3", r"fkv_score_kernelILi7ELi4E"),
+    ("score c2", r"fkv_score_kernelILi4ELi4ELi8ELi4E"),
+    ("score c3", r"fkv_score_kernelILi7ELi4ELi4ELi8E"),
     ("select c2", r"fkv_select_kernelILi1ELi4ELi1ELi1024E"),
     ("select c3", r"fkv_select_kernelILi4ELi8ELi4ELi256E"),
     ("attention c2", r"fkv_attn_cluster_kernelILi3ELi4E"),
-    ("attention c3", r"fkv_attn_cluster_kernelILi3ELi8E"),
+    ("attention c3", r"fkv_attn_cluster_kernelILi2ELi8E"),
     ("recall", r"fkv_recall_kernel"),
     ("append", r"fkv_append_kernel"),
 ]
