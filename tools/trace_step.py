@@ -7,7 +7,8 @@ import numpy as np, torch
 import paper_2505_13109_b200 as P
 import synth
 
-nb, nq, nk, d, p, ctx = 8, 32, 8, 128, 32, 32768
+CFG = {"c2": (8, 32, 8, 128, 32, 32768), "c3": (4, 28, 4, 128, 32, 131072)}
+nb, nq, nk, d, p, ctx = CFG[os.environ.get("FKV_TRACE_CFG", "c2")]
 L = int(os.environ.get("FKV_TRACE_LAYERS", "2"))
 cfg = P.FreeKVConfig(n_layers=L, batch=nb, n_qo=nq, n_kv=nk, max_ctx_tokens=ctx + 64)
 fkv = P.FreeKV(cfg)
