@@ -87,6 +87,9 @@ __global__ void __launch_bounds__(NT, NT == kSelThreads && LPT * GM <= 16 ? 4 : 
     if constexpr (NC > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // every CTA started
     __syncthreads();
     if (tid == 0) trace_stamp(X.trace, 1, blockIdx.x, 6);
+    // the flag decided before this kernel (score grid / pre kernel, complete here): its load
+    // latency overlaps the ranking instead of sitting between the ranking and finish_unit
+    const int flag_pre = (flag_src != 0 && tid == 0) ? (int)__ldcg(L.flags + u) : 0;
     int cnt;
     if (rank_all) {
         if (!leader) return;
@@ -125,7 +128,7 @@ __global__ void __launch_bounds__(NT, NT == kSelThreads && LPT * GM <= 16 ? 4 : 
             L.flags[u] = (uint8_t)flag;
             L.cbar[u] = pooled;
         } else {
-            flag = __ldcg(L.flags + u);
+            flag = flag_pre;
         }
         U.flag = flag;
         if (corrected_out) corrected_out[u] = (uint8_t)flag;
