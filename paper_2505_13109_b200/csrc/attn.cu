@@ -306,6 +306,11 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 3)
     constexpr int kQv = (kMaxG * (kHeadDim / 4) + kAttnWarpsPerCta * 32 - 1) / (kAttnWarpsPerCta * 32);
     uint2 qv[kQv];
     const int b = u / D.n_kv, m = u % D.n_kv;
+    // ... and the leader's commit inputs (the select's pending selection): an early unit waits
+    // for the select here, so these loads overlap the merges below instead of following them
+    const bool commit = mode != 3 && (mode != 1 || flag);
+    constexpr int kPend = (256 + kAttnWarpsPerCta * 32 - 1) / (kAttnWarpsPerCta * 32);  // K <= 256
+    int pend_pg[kPend], pend_sl[kPend], pend_fr = 0, pend_ct = 0;
     if (crank == 0) {
 #pragma unroll
         for (int i = 0; i < kQv; ++i) {
@@ -313,6 +318,21 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 3)
             if (e < G * (kHeadDim / 4)) {
                 const size_t row = (size_t)b * D.n_qo + m * G + e / (kHeadDim / 4);
                 qv[i] = reinterpret_cast<const uint2*>(q + row * kHeadDim)[e % (kHeadDim / 4)];
+            }
+        }
+        if (early) pdl_wait();  // q_prev is read by this step's score grid; R by the select
+        if (commit) {
+#pragma unroll
+            for (int i = 0; i < kPend; ++i) {
+                const int a = tid + i * (int)blockDim.x;
+                if (a < D.K) {
+                    pend_pg[i] = __ldcg(L.pend_pages + (size_t)u * D.K + a);
+                    pend_sl[i] = __ldcg(L.pend_slot + (size_t)u * D.K + a);
+                }
+            }
+            if (tid == 0) {
+                pend_fr = __ldcg(L.pend_front + u);
+                pend_ct = __ldcg(L.pend_cnt + u);
             }
         }
     }
@@ -361,8 +381,7 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 3)
             reinterpret_cast<float4*>(out + row * kHeadDim)[e % (kHeadDim / 4)] = o4;
         }
         // q_prev := q_i -- after the select (and so the score grid, whose correction check reads
-        // q_prev) is complete when this unit attended early
-        if (early) pdl_wait();
+        // q_prev) is complete when this unit attended early (waited above)
 #pragma unroll
         for (int qi = 0; qi < kQv; ++qi) {
             const int e = tid + qi * (int)blockDim.x;
@@ -372,14 +391,18 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 3)
         }
         // commit R := S_i: every unit in modes 0 and 2; in mode 1 the corrected units (the
         // others' S_i is committed by the next step's pre kernel, after their background recall)
-        if (mode != 3 && (mode != 1 || flag)) {
-            for (int i = tid; i < D.K; i += blockDim.x) {
-                L.res_pages[(size_t)u * D.K + i] = __ldcg(L.pend_pages + (size_t)u * D.K + i);
-                L.res_slot[(size_t)u * D.K + i] = __ldcg(L.pend_slot + (size_t)u * D.K + i);
+        if (commit) {
+#pragma unroll
+            for (int i = 0; i < kPend; ++i) {
+                const int a = tid + i * (int)blockDim.x;
+                if (a < D.K) {
+                    L.res_pages[(size_t)u * D.K + a] = pend_pg[i];
+                    L.res_slot[(size_t)u * D.K + a] = pend_sl[i];
+                }
             }
             if (tid == 0) {
-                L.res_front[u] = __ldcg(L.pend_front + u);
-                L.res_cnt[u] = __ldcg(L.pend_cnt + u);
+                L.res_front[u] = pend_fr;
+                L.res_cnt[u] = pend_ct;
                 L.res_valid[u] = 1;
                 L.pend_valid[u] = 0;
                 X.ready[u] = 0;
